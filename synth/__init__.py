@@ -1,0 +1,34 @@
+"""Seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+Holds none of the method's arithmetic: keys come from numpy's PCG64 stream
+(not SplitMix64, which is the method's own mixer), de-duplicated so every key
+set is a valid MPHF input.  Workload shape follows the paper's "random 128-bit
+integers as MHC" setup: uniform 64-bit keys, no structure or skew.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def keys(n: int, seed: int) -> np.ndarray:
+    """n distinct uniform uint64 keys, deterministic in (n, seed)."""
+    gen = np.random.Generator(np.random.PCG64(seed))
+    raw = gen.bit_generator.random_raw(n)
+    out = np.asarray(raw, dtype=np.uint64)
+    while True:
+        _, first = np.unique(out, return_index=True)
+        if len(first) == len(out):
+            return out
+        first.sort()
+        out = out[first]
+        extra = np.asarray(gen.bit_generator.random_raw(n - len(out)), dtype=np.uint64)
+        out = np.concatenate([out, extra])
+
+
+# Workload recipes (BASELINE.json configs); key seeds follow BASELINE.md section 4.
+CONFIGS = {
+    "C1": dict(n=10_000, leaf=8, bucket=100, seed=1),
+    "C2": dict(n=5_000_000, leaf=8, bucket=100, seed=2),
+    "C3": dict(n=5_000_000, leaf=16, bucket=2000, seed=3),
+    "C5": dict(n=100_000_000, leaf=12, bucket=1000, seed=5),
+}
