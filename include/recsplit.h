@@ -1,0 +1,170 @@
+/*
+ * recsplit.h -- C ABI of the B200-native RecSplit MPHF builder
+ * (arXiv 2212.09562: RecSplit with rotation fitting; GPU construction).
+ *
+ * Citation keys: P:n = line n of the paper text.
+ * lists every reading (R1..R14) taken where the paper is silent.
+ *
+ * Problem statement: a minimal perfect hash function maps a set S of
+ * n keys bijectively onto [0, n); evaluating it on a key outside S returns an
+ * arbitrary value in [0, n).  Construction: keys -> buckets of expected
+ * size b -> per bucket a splitting tree whose inner nodes store the smallest seed
+ * that splits the keys into the fanout-prescribed part sizes and whose
+ * leaves store the smallest (seed, rotation) value found by rotation fitting
+ * (minimal-value rule P:297-300) -- or the smallest brute-force seed
+ * when rotation fitting is off.  Values are Golomb-Rice coded per tree
+ * in preorder with a trend-subtracted Elias-Fano bucket index.
+ *
+ * Every search step runs in hand-written sm_100a CUDA kernels; there is NO CPU
+ * fallback: without a usable CUDA device the build calls return RECSPLIT_E_CUDA.
+ *
+ * Conventions
+ *  - All functions return RECSPLIT_OK (0) or a negative error code; on error
+ *    recsplit_last_error() returns a thread-local message describing the failure.
+ *  - Output buffers (recsplit_bytes) are allocated by the library with malloc and
+ *    owned by the caller, who releases them with recsplit_free().  On any error
+ *    *out = {NULL, 0} and nothing leaks.
+ *  - Input pointers are borrowed for the duration of the call and never retained.
+ *  - The output bytes are a pure function of (key set, leaf_size, bucket_size,
+ *    rotation_fitting, global_seed): independent of key order, device, shard
+ *    count and kernel schedule.
+ *  - Builds are serialised per process (an internal mutex); queries are reentrant.
+ */
+#ifndef RECSPLIT_H
+#define RECSPLIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define RECSPLIT_API __attribute__((visibility("default")))
+#else
+#define RECSPLIT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    RECSPLIT_OK = 0,
+    RECSPLIT_E_INVALID = -1,   /* bad argument: n == 0, n >= 2^32, leaf_size outside [2,24],
+                                  bucket_size == 0, a bucket larger than the supported
+                                  maximum (recsplit_max_bucket_keys()), NULL pointer */
+    RECSPLIT_E_DUPLICATE = -2, /* two equal keys (detected before any search) */
+    RECSPLIT_E_NOMEM = -3,     /* host or device allocation failed */
+    RECSPLIT_E_CUDA = -4,      /* no usable CUDA device / kernel launch or runtime error */
+    RECSPLIT_E_FORMAT = -5,    /* corrupt, truncated or unsupported serialized MPHF */
+    RECSPLIT_E_SEED_CAP = -6   /* a node needed more than 2^40 trials (diagnostic) */
+};
+
+/* A library-allocated byte buffer; free with recsplit_free(). */
+typedef struct {
+    uint8_t *data;
+    size_t size;
+} recsplit_bytes;
+
+/* Options (NULL = defaults: rotation fitting on, global_seed 0, current device). */
+typedef struct {
+    uint32_t struct_size;      /* sizeof(recsplit_options) */
+    uint32_t rotation_fitting; /* 1: leaves by rotation fitting; 0: brute force */
+    uint64_t global_seed;      /* g of the master hash code (reading R2) */
+    int32_t device;            /* CUDA device ordinal; -1 = current device */
+    uint32_t virtual_shards;   /* >1: run the bucket-range sharded path with this many
+                                  shards on one device and stitch them (tests the multi-GPU
+                                  offset logic); 0/1 = unsharded */
+} recsplit_options;
+
+/* Per-build statistics (optional output). Times are device (CUDA event) seconds. */
+typedef struct {
+    double t_total;        /* whole recsplit_build* call, host wall clock */
+    double t_h2d;          /* host->device key copy (0 for the device-input entry point) */
+    double t_partition;    /* hash + bucket counting sort + per-bucket sort/dedupe */
+    double t_tree;         /* node-table expansion */
+    double t_search[4];    /* upper splits, lower level 2, lower level 1, leaves */
+    double t_reorder;      /* key redistribution after splits */
+    double t_encode;       /* Golomb-Rice + Elias-Fano + serialization */
+    double t_d2h;          /* device->host result copy */
+    uint64_t algo_evals[4];  /* algorithmic remix evaluations per class [upper,L2,L1,leaf]:
+                                sum over nodes of (trials up to and incl. the minimal one) x keys */
+    uint64_t nodes[4];       /* node counts per class */
+    uint64_t data_bits;      /* Golomb-Rice bits D */
+    uint64_t index_bits;     /* Elias-Fano lower+upper bits of both sequences */
+    uint32_t kernel_launches; /* CUDA kernels this library launched during the build */
+    uint32_t max_bucket;      /* largest bucket size */
+} recsplit_stats;
+
+/* Library version (format version is the header's u16 version = 1). */
+RECSPLIT_API int recsplit_version(void);
+
+/* Largest bucket (keys) the device path supports; larger buckets -> RECSPLIT_E_INVALID. */
+RECSPLIT_API uint32_t recsplit_max_bucket_keys(void);
+
+/*
+ * Build the MPHF of the n distinct 64-bit keys at `keys` (HOST memory, pageable or
+ * pinned) with leaf size l = leaf_size (P:110, 2..24) and expected bucket size
+ * b = bucket_size.  Rotation fitting on, global seed 0.  On success *out
+ * receives the serialized MPHF (format: DESIGN.md section 6).
+ */
+RECSPLIT_API int recsplit_build(const uint64_t *keys, size_t n, uint32_t leaf_size, uint32_t bucket_size,
+                   recsplit_bytes *out);
+
+/* As recsplit_build with options (nullable) and statistics (nullable). */
+RECSPLIT_API int recsplit_build_ex(const uint64_t *keys, size_t n, uint32_t leaf_size, uint32_t bucket_size,
+                      const recsplit_options *opt, recsplit_bytes *out, recsplit_stats *stats);
+
+/*
+ * As recsplit_build_ex, but `d_keys` is a DEVICE pointer (n x u64, on opt->device)
+ * and all work is ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ * The call returns after the serialized bytes are in host memory.
+ */
+RECSPLIT_API int recsplit_build_device(const uint64_t *d_keys, size_t n, uint32_t leaf_size,
+                          uint32_t bucket_size, const recsplit_options *opt, void *stream,
+                          recsplit_bytes *out, recsplit_stats *stats);
+
+/*
+ * Diagnostic build: additionally returns every stored node value (u64) in bucket
+ * order, each bucket's tree in preorder, as a malloc'ed array in *values
+ * (*n_values entries); free with recsplit_free_ptr().
+ */
+RECSPLIT_API int recsplit_build_values(const uint64_t *keys, size_t n, uint32_t leaf_size,
+                          uint32_t bucket_size, const recsplit_options *opt, recsplit_bytes *out,
+                          uint64_t **values, size_t *n_values);
+
+/* Evaluate the MPHF serialized at mphf[0..size) on one key (host).  For a key of
+ * the build set the result is its unique index in [0, n); otherwise some value in
+ * [0, n).  Corrupt blobs -> RECSPLIT_E_FORMAT. */
+RECSPLIT_API int recsplit_query(const uint8_t *mphf, size_t size, uint64_t key, uint64_t *out_index);
+
+/* Evaluate on n keys (host, multi-threaded); out has n entries. */
+RECSPLIT_API int recsplit_query_many(const uint8_t *mphf, size_t size, const uint64_t *keys, size_t n,
+                        uint64_t *out);
+
+/* bits/object of a serialized MPHF: (Golomb-Rice bits + Elias-Fano bits) / n,
+ * excluding the fixed header and word padding (reading R14). */
+RECSPLIT_API int recsplit_bits_per_key(const uint8_t *mphf, size_t size, double *out);
+
+/*
+ * Kernel-level entry points (parity tests; host pointers, copied internally).
+ * Leaves: node j has keys lo[off[j] .. off[j+1]) (1 <= size <= 24) with A/B bits
+ * isb[] (reading R7); out[j] = stored value (k*m + r, rotation_fitting=1;
+ * brute-force seed otherwise).  Splits: node j has keys lo[off[j]..off[j+1]), size
+ * s > leaf_size; out[j] = smallest seed giving the prescribed parts.
+ */
+RECSPLIT_API int recsplit_search_leaves(const uint64_t *lo, const uint8_t *isb, const uint32_t *off,
+                           uint32_t n_nodes, uint32_t rotation_fitting, uint64_t *out);
+RECSPLIT_API int recsplit_search_splits(const uint64_t *lo, const uint32_t *off, uint32_t n_nodes,
+                           uint32_t leaf_size, uint64_t *out);
+
+/* Library tables (parity tests): Golomb-Rice parameter tau of a node of size s
+ * (leaf if s <= leaf_size), computed by the library's own host code. */
+RECSPLIT_API int recsplit_tau(uint32_t leaf_size, uint32_t s, uint32_t rotation_fitting);
+
+RECSPLIT_API void recsplit_free(recsplit_bytes *b); /* NULL-safe; zeroes *b */
+RECSPLIT_API void recsplit_free_ptr(void *p);
+RECSPLIT_API const char *recsplit_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RECSPLIT_H */

@@ -1,0 +1,212 @@
+"""Thin Python binding of the B200-native RecSplit builder (``include/recsplit.h``).
+
+Argument marshalling only: every construction step runs in the CUDA kernels of
+``lib/librecsplit_b200.so``.  There is no CPU fallback -- if the library is
+missing or no CUDA device is usable, calls raise ``RecSplitError``.
+PyTorch is used only to pass device memory and streams (``build_device``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "librecsplit_b200.so")
+
+OK, E_INVALID, E_DUPLICATE, E_NOMEM, E_CUDA, E_FORMAT, E_SEED_CAP = 0, -1, -2, -3, -4, -5, -6
+
+# Every symbol include/recsplit.h declares.
+SYMBOLS = [
+    "recsplit_version", "recsplit_max_bucket_keys", "recsplit_build", "recsplit_build_ex",
+    "recsplit_build_device", "recsplit_build_values", "recsplit_query", "recsplit_query_many",
+    "recsplit_bits_per_key", "recsplit_search_leaves", "recsplit_search_splits", "recsplit_tau",
+    "recsplit_free", "recsplit_free_ptr", "recsplit_last_error",
+]
+
+
+class RecSplitError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"recsplit error {code}: {msg}")
+        self.code = code
+
+
+class Bytes(C.Structure):
+    _fields_ = [("data", C.POINTER(C.c_uint8)), ("size", C.c_size_t)]
+
+
+class Options(C.Structure):
+    _fields_ = [("struct_size", C.c_uint32), ("rotation_fitting", C.c_uint32),
+                ("global_seed", C.c_uint64), ("device", C.c_int32), ("virtual_shards", C.c_uint32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("t_total", C.c_double), ("t_h2d", C.c_double), ("t_partition", C.c_double),
+                ("t_tree", C.c_double), ("t_search", C.c_double * 4), ("t_reorder", C.c_double),
+                ("t_encode", C.c_double), ("t_d2h", C.c_double), ("algo_evals", C.c_uint64 * 4),
+                ("nodes", C.c_uint64 * 4), ("data_bits", C.c_uint64), ("index_bits", C.c_uint64),
+                ("kernel_launches", C.c_uint32), ("max_bucket", C.c_uint32)]
+
+    def as_dict(self) -> dict:
+        return {
+            "t_total": self.t_total, "t_h2d": self.t_h2d, "t_partition": self.t_partition,
+            "t_tree": self.t_tree, "t_search": list(self.t_search), "t_reorder": self.t_reorder,
+            "t_encode": self.t_encode, "t_d2h": self.t_d2h, "algo_evals": list(self.algo_evals),
+            "nodes": list(self.nodes), "data_bits": self.data_bits, "index_bits": self.index_bits,
+            "kernel_launches": self.kernel_launches, "max_bucket": self.max_bucket,
+        }
+
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RecSplitError(E_CUDA, f"{LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P64, P8, P32 = C.POINTER(C.c_uint64), C.POINTER(C.c_uint8), C.POINTER(C.c_uint32)
+        u32, u64, sz, i32 = C.c_uint32, C.c_uint64, C.c_size_t, C.c_int
+        L.recsplit_version.restype = i32
+        L.recsplit_max_bucket_keys.restype = u32
+        L.recsplit_build.argtypes = [P64, sz, u32, u32, C.POINTER(Bytes)]
+        L.recsplit_build_ex.argtypes = [P64, sz, u32, u32, C.POINTER(Options), C.POINTER(Bytes),
+                                        C.POINTER(Stats)]
+        L.recsplit_build_device.argtypes = [C.c_void_p, sz, u32, u32, C.POINTER(Options), C.c_void_p,
+                                            C.POINTER(Bytes), C.POINTER(Stats)]
+        L.recsplit_build_values.argtypes = [P64, sz, u32, u32, C.POINTER(Options), C.POINTER(Bytes),
+                                            C.POINTER(P64), C.POINTER(sz)]
+        L.recsplit_query.argtypes = [P8, sz, u64, P64]
+        L.recsplit_query_many.argtypes = [P8, sz, P64, sz, P64]
+        L.recsplit_bits_per_key.argtypes = [P8, sz, C.POINTER(C.c_double)]
+        L.recsplit_search_leaves.argtypes = [P64, P8, P32, u32, u32, P64]
+        L.recsplit_search_splits.argtypes = [P64, P32, u32, u32, P64]
+        L.recsplit_tau.argtypes = [u32, u32, u32]
+        L.recsplit_free.argtypes = [C.POINTER(Bytes)]
+        L.recsplit_free.restype = None
+        L.recsplit_free_ptr.argtypes = [C.c_void_p]
+        L.recsplit_free_ptr.restype = None
+        L.recsplit_last_error.restype = C.c_char_p
+        for name in ("recsplit_build", "recsplit_build_ex", "recsplit_build_device", "recsplit_build_values",
+                     "recsplit_query", "recsplit_query_many", "recsplit_bits_per_key",
+                     "recsplit_search_leaves", "recsplit_search_splits", "recsplit_tau"):
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc < 0:
+        raise RecSplitError(rc, lib().recsplit_last_error().decode())
+    return rc
+
+
+def _p64(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def _opts(rotation_fitting: bool, global_seed: int, device: int, virtual_shards: int):
+    return Options(C.sizeof(Options), int(bool(rotation_fitting)), global_seed, device, virtual_shards)
+
+
+def _take(b: Bytes) -> bytes:
+    out = C.string_at(b.data, b.size)
+    lib().recsplit_free(C.byref(b))
+    return out
+
+
+def build(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool = True, global_seed: int = 0,
+          device: int = -1, virtual_shards: int = 0, stats: bool = False):
+    """Build from host keys (uint64 array).  Returns bytes (and a stats dict)."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    b = Bytes()
+    st = Stats()
+    o = _opts(rotation_fitting, global_seed, device, virtual_shards)
+    _check(lib().recsplit_build_ex(_p64(keys), len(keys), leaf_size, bucket_size, C.byref(o), C.byref(b),
+                                   C.byref(st)))
+    blob = _take(b)
+    return (blob, st.as_dict()) if stats else blob
+
+
+def build_device(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
+                 global_seed: int = 0, stream=None, stats: bool = False):
+    """Build from a CUDA tensor of keys (int64/uint64 bit patterns) resident in HBM."""
+    import torch
+
+    if not keys_tensor.is_cuda or not keys_tensor.is_contiguous() or keys_tensor.element_size() != 8:
+        raise ValueError("keys_tensor must be a contiguous 8-byte CUDA tensor")
+    if stream is None:
+        stream = torch.cuda.current_stream(keys_tensor.device)
+    b = Bytes()
+    st = Stats()
+    o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, 0)
+    _check(lib().recsplit_build_device(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), leaf_size,
+                                       bucket_size, C.byref(o), C.c_void_p(stream.cuda_stream), C.byref(b),
+                                       C.byref(st)))
+    blob = _take(b)
+    return (blob, st.as_dict()) if stats else blob
+
+
+def build_values(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
+                 global_seed: int = 0, virtual_shards: int = 0):
+    """Diagnostic build: (bytes, node values in bucket order / preorder)."""
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    b = Bytes()
+    vp = C.POINTER(C.c_uint64)()
+    nv = C.c_size_t()
+    o = _opts(rotation_fitting, global_seed, -1, virtual_shards)
+    _check(lib().recsplit_build_values(_p64(keys), len(keys), leaf_size, bucket_size, C.byref(o), C.byref(b),
+                                       C.byref(vp), C.byref(nv)))
+    vals = np.ctypeslib.as_array(vp, shape=(nv.value,)).copy() if nv.value else np.zeros(0, np.uint64)
+    lib().recsplit_free_ptr(vp)
+    return _take(b), vals
+
+
+def query(blob: bytes, key: int) -> int:
+    out = C.c_uint64()
+    buf = np.frombuffer(blob, dtype=np.uint8)
+    _check(lib().recsplit_query(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob), key, C.byref(out)))
+    return out.value
+
+
+def query_many(blob: bytes, keys) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    out = np.zeros(len(keys), dtype=np.uint64)
+    buf = np.frombuffer(blob, dtype=np.uint8)
+    _check(lib().recsplit_query_many(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob), _p64(keys),
+                                     len(keys), _p64(out)))
+    return out
+
+
+def bits_per_key(blob: bytes) -> float:
+    out = C.c_double()
+    buf = np.frombuffer(blob, dtype=np.uint8)
+    _check(lib().recsplit_bits_per_key(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob), C.byref(out)))
+    return out.value
+
+
+def search_leaves(lo, isb, offsets, rotation_fitting: bool = True) -> np.ndarray:
+    lo = np.ascontiguousarray(lo, dtype=np.uint64)
+    isb = np.ascontiguousarray(isb, dtype=np.uint8)
+    off = np.ascontiguousarray(offsets, dtype=np.uint32)
+    out = np.zeros(max(len(off) - 1, 0), dtype=np.uint64)
+    _check(lib().recsplit_search_leaves(_p64(lo), isb.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                        off.ctypes.data_as(C.POINTER(C.c_uint32)), len(out),
+                                        int(rotation_fitting), _p64(out)))
+    return out
+
+
+def search_splits(lo, offsets, leaf_size: int) -> np.ndarray:
+    lo = np.ascontiguousarray(lo, dtype=np.uint64)
+    off = np.ascontiguousarray(offsets, dtype=np.uint32)
+    out = np.zeros(max(len(off) - 1, 0), dtype=np.uint64)
+    _check(lib().recsplit_search_splits(_p64(lo), off.ctypes.data_as(C.POINTER(C.c_uint32)), len(out),
+                                        leaf_size, _p64(out)))
+    return out
+
+
+def tau(leaf_size: int, s: int, rotation_fitting: bool = True) -> int:
+    return _check(lib().recsplit_tau(leaf_size, s, int(rotation_fitting)))

@@ -1,0 +1,489 @@
+// C ABI (include/recsplit.h): argument validation, error mapping, H2D/D2H for the
+// host-pointer entry points, and the host query.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/recsplit.h"
+#include "pipeline.h"
+#include "tables.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::mutex g_build_mu;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        g_err.clear();
+        return f();
+    } catch (const rs::Error& e) {
+        return fail(e.code, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(RECSPLIT_E_NOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(RECSPLIT_E_CUDA, e.what());
+    }
+}
+
+int check_args(size_t n, uint32_t leaf, uint32_t b) {
+    if (n == 0) return fail(RECSPLIT_E_INVALID, "n must be >= 1");
+    if (n >= (1ull << 32)) return fail(RECSPLIT_E_INVALID, "n must be < 2^32");
+    if (leaf < 2 || leaf > 24) return fail(RECSPLIT_E_INVALID, "leaf_size must be in [2, 24]");
+    if (b == 0) return fail(RECSPLIT_E_INVALID, "bucket_size must be >= 1");
+    return RECSPLIT_OK;
+}
+
+rs::BuildParams params_of(size_t n, uint32_t leaf, uint32_t b, const recsplit_options* opt) {
+    rs::BuildParams p;
+    p.n = n;
+    p.leaf = leaf;
+    p.bucket = b;
+    p.rf = true;
+    p.g = 0;
+    p.device = -1;
+    p.shards = 1;
+    if (opt) {
+        if (opt->struct_size < sizeof(recsplit_options)) throw rs::Error(RECSPLIT_E_INVALID, "bad options struct_size");
+        p.rf = opt->rotation_fitting != 0;
+        p.g = opt->global_seed;
+        p.device = opt->device;
+        p.shards = opt->virtual_shards ? opt->virtual_shards : 1;
+    }
+    return p;
+}
+
+void select_device(int dev) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        throw rs::Error(RECSPLIT_E_CUDA, std::string("no usable CUDA device: ") + cudaGetErrorString(e));
+    if (dev >= 0) {
+        if (dev >= count) throw rs::Error(RECSPLIT_E_INVALID, "device ordinal out of range");
+        e = cudaSetDevice(dev);
+        if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, cudaGetErrorString(e));
+    }
+}
+
+int emit(const rs::BuildOutput& o, recsplit_bytes* out) {
+    out->data = (uint8_t*)malloc(o.bytes.size());
+    if (!out->data) return fail(RECSPLIT_E_NOMEM, "host allocation failed");
+    memcpy(out->data, o.bytes.data(), o.bytes.size());
+    out->size = o.bytes.size();
+    return RECSPLIT_OK;
+}
+
+int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, const recsplit_options* opt,
+                    recsplit_bytes* out, recsplit_stats* stats, rs::BuildOutput* keep, bool want_values) {
+    if (!out) return fail(RECSPLIT_E_INVALID, "out is NULL");
+    out->data = nullptr;
+    out->size = 0;
+    if (!keys) return fail(RECSPLIT_E_INVALID, "keys is NULL");
+    int rc = check_args(n, leaf, b);
+    if (rc) return rc;
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        auto t0 = std::chrono::steady_clock::now();
+        rs::BuildParams p = params_of(n, leaf, b, opt);
+        select_device(p.device);
+        cudaStream_t st;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+            throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{st};
+        uint64_t* d_keys = nullptr;
+        cudaError_t e = cudaMallocAsync(&d_keys, n * 8, st);
+        if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_NOMEM, "device allocation of keys failed");
+        struct KeyGuard {
+            uint64_t* p;
+            cudaStream_t s;
+            ~KeyGuard() { cudaFreeAsync(p, s); }
+        } kg{d_keys, st};
+        cudaEvent_t a, z;
+        cudaEventCreate(&a);
+        cudaEventCreate(&z);
+        cudaEventRecord(a, st);
+        e = cudaMemcpyAsync(d_keys, keys, n * 8, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, cudaGetErrorString(e));
+        cudaEventRecord(z, st);
+        rs::BuildOutput local;
+        rs::BuildOutput& o = keep ? *keep : local;
+        rs::build_on_device(d_keys, p, st, want_values, o);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, z);
+        cudaEventDestroy(a);
+        cudaEventDestroy(z);
+        o.stats.t_h2d = ms * 1e-3;
+        o.stats.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (stats) *stats = o.stats;
+        return emit(o, out);
+    });
+}
+
+// ------------------------------------------------------------- host query --
+
+uint64_t rd64(const uint8_t* p) {
+    uint64_t x;
+    memcpy(&x, p, 8);
+    return x;
+}
+
+struct EFView {
+    uint32_t L;
+    uint64_t nlow, nup;
+    const uint8_t* low;
+    const uint8_t* up;
+};
+
+struct Parsed {
+    uint32_t leaf;
+    bool rf;
+    uint64_t g, n, B, D, dC, beta;
+    int64_t dR;
+    EFView ec, ep;
+    const uint8_t* data;
+    std::vector<uint64_t> C, P;  // decoded index
+    std::shared_ptr<const rs::Tables> T;
+};
+
+uint64_t word_at(const uint8_t* base, uint64_t i) { return rd64(base + 8 * i); }
+
+bool parse_ef(const uint8_t*& p, const uint8_t* end, EFView& e) {
+    if (end - p < 16) return false;
+    e.L = p[0];
+    if (e.L > 63) return false;
+    for (int i = 1; i < 8; ++i)
+        if (p[i]) return false;
+    e.nlow = rd64(p + 8);
+    p += 16;
+    if ((uint64_t)(end - p) / 8 < (e.nlow + 63) / 64) return false;
+    e.low = p;
+    p += 8 * ((e.nlow + 63) / 64);
+    if (end - p < 8) return false;
+    e.nup = rd64(p);
+    p += 8;
+    if ((uint64_t)(end - p) / 8 < (e.nup + 63) / 64) return false;
+    e.up = p;
+    p += 8 * ((e.nup + 63) / 64);
+    return true;
+}
+
+bool ef_decode(const EFView& e, uint64_t k, std::vector<uint64_t>& v) {
+    if (e.nlow != k * e.L) return false;
+    v.assign(k, 0);
+    uint64_t i = 0;
+    const uint64_t words = (e.nup + 63) / 64;
+    for (uint64_t w = 0; w < words && i < k; ++w) {
+        uint64_t x = word_at(e.up, w);
+        while (x && i < k) {
+            const uint64_t pos = w * 64 + __builtin_ctzll(x);
+            x &= x - 1;
+            if (pos >= e.nup) return false;
+            uint64_t lo = 0;
+            if (e.L) {
+                const uint64_t bp = i * e.L;
+                const uint64_t a = word_at(e.low, bp >> 6);
+                const uint64_t sh = bp & 63;
+                lo = a >> sh;
+                if (sh + e.L > 64) lo |= word_at(e.low, (bp >> 6) + 1) << (64 - sh);
+                lo &= (e.L == 64) ? ~0ull : ((1ull << e.L) - 1);
+            }
+            v[i] = ((pos - i) << e.L) | lo;
+            ++i;
+        }
+    }
+    return i == k;
+}
+
+int parse(const uint8_t* blob, size_t size, Parsed& M) {
+    if (!blob || size < 72 || memcmp(blob, "RSRF", 4) != 0) return fail(RECSPLIT_E_FORMAT, "bad magic / size");
+    uint16_t ver;
+    memcpy(&ver, blob + 4, 2);
+    if (ver != 1) return fail(RECSPLIT_E_FORMAT, "unsupported format version");
+    M.leaf = blob[6];
+    M.rf = blob[7] & 1;
+    if (M.leaf < 2 || M.leaf > 24) return fail(RECSPLIT_E_FORMAT, "bad leaf size");
+    M.g = rd64(blob + 16);
+    M.n = rd64(blob + 24);
+    M.B = rd64(blob + 32);
+    M.D = rd64(blob + 40);
+    M.dC = rd64(blob + 48);
+    M.beta = rd64(blob + 56);
+    M.dR = (int64_t)rd64(blob + 64);
+    if (M.n == 0 || M.B == 0 || M.B > M.n + 1) return fail(RECSPLIT_E_FORMAT, "bad n / B");
+    const uint8_t* p = blob + 72;
+    const uint8_t* end = blob + size;
+    if (!parse_ef(p, end, M.ec) || !parse_ef(p, end, M.ep)) return fail(RECSPLIT_E_FORMAT, "truncated index");
+    if ((uint64_t)(end - p) != 8 * ((M.D + 63) / 64)) return fail(RECSPLIT_E_FORMAT, "data length mismatch");
+    M.data = p;
+    std::vector<uint64_t> c, q;
+    if (!ef_decode(M.ec, M.B + 1, c) || !ef_decode(M.ep, M.B + 1, q)) return fail(RECSPLIT_E_FORMAT, "bad index");
+    M.C.resize(M.B + 1);
+    M.P.resize(M.B + 1);
+    uint64_t smax = 1;
+    for (uint64_t i = 0; i <= M.B; ++i) {
+        M.C[i] = c[i] + i * M.dC;
+        M.P[i] = (uint64_t)((int64_t)q[i] + (int64_t)i * M.dR) +
+                 (uint64_t)(((unsigned __int128)M.beta * M.C[i]) >> 20);
+        if (i) {
+            if (M.C[i] < M.C[i - 1] || M.P[i] < M.P[i - 1]) return fail(RECSPLIT_E_FORMAT, "index not monotone");
+            smax = std::max<uint64_t>(smax, M.C[i] - M.C[i - 1]);
+        }
+    }
+    if (M.C[0] != 0 || M.C[M.B] != M.n || M.P[0] != 0 || M.P[M.B] != M.D) return fail(RECSPLIT_E_FORMAT, "bad index ends");
+    if (smax > (1u << 20)) return fail(RECSPLIT_E_FORMAT, "bucket too large");
+    M.T = rs::get_tables(M.leaf, M.rf, (uint32_t)smax);
+    return RECSPLIT_OK;
+}
+
+inline int bit_at(const uint8_t* d, uint64_t pos) { return (int)((word_at(d, pos >> 6) >> (pos & 63)) & 1); }
+
+uint64_t remix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+inline uint32_t remap(uint64_t h, uint64_t r) { return (uint32_t)(((h >> 32) * r) >> 32); }
+
+// position just after the `cnt`-th one-bit at or after `pos` (cnt >= 1), word-wise
+bool skip_ones(const uint8_t* d, uint64_t D, uint64_t& pos, uint64_t cnt) {
+    while (cnt) {
+        if (pos >= D) return false;
+        uint64_t w = word_at(d, pos >> 6) >> (pos & 63);
+        const uint64_t avail = 64 - (pos & 63);
+        const uint64_t c = (uint64_t)__builtin_popcountll(w);
+        if (c < cnt) {
+            cnt -= c;
+            pos += avail;
+            continue;
+        }
+        // select the cnt-th one inside w
+        for (uint64_t k = 1; k < cnt; ++k) w &= w - 1;
+        pos += __builtin_ctzll(w) + 1;
+        cnt = 0;
+    }
+    return true;
+}
+
+int query_one(const Parsed& M, uint64_t key, uint64_t* out) {
+    const rs::Tables& T = *M.T;
+    const uint64_t hi = remix(key ^ M.g ^ 0x9E3779B97F4A7C15ULL);
+    const uint64_t lo = remix(key ^ M.g ^ 0xC2B2AE3D27D4EB4FULL);
+    const uint64_t i = remap(hi, M.B);
+    uint64_t s = M.C[i + 1] - M.C[i];
+    uint64_t offset = M.C[i];
+    if (s == 0) {
+        *out = 0;
+        return RECSPLIT_OK;
+    }
+    uint64_t fc = M.P[i], uc = M.P[i] + T.F[s];
+    for (;;) {
+        const uint32_t tau = T.tau[s];
+        const uint64_t u0 = uc;
+        if (!skip_ones(M.data, M.D, uc, 1)) return fail(RECSPLIT_E_FORMAT, "unary code out of range");
+        const uint64_t q = uc - u0 - 1;
+        uint64_t fixed = 0;
+        for (uint32_t t = 0; t < tau; ++t) fixed |= (uint64_t)bit_at(M.data, fc + t) << t;
+        fc += tau;
+        const uint64_t x = (q << tau) | fixed;
+        if (s <= M.leaf) {
+            const uint64_t m = s;
+            const uint64_t base = M.rf ? x - x % m : x;
+            uint64_t v = remap(remix(lo + base), m);
+            if (M.rf && (hi & 1)) v = (v + x % m) % m;  // B keys: rotation = addition mod m
+            *out = offset + v;
+            return RECSPLIT_OK;
+        }
+        uint32_t parts[64];
+        const int f = rs::split_parts(T.sh, (uint32_t)s, parts);
+        const uint32_t v = remap(remix(lo + x), s);
+        uint32_t j = 0, accp = parts[0];
+        while (v >= accp) accp += parts[++j];
+        for (uint32_t c = 0; c < j; ++c) {
+            fc += T.F[parts[c]];
+            if (!skip_ones(M.data, M.D, uc, T.N[parts[c]])) return fail(RECSPLIT_E_FORMAT, "unary skip out of range");
+            offset += parts[c];
+        }
+        (void)f;
+        s = parts[j];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int recsplit_version(void) { return 1; }
+
+uint32_t recsplit_max_bucket_keys(void) { return 8192; }
+
+int recsplit_build(const uint64_t* keys, size_t n, uint32_t leaf_size, uint32_t bucket_size, recsplit_bytes* out) {
+    return build_host_keys(keys, n, leaf_size, bucket_size, nullptr, out, nullptr, nullptr, false);
+}
+
+int recsplit_build_ex(const uint64_t* keys, size_t n, uint32_t leaf_size, uint32_t bucket_size,
+                      const recsplit_options* opt, recsplit_bytes* out, recsplit_stats* stats) {
+    return build_host_keys(keys, n, leaf_size, bucket_size, opt, out, stats, nullptr, false);
+}
+
+int recsplit_build_device(const uint64_t* d_keys, size_t n, uint32_t leaf_size, uint32_t bucket_size,
+                          const recsplit_options* opt, void* stream, recsplit_bytes* out, recsplit_stats* stats) {
+    if (!out) return fail(RECSPLIT_E_INVALID, "out is NULL");
+    out->data = nullptr;
+    out->size = 0;
+    if (!d_keys) return fail(RECSPLIT_E_INVALID, "d_keys is NULL");
+    int rc = check_args(n, leaf_size, bucket_size);
+    if (rc) return rc;
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        auto t0 = std::chrono::steady_clock::now();
+        rs::BuildParams p = params_of(n, leaf_size, bucket_size, opt);
+        select_device(p.device);
+        rs::BuildOutput o;
+        rs::build_on_device(d_keys, p, (cudaStream_t)stream, false, o);
+        o.stats.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (stats) *stats = o.stats;
+        return emit(o, out);
+    });
+}
+
+int recsplit_build_values(const uint64_t* keys, size_t n, uint32_t leaf_size, uint32_t bucket_size,
+                          const recsplit_options* opt, recsplit_bytes* out, uint64_t** values, size_t* n_values) {
+    if (!values || !n_values) return fail(RECSPLIT_E_INVALID, "values is NULL");
+    *values = nullptr;
+    *n_values = 0;
+    rs::BuildOutput o;
+    int rc = build_host_keys(keys, n, leaf_size, bucket_size, opt, out, nullptr, &o, true);
+    if (rc) return rc;
+    *values = (uint64_t*)malloc(std::max<size_t>(o.values.size(), 1) * 8);
+    if (!*values) {
+        recsplit_free(out);
+        return fail(RECSPLIT_E_NOMEM, "host allocation failed");
+    }
+    if (!o.values.empty()) memcpy(*values, o.values.data(), o.values.size() * 8);
+    *n_values = o.values.size();
+    return RECSPLIT_OK;
+}
+
+int recsplit_query(const uint8_t* mphf, size_t size, uint64_t key, uint64_t* out_index) {
+    if (!out_index) return fail(RECSPLIT_E_INVALID, "out_index is NULL");
+    return guarded([&]() -> int {
+        Parsed M;
+        int rc = parse(mphf, size, M);
+        if (rc) return rc;
+        return query_one(M, key, out_index);
+    });
+}
+
+int recsplit_query_many(const uint8_t* mphf, size_t size, const uint64_t* keys, size_t n, uint64_t* out) {
+    if ((!keys || !out) && n) return fail(RECSPLIT_E_INVALID, "NULL keys/out");
+    return guarded([&]() -> int {
+        Parsed M;
+        int rc = parse(mphf, size, M);
+        if (rc) return rc;
+        unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 64));
+        if (n < 100000) nt = 1;
+        std::vector<int> rcs(nt, 0);
+        std::vector<std::string> errs(nt);
+        auto work = [&](unsigned t) {
+            const size_t a = n * t / nt, b = n * (t + 1) / nt;
+            for (size_t i = a; i < b; ++i) {
+                int r = query_one(M, keys[i], out + i);
+                if (r) {
+                    rcs[t] = r;
+                    errs[t] = g_err;
+                    return;
+                }
+            }
+        };
+        if (nt == 1) {
+            work(0);
+        } else {
+            std::vector<std::thread> th;
+            for (unsigned t = 0; t < nt; ++t) th.emplace_back(work, t);
+            for (auto& x : th) x.join();
+        }
+        for (unsigned t = 0; t < nt; ++t)
+            if (rcs[t]) return fail(rcs[t], errs[t]);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_bits_per_key(const uint8_t* mphf, size_t size, double* out) {
+    if (!out) return fail(RECSPLIT_E_INVALID, "out is NULL");
+    return guarded([&]() -> int {
+        Parsed M;
+        int rc = parse(mphf, size, M);
+        if (rc) return rc;
+        *out = (double)(M.D + M.ec.nlow + M.ec.nup + M.ep.nlow + M.ep.nup) / (double)M.n;
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_search_leaves(const uint64_t* lo, const uint8_t* isb, const uint32_t* off, uint32_t n_nodes,
+                           uint32_t rotation_fitting, uint64_t* out) {
+    if (!lo || !isb || !off || !out) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    for (uint32_t j = 0; j < n_nodes; ++j) {
+        const uint32_t s = off[j + 1] - off[j];
+        if (off[j + 1] < off[j] || s < 1 || s > 24) return fail(RECSPLIT_E_INVALID, "leaf sizes must be in [1, 24]");
+    }
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        select_device(-1);
+        rs::search_leaves_host(lo, isb, off, n_nodes, rotation_fitting != 0, out);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_search_splits(const uint64_t* lo, const uint32_t* off, uint32_t n_nodes, uint32_t leaf_size,
+                           uint64_t* out) {
+    if (!lo || !off || !out) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    if (leaf_size < 2 || leaf_size > 24) return fail(RECSPLIT_E_INVALID, "leaf_size must be in [2, 24]");
+    for (uint32_t j = 0; j < n_nodes; ++j) {
+        const uint32_t s = off[j + 1] - off[j];
+        if (off[j + 1] < off[j] || s <= leaf_size || s > 8192)
+            return fail(RECSPLIT_E_INVALID, "split sizes must be in (leaf_size, 8192]");
+    }
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        select_device(-1);
+        rs::search_splits_host(lo, off, n_nodes, leaf_size, out);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_tau(uint32_t leaf_size, uint32_t s, uint32_t rotation_fitting) {
+    if (leaf_size < 2 || leaf_size > 24 || s > (1u << 20)) return fail(RECSPLIT_E_INVALID, "bad arguments");
+    if (s == 0) return 0;
+    auto T = rs::get_tables(leaf_size, rotation_fitting != 0, s);
+    return (int)T->tau[s];
+}
+
+void recsplit_free(recsplit_bytes* b) {
+    if (!b) return;
+    free(b->data);
+    b->data = nullptr;
+    b->size = 0;
+}
+
+void recsplit_free_ptr(void* p) { free(p); }
+
+const char* recsplit_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

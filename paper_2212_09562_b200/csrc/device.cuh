@@ -1,0 +1,77 @@
+// Device helpers for the RecSplit construction kernels (sm_100a).
+// Citation keys: P:n = PAPER.md line n; R<k> = DESIGN.md reading k.
+#pragma once
+#include <cstdint>
+
+namespace rsd {
+
+typedef uint64_t u64;
+typedef uint32_t u32;
+typedef uint8_t u8;
+
+constexpr u32 FULL = 0xffffffffu;
+constexpr u32 NONE = 0xffffffffu;
+
+// SplitMix64 finalizer constants (R1) and master-hash salts (R2).
+constexpr u64 MIX_C1 = 0xbf58476d1ce4e5b9ULL;
+constexpr u64 MIX_C2 = 0x94d049bb133111ebULL;
+constexpr u32 MIX_C2L = 0x133111ebu;
+constexpr u32 MIX_C2H = 0x94d049bbu;
+constexpr u64 MHC_SALT_HI = 0x9E3779B97F4A7C15ULL;
+constexpr u64 MHC_SALT_LO = 0xC2B2AE3D27D4EB4FULL;
+
+// Full 64-bit remix (used once per key for the master hash code).
+__device__ __forceinline__ u64 remix64(u64 z) {
+    z = (z ^ (z >> 30)) * MIX_C1;
+    z = (z ^ (z >> 27)) * MIX_C2;
+    return z ^ (z >> 31);
+}
+
+// High 32 bits of remix(x): the only bits remap (R3) consumes.  The last multiply
+// only needs the high word of the 64x64 product: hi(xl*C2L) + xl*C2H + xh*C2L.
+__device__ __forceinline__ u32 remix_hi(u64 x) {
+    x ^= x >> 30;
+    x *= MIX_C1;
+    x ^= x >> 27;
+    const u32 xl = (u32)x, xh = (u32)(x >> 32);
+    const u32 zh = __umulhi(xl, MIX_C2L) + xl * MIX_C2H + xh * MIX_C2L;
+    return zh ^ (zh >> 31);
+}
+
+// remap(h, r) = floor(h_hi * r / 2^32)  (R3) given h_hi
+__device__ __forceinline__ u32 remap_hi(u32 hhi, u32 r) { return __umulhi(hhi, r); }
+
+// x << s with PTX clamping semantics: s >= 32 gives 0 (used by packed counters).
+__device__ __forceinline__ u32 shl_clamp(u32 x, u32 s) {
+    u32 r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+
+__device__ __forceinline__ u32 lanemask_lt() {
+    u32 r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ u64 shfl64(u64 v, int src) {
+    u32 lo = __shfl_sync(FULL, (u32)v, src), hi = __shfl_sync(FULL, (u32)(v >> 32), src);
+    return ((u64)hi << 32) | lo;
+}
+
+__device__ __forceinline__ u64 ld_volatile_u64(const u64* p) { return *(const volatile u64*)p; }
+
+// Search-phase node record (one per node of a phase list).
+struct NodeRec {
+    u32 key_off;  // first key of the node in the key arrays
+    u32 size;     // s
+    u32 slot;     // global preorder slot of its stored value
+    u32 pad;
+};
+
+// Template node (mirrors rs::TNode).
+struct TNodeD {
+    u32 rel_off, size, fixed_off, phase, tau, phase_rank;
+};
+
+}  // namespace rsd

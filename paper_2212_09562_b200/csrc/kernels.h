@@ -1,0 +1,92 @@
+// Host-callable launchers of the sm_100a kernels (one per pipeline step).
+// All launches are asynchronous on `st`; errors surface through cudaGetLastError.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace rs {
+
+using rsd::u32;
+using rsd::u64;
+using rsd::u8;
+
+// Launch counter (kernels issued by this library in the current build).
+extern thread_local uint32_t g_launches;
+
+// ---- scan (scan.cu): out[0..n] = exclusive prefix sums of in[0..n), out[n] = total.
+size_t scan_temp_bytes(size_t n);
+void exscan_u32_to_u64(const u32* in, u64* out, size_t n, void* temp, cudaStream_t st);
+void exscan_u64(const u64* in, u64* out, size_t n, void* temp, cudaStream_t st);
+
+// ---- partition (partition.cu), steps A1-A2 of SURVEY section 8(a).
+// hi/lo master hash codes, bucket id, bucket histogram (must be zeroed).
+void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64* hi, u64* lo, u32* bkt, u32* hist,
+                 cudaStream_t st);
+// max/min bucket size and presence bitmap of sizes (present must be zeroed, cap+1 bytes)
+void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u8* present, u32 cap,
+                         cudaStream_t st);
+// scatter keys to bucket order (cursor = copy of exclusive offsets)
+void launch_scatter(const u64* hi, const u64* lo, const u32* bkt, u64 n, u64* cursor, u64* hi2,
+                    u64* lo2, cudaStream_t st);
+// per-bucket sort by hi + duplicate flag + lo/ab extraction; smax = largest bucket
+void launch_bucket_sort(const u64* hi2, const u64* lo2, const u64* C, u64 B, u32 smax, u64* lo_s,
+                        u8* ab_s, u32* dup, cudaStream_t st);
+constexpr u32 kMaxBucketKeys = 8192;
+
+// ---- tree (encode.cu): node counts per bucket, node expansion into phase lists.
+void launch_bucket_counts(const u64* C, u64 B, const u32* N, const u32* phase_cnt, u32 NP,
+                          u64* M /*[(NP+1)*(B+1)]*/, cudaStream_t st);
+void launch_expand(const u64* C, u64 B, const u64* Mscan, u32 NP, const u32* tstart,
+                   const rsd::TNodeD* tnodes, const u64* phase_off /*[NP]*/, rsd::NodeRec* nodes,
+                   cudaStream_t st);
+
+// ---- search (search.cu): the hot path, steps A4-A9.
+enum SearchKind { SK_UPPER = 0, SK_LOWER = 1, SK_LEAF_RF = 2, SK_LEAF_BF = 3 };
+struct PhaseLaunch {
+    SearchKind kind;
+    const rsd::NodeRec* nodes;
+    const u32* n_nodes;  // device count
+    u32 n_nodes_host;    // host copy (for launch sizing)
+    const u64* lo;
+    const u8* ab;
+    u64* values;    // by slot; initialised to ~0
+    u32* next_win;  // by slot; initialised to 0
+    u32* cursor;    // zeroed
+    int* active;    // n_warps entries, set to -1
+    u32* err;
+    const u32* dup;  // nonzero: duplicate keys, searches return immediately
+    u32 leaf, u1, u2;
+    u32 max_size;   // largest node size in this phase
+    u32 iters;      // 32-seed iterations per window
+    int help;
+    int sm_count;
+};
+void launch_search(const PhaseLaunch& P, cudaStream_t st);
+u32 search_active_slots(int sm_count);
+
+// key redistribution after a split phase (A7): in -> out for the phase's nodes
+void launch_reorder(const rsd::NodeRec* nodes, u32 n_nodes, const u64* values, const u64* lo_in,
+                    const u8* ab_in, u64* lo_out, u8* ab_out, u32 leaf, u32 u1, u32 u2,
+                    cudaStream_t st);
+
+// ---- encode (encode.cu), steps A10-A11.
+// bucket bit lengths: F(s) + N(s) + sum (x >> tau); also algorithmic-evals statistics
+void launch_bucket_bits(const u64* C, u64 B, const u64* nodebase, const u32* tstart,
+                        const rsd::TNodeD* tnodes, const u64* F, const u64* values, u32 leaf,
+                        u32 u1, u32 u2, int rf, u64* len, unsigned long long* evals /*[4]*/,
+                        cudaStream_t st);
+void launch_write_data(const u64* C, u64 B, const u64* nodebase, const u32* tstart,
+                       const rsd::TNodeD* tnodes, const u64* F, const u64* values, const u64* P,
+                       unsigned long long* words, cudaStream_t st);
+// min over i of R[i+1]-R[i], R[i] = P[i] - floor(beta C[i] / 2^20)
+void launch_min_residual(const u64* C, const u64* P, u64 B, u64 beta, long long* out,
+                         cudaStream_t st);
+// EF lower/upper bits of C'[i] = C[i] - i dC and P'[i] = R[i] - i dR
+void launch_ef_write(const u64* C, const u64* P, u64 B, u64 dC, u64 beta, long long dR, u32 LC,
+                     u32 LP, unsigned long long* c_low, unsigned long long* c_up,
+                     unsigned long long* p_low, unsigned long long* p_up, cudaStream_t st);
+
+}  // namespace rs

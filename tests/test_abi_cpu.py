@@ -1,0 +1,91 @@
+"""CPU-side checks of the C-ABI library (no compute calls that need a GPU).
+
+* the library loads and exports every symbol include/recsplit.h declares;
+* its host tables (tau) agree with the oracle's for every reachable node class;
+* its host query reads the oracle's serialized format (cross-check of two
+  independent readers/writers of DESIGN.md section 6);
+* without a GPU the build fails loudly (RECSPLIT_E_CUDA) -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2212_09562_b200 as rs
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_symbols_exported():
+    hdr = open(os.path.join(ROOT, "include", "recsplit.h")).read()
+    declared = set(re.findall(r"RECSPLIT_API[^;(]*?\b(recsplit_\w+)\s*\(", hdr))
+    assert declared == set(rs.SYMBOLS)
+    L = rs.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.recsplit_version() == 1
+    assert L.recsplit_max_bucket_keys() == 8192
+
+
+@pytest.mark.parametrize("leaf", [2, 3, 5, 8, 12, 16, 20, 24])
+@pytest.mark.parametrize("rf", [True, False])
+def test_tau_tables_match_oracle(leaf, rf):
+    """Library (log-factorial sums, expm1) vs oracle (lgamma, squaring) tau for every
+    node size up to 2600 -- the tie margin is ~7e-6 so any faithful evaluation agrees."""
+    for s in list(range(1, 400)) + list(range(400, 2600, 7)):
+        assert rs.tau(leaf, s, rf) == oracle.tau(leaf, s, rf), (leaf, s, rf)
+
+
+@pytest.mark.parametrize("leaf,b,rf,n", [(8, 100, True, 10000), (5, 5, True, 3000), (16, 300, False, 2000),
+                                          (3, 1, True, 500), (24, 50, True, 100), (12, 1000, True, 3000)])
+def test_library_query_reads_oracle_format(leaf, b, rf, n):
+    keys = synth.keys(n, leaf * 7 + b)
+    blob = oracle.build(keys, leaf, b, rf=rf, threads=4)
+    q = rs.query_many(blob, keys)
+    assert np.array_equal(q, oracle.query_many(blob, keys))
+    assert np.array_equal(np.sort(q), np.arange(n, dtype=np.uint64))
+    assert rs.query(blob, int(keys[0])) == int(q[0])
+
+
+def test_corrupt_blob_is_format_error():
+    keys = synth.keys(1000, 3)
+    blob = oracle.build(keys, 8, 100)
+    for bad in (blob[:50], b"XXXX" + blob[4:], blob[:-8], blob + b"\0" * 8):
+        with pytest.raises(rs.RecSplitError) as e:
+            rs.query_many(bad, keys[:10])
+        assert e.value.code == rs.E_FORMAT
+
+
+def test_bits_per_key_accounting():
+    keys = synth.keys(10000, 1)
+    blob = oracle.build(keys, 8, 100)
+    from test_oracle_pins import bits_per_object
+    assert rs.bits_per_key(blob) == pytest.approx(bits_per_object(blob))
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    keys = synth.keys(100, 1)
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.build(keys, 8, 100)
+    assert e.value.code == rs.E_CUDA
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.search_leaves(np.zeros(4, np.uint64), np.zeros(4, np.uint8), [0, 4])
+    assert e.value.code == rs.E_CUDA
+
+
+def test_argument_validation():
+    keys = synth.keys(10, 1)
+    for leaf, b in [(1, 10), (25, 10), (8, 0)]:
+        with pytest.raises(rs.RecSplitError) as e:
+            rs.build(keys, leaf, b)
+        assert e.value.code == rs.E_INVALID
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.build(np.zeros(0, np.uint64), 8, 100)
+    assert e.value.code == rs.E_INVALID

@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar: bit-exact -- every stored value and every serialized byte is integer work.
+Kernel level: leaf (rotation fitting / brute force) and split searches on random
+nodes of every size class.  End to end: full byte parity on C1 and C2 and on many
+small configurations (ragged buckets, empty buckets, m=1 leaves, fanout edge cases);
+sampled per-bucket parity at the full C3 size in the launch configuration bench.py
+times, plus properties that hold at any size (bijectivity, bits/object).
+"""
+from __future__ import annotations
+
+import math
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2212_09562_b200 as rs
+import synth
+
+pytestmark = pytest.mark.gpu
+
+M64 = (1 << 64) - 1
+
+
+def _mhc_np(keys, g=0):
+    """Vectorised master hash for selecting buckets in the sampled tests (R2)."""
+    def remix(z):
+        with np.errstate(over="ignore"):
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return z ^ (z >> np.uint64(31))
+    k = keys ^ np.uint64(g)
+    return remix(k ^ np.uint64(0x9E3779B97F4A7C15)), remix(k ^ np.uint64(0xC2B2AE3D27D4EB4F))
+
+
+# ------------------------------------------------------------------ kernel level --
+
+@pytest.mark.parametrize("rf", [True, False])
+def test_leaf_search_parity(rf):
+    rng = np.random.default_rng(11 + rf)
+    sizes = []
+    for m in range(1, 17):
+        sizes += [m] * (400 if m <= 12 else 60)
+    if not rf:
+        sizes = [m for m in sizes if m <= 11] + [12] * 10
+    rng.shuffle(sizes)
+    off = np.zeros(len(sizes) + 1, dtype=np.uint32)
+    off[1:] = np.cumsum(sizes)
+    lo = rng.integers(0, M64, size=int(off[-1]), dtype=np.uint64, endpoint=True)
+    isb = rng.integers(0, 2, size=int(off[-1]), dtype=np.uint8)
+    got = rs.search_leaves(lo, isb, off, rotation_fitting=rf)
+    sl = [(int(off[j]), int(off[j + 1])) for j in range(len(sizes))]
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        if rf:
+            want = list(ex.map(lambda ab: oracle.leaf_rf(lo[ab[0]:ab[1]], isb[ab[0]:ab[1]]), sl))
+        else:
+            want = list(ex.map(lambda ab: oracle.leaf_bf(lo[ab[0]:ab[1]]), sl))
+    assert got.tolist() == want
+
+
+def test_leaf_search_large_m():
+    rng = np.random.default_rng(5)
+    sizes = [17, 18, 20, 24, 24, 19]
+    off = np.zeros(len(sizes) + 1, dtype=np.uint32)
+    off[1:] = np.cumsum(sizes)
+    lo = rng.integers(0, M64, size=int(off[-1]), dtype=np.uint64, endpoint=True)
+    isb = rng.integers(0, 2, size=int(off[-1]), dtype=np.uint8)
+    got = rs.search_leaves(lo, isb, off, rotation_fitting=True)
+    with ThreadPoolExecutor(len(sizes)) as ex:
+        want = list(ex.map(lambda j: oracle.leaf_rf(lo[off[j]:off[j + 1]], isb[off[j]:off[j + 1]]),
+                           range(len(sizes))))
+    assert got.tolist() == want
+
+
+@pytest.mark.parametrize("leaf", [2, 3, 5, 8, 12, 16, 19, 20, 24])
+def test_split_search_parity(leaf):
+    """Every split class the oracle can finish in seconds: L1 full/partial, L2
+    full/partial, upper (fanout 2), and the 64-bit packed-counter path (l >= 19)."""
+    _, _, u1, u2 = oracle.shape(leaf)
+    rng = np.random.default_rng(leaf)
+    cands = {leaf + 1, 2 * leaf + 1, 3 * leaf, 5 * leaf, 7 * leaf + 1, 8 * leaf, u1 - 1, u1, u1 + 1,
+             2 * u1 + 1, 3 * u1, u2 - 1, u2, u2 + 3, 2 * u2 + 1, 3 * u2 + 7}
+    sizes = []
+    for s in sorted(cands):
+        if s <= leaf or s > 8192:
+            continue
+        work = s / oracle.split_prob(leaf, s)  # expected oracle remix evaluations
+        if work <= 3e8:
+            sizes += [s] * (6 if work < 1e7 else 2)
+    rng.shuffle(sizes)
+    off = np.zeros(len(sizes) + 1, dtype=np.uint32)
+    off[1:] = np.cumsum(sizes)
+    lo = rng.integers(0, M64, size=int(off[-1]), dtype=np.uint64, endpoint=True)
+    got = rs.search_splits(lo, off, leaf)
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        want = list(ex.map(lambda j: oracle.find_split(leaf, lo[off[j]:off[j + 1]]), range(len(sizes))))
+    assert got.tolist() == want
+
+
+# ------------------------------------------------------------------- end to end --
+
+def _check_full(keys, leaf, b, rf=True, threads=None):
+    threads = threads or os.cpu_count()
+    want, want_vals = oracle.build(keys, leaf, b, rf=rf, threads=threads, values=True)
+    got, vals = rs.build_values(keys, leaf, b, rotation_fitting=rf)
+    if not np.array_equal(vals, want_vals):
+        bad = np.flatnonzero(vals != want_vals)
+        raise AssertionError(f"{len(bad)} node values differ, first at slot {bad[0]}: "
+                             f"gpu {vals[bad[0]]} oracle {want_vals[bad[0]]}")
+    assert got == want
+    return got
+
+
+def test_c1_full_parity_and_bijective():
+    cfg = synth.CONFIGS["C1"]
+    keys = synth.keys(cfg["n"], cfg["seed"])
+    blob = _check_full(keys, cfg["leaf"], cfg["bucket"])
+    q = rs.query_many(blob, keys)
+    assert np.array_equal(np.sort(q), np.arange(len(keys), dtype=np.uint64))
+    assert rs.build(keys[::-1].copy(), cfg["leaf"], cfg["bucket"]) == blob  # key order invariance
+
+
+@pytest.mark.parametrize("leaf,b,rf,n", [
+    (2, 7, True, 5000), (3, 1, True, 2000), (4, 3, False, 4000), (5, 5, True, 20000), (6, 50, True, 20000),
+    (7, 30, True, 20000), (8, 100, False, 20000), (10, 64, True, 20000), (11, 500, True, 20000),
+    (12, 1000, True, 30000), (13, 200, True, 6000), (14, 2000, True, 8000), (16, 2000, True, 6000),
+    (16, 40, True, 4000), (18, 300, True, 2000), (20, 100, True, 600), (24, 24, True, 200),
+    (8, 7000, True, 21000), (8, 100, True, 1), (8, 100, True, 2), (16, 100, True, 17), (9, 9, True, 99),
+])
+def test_small_configs_full_parity(leaf, b, rf, n):
+    keys = synth.keys(n, 1000 * leaf + b)
+    blob = _check_full(keys, leaf, b, rf=rf)
+    q = rs.query_many(blob, keys)
+    assert np.array_equal(np.sort(q), np.arange(n, dtype=np.uint64))
+
+
+def test_duplicate_keys_rejected():
+    keys = synth.keys(5000, 9)
+    keys[77] = keys[4000]
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.build(keys, 8, 100)
+    assert e.value.code == rs.E_DUPLICATE
+
+
+def test_bucket_cap_enforced():
+    keys = synth.keys(30000, 3)
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.build(keys, 8, 20000)  # one bucket of 20000 > 8192
+    assert e.value.code == rs.E_INVALID
+
+
+def test_device_entry_matches_host_entry():
+    import torch
+    keys = synth.keys(50000, 21)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    assert rs.build_device(kt, 12, 500) == rs.build(keys, 12, 500)
+
+
+@pytest.mark.slow
+def test_c2_full_parity():
+    """C2 at full size (n=5e6, l=8, b=100): every byte equals the oracle."""
+    cfg = synth.CONFIGS["C2"]
+    keys = synth.keys(cfg["n"], cfg["seed"])
+    blob = _check_full(keys, cfg["leaf"], cfg["bucket"])
+    q = rs.query_many(blob, keys)
+    assert np.array_equal(np.sort(q), np.arange(len(keys), dtype=np.uint64))
+    bpk = rs.bits_per_key(blob)
+    assert abs(bpk - 1.806) < 0.02, bpk  # paper P:828 (SIMDRecSplit l=8, b=100)
+
+
+def _subtree_nodes(leaf):
+    memo = {}
+
+    def N(s):
+        if s == 0:
+            return 0
+        if s not in memo:
+            memo[s] = 1 + sum(N(c) for c in oracle.parts(leaf, s))
+        return memo[s]
+    return N
+
+
+@pytest.mark.slow
+def test_c3_sampled_bucket_parity_and_properties():
+    """C3 at full size (n=5e6, l=16, b=2000) as bench.py builds it: the values of
+    sampled buckets equal the oracle's, the MPHF is bijective, bits/object ~ 1.560
+    (P:581)."""
+    cfg = synth.CONFIGS["C3"]
+    keys = synth.keys(cfg["n"], cfg["seed"])
+    leaf, b = cfg["leaf"], cfg["bucket"]
+    blob, vals = rs.build_values(keys, leaf, b)
+    q = rs.query_many(blob, keys)
+    assert np.array_equal(np.sort(q), np.arange(len(keys), dtype=np.uint64))
+    bpk = rs.bits_per_key(blob)
+    assert abs(bpk - 1.560) < 0.004, bpk
+    hi, _ = _mhc_np(keys)
+    B = (len(keys) + b - 1) // b
+    bucket = ((hi >> np.uint64(32)) * np.uint64(B)) >> np.uint64(32)
+    sizes = np.bincount(bucket.astype(np.int64), minlength=B)
+    N = _subtree_nodes(leaf)
+    nb = np.concatenate([[0], np.cumsum([N(int(s)) for s in sizes])])
+    assert nb[-1] == len(vals)
+    rng = np.random.default_rng(0)
+    sample = sorted(rng.choice(B, size=min(B, max(4, os.cpu_count() or 4)), replace=False).tolist())
+    sample[0] = int(np.argmax(sizes))  # include the largest bucket
+    order = np.argsort(bucket, kind="stable")
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+
+    def one(i):
+        ks = keys[order[starts[i]:starts[i + 1]]]
+        return i, oracle.bucket_values(ks, leaf)
+
+    with ThreadPoolExecutor(len(sample)) as ex:
+        for i, want in ex.map(one, sample):
+            assert vals[nb[i]:nb[i + 1]].tolist() == want.tolist(), f"bucket {i}"
