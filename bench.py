@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""Benchmark: RecSplit MPHF construction keys/s on B200 (BASELINE.json metric).
+
+A "step" is one complete construction of the MPHF of the workload's keys: hash +
+bucket sort, every split and leaf search, key redistribution, Golomb-Rice and
+Elias-Fano encoding, serialization.  Default workload: C3 (n=5e6 keys, l=16, b=2000,
+rotation fitting) -- the north-star target and the paper's 1.56 bits/object point.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+value      keys/s with the keys already resident in HBM (device-pointer ABI entry),
+           device time (CUDA events on the launch stream), L2 flushed between steps;
+           for N>1: total keys of all ranks / max over ranks.
+e2e        the same metric through recsplit_build with HOST keys (pinned), H2D and
+           the result D2H inside the timed region (host wall clock around the call).
+roofline   dominant kernel = the lower-level-1 split search (62% of the work at C3):
+           algorithmic remix evaluations (sum over nodes of (minimal seed + 1) x keys)
+           / that kernel's CUDA-event duration, against the INT32-pipe peak.
+cpu_baseline / --impl reference: the plain C oracle, as it stands, on this host's cores,
+           on a bounded sample of the same workload (whole buckets).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+PAPER_KEYS_PER_S = {"C3": 1.0e6}  # GPURecSplit RF, l=16 b=2000: 1.0 us/object on RTX 3090
+WORKLOAD_TEXT = {
+    "C1": "C1: n=1e4 random u64 keys, l=8, b=100, rotation fitting",
+    "C2": "C2: n=5e6 random u64 keys, l=8, b=100, rotation fitting",
+    "C3": "C3: n=5e6 random u64 keys, l=16, b=2000, rotation fitting",
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def int32_peak_evals(sm_count: int, mhz: float) -> float:
+    """INT32 roofline in remix evaluations/s: 4 SMSPs x 32 lanes
+    issue per clock, ALU and FMA pipes 64 lanes/clk/SM each; the minimal SplitMix64
+    evaluation + remap + packed count needs 21 integer instructions split 10.5/10.5
+    over the two pipes -> 64/10.5 = 6.10 evaluations per clock per SM."""
+    return sm_count * mhz * 1e6 * (64.0 / 10.5)
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].strip().lower() == "active":
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_sample(cfg: dict, keys: np.ndarray, budget_s: float, threads: int):
+    """Run the oracle on whole buckets of the workload (largest-bucket-first order is
+    avoided: buckets are taken in index order) until ~budget_s of wall time; returns
+    (keys processed, seconds, buckets)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+
+    oracle.compile_oracle()
+    n, leaf, b = cfg["n"], cfg["leaf"], cfg["bucket"]
+    B = (n + b - 1) // b
+
+    def remix(z):
+        with np.errstate(over="ignore"):
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return z ^ (z >> np.uint64(31))
+    hi = remix(keys ^ np.uint64(0x9E3779B97F4A7C15))
+    bucket = ((hi >> np.uint64(32)) * np.uint64(B)) >> np.uint64(32)
+    order = np.argsort(bucket, kind="stable")
+    sizes = np.bincount(bucket.astype(np.int64), minlength=B)
+    starts = np.concatenate([[0], np.cumsum(sizes)])
+    done_keys, nb = 0, 0
+    t0 = time.perf_counter()
+    i = 0
+    with ThreadPoolExecutor(threads) as ex:
+        while i < B and time.perf_counter() - t0 < budget_s:
+            batch = list(range(i, min(B, i + threads)))
+            i += len(batch)
+            list(ex.map(lambda j: oracle.bucket_values(keys[order[starts[j]:starts[j + 1]]], leaf), batch))
+            done_keys += int(sum(sizes[j] for j in batch))
+            nb += len(batch)
+    return done_keys, time.perf_counter() - t0, nb
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = synth.CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        # the oracle arm: rank 0 only, on host cores, bounded sample per step
+        if rank != 0:
+            return
+        keys = synth.keys(cfg["n"], cfg["seed"])
+        import oracle
+        c1 = synth.CONFIGS["C1"]
+        for _ in range(args.warmup):  # warm-up: one small build (page-in, thread start-up)
+            oracle.build(synth.keys(c1["n"], c1["seed"]), c1["leaf"], c1["bucket"], threads=threads)
+        tot_k, tot_t, tot_b = 0, 0.0, 0
+        for _ in range(args.steps):  # each step: one round of `threads` whole buckets
+            k, t, nb = cpu_sample(cfg, keys, 0.0, threads)
+            tot_k, tot_t, tot_b = tot_k + k, tot_t + t, tot_b + nb
+        v = tot_k / tot_t
+        sample = f"{tot_b} whole buckets ({tot_k} keys) of the {args.config} workload over {args.steps} steps"
+        print(json.dumps({
+            "impl": "reference", "metric": "MPHF construction keys/s", "value": v, "unit": "keys/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_TEXT[args.config], "n": cfg["n"], "leaf": cfg["leaf"],
+                       "bucket": cfg["bucket"]},
+            "cpu_baseline": {"value": v, "unit": "keys/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    import torch
+
+    import paper_2212_09562_b200 as rs
+
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    # weak scaling: each rank builds its own 5e6-key MPHF (independent key sets)
+    keys = synth.keys(cfg["n"], cfg["seed"] + 1000 * rank)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def one_step():
+        flush.zero_()  # L2 flush (inputs are 40 MB < 126 MB L2)
+        a = torch.cuda.Event(enable_timing=True)
+        z = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        blob, st = rs.build_device(kt, cfg["leaf"], cfg["bucket"], stream=stream, stats=True)
+        z.record(stream)
+        z.synchronize()
+        return a.elapsed_time(z) * 1e-3, blob, st
+
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(dev)
+    times, stats = [], []
+    blob = None
+    for _ in range(args.steps):
+        t, blob, st = one_step()
+        times.append(t)
+        stats.append(st)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    mean_t = float(np.mean(times))
+    t_all = torch.tensor([mean_t], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t_all, op=torch.distributed.ReduceOp.MAX)
+    t_max = float(t_all.item())
+    value = cfg["n"] * world / t_max
+
+    # ---- e2e: host keys through recsplit_build, H2D + D2H inside the timed region
+    pinned = torch.from_numpy(keys.view(np.int64)).pin_memory()
+    pkeys = pinned.numpy().view(np.uint64)
+    rs.build(pkeys, cfg["leaf"], cfg["bucket"])  # warm
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eb = rs.build(pkeys, cfg["leaf"], cfg["bucket"])
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_t = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = cfg["n"] * world / float(e2e_t.item())
+    assert eb == blob, "host-input and device-input builds differ"
+
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (lower-level-1 split search)
+    cls = 2
+    evals = float(np.mean([s["algo_evals"][cls] for s in stats]))
+    kt_s = float(np.mean([s["t_search"][cls] for s in stats]))
+    peaks = _peaks()
+    max_mhz = peaks.get("sm_max_mhz", 1965.0)
+    peak = int32_peak_evals(sms, max_mhz) / 1e9
+    achieved = evals / kt_s / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_l1_split_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    st0 = stats[-1]
+    line = {
+        "metric": "MPHF construction keys/s", "value": value, "unit": "keys/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t_max,
+        "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": (value / world / PAPER_KEYS_PER_S[args.config]) if args.config in PAPER_KEYS_PER_S else None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_TEXT[args.config], "n": cfg["n"], "leaf": cfg["leaf"],
+                   "bucket": cfg["bucket"], "keys_per_rank": cfg["n"], "l2": "flushed between steps",
+                   "bits_per_key": rs.bits_per_key(blob), "parallelism": f"replicas{world}" if world > 1 else "1gpu"},
+        "e2e": {"value": e2e_value, "unit": "keys/s", "h2d_bytes_per_step": int(cfg["n"] * 8),
+                "d2h_bytes_per_step": len(blob)},
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "roofline": {"bound": "alu", "kernel": "k_search<SK_LOWER> (lower level 1 splits)",
+                     "achieved": achieved, "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
+                     "traffic": traffic,
+                     "peak_note": f"{sms} SMs x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) x 6.10 evals/clk/SM"},
+        "phases_s": {"partition": st0["t_partition"], "tree": st0["t_tree"], "upper": st0["t_search"][0],
+                     "lower2": st0["t_search"][1], "lower1": st0["t_search"][2], "leaves": st0["t_search"][3],
+                     "reorder": st0["t_reorder"], "encode": st0["t_encode"], "d2h": st0["t_d2h"]},
+        "algo_evals_per_step": [int(x) for x in st0["algo_evals"]],
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        k, t, nb = cpu_sample(cfg, keys, args.cpu_budget, threads)
+        line["cpu_baseline"] = {"value": k / t, "unit": "keys/s", "cores": threads, "kind": "oracle",
+                                "sample": f"{nb} whole buckets ({k} keys) of the {args.config} workload, "
+                                          f"{threads} threads over contiguous buckets"}
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

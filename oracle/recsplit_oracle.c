@@ -104,16 +104,12 @@ int oracle_parts(u32 leaf, u32 s, u32 *parts) {
     return (int)f;
 }
 
-/* Child index of key for a split node of size s with seed sigma.
- * lower levels: floor(remap(h, s) / unit); upper: [remap(h, s) >= c0]. */
+/* Child index of key for a split node of size s with seed sigma:
+ * lower levels: floor(remap(h, s) / unit) with unit = parts[0];
+ * upper level:  [remap(h, s) >= c0] = floor(remap(h, s) / c0), since s <= 2 c0. */
 static u32 part_of(u32 s, const u32 *parts, int f, u64 lo, u64 sigma) {
-    u32 v = oracle_remap(node_hash(lo, sigma), s);
-    u32 acc = 0;
-    for (int j = 0; j < f; j++) {
-        acc += parts[j];
-        if (v < acc) return (u32)j;
-    }
-    return (u32)(f - 1); /* unreachable: v < s = sum(parts) */
+    (void)f;
+    return oracle_remap(node_hash(lo, sigma), s) / parts[0];
 }
 
 /* ------------------------------------------------------------------ search -- */
@@ -128,7 +124,7 @@ int oracle_find_split(u32 leaf, const u64 *lo, u32 s, u64 *out_sigma) {
     if (f == 0) return ORC_E_INVALID;
     for (u64 sigma = 0; sigma < SEED_CAP; sigma++) {
         u32 cnt[64];
-        memset(cnt, 0, sizeof cnt);
+        for (int j = 0; j < f; j++) cnt[j] = 0;
         for (u32 k = 0; k < s; k++) cnt[part_of(s, parts, f, lo[k], sigma)]++;
         int ok = 1;
         for (int j = 0; j < f; j++)
