@@ -123,7 +123,7 @@ def cpu_sample(cfg: dict, keys: np.ndarray, budget_s: float, threads: int):
     t0 = time.perf_counter()
     i = 0
     with ThreadPoolExecutor(threads) as ex:
-        while i < B and time.perf_counter() - t0 < budget_s:
+        while i < B and (nb == 0 or time.perf_counter() - t0 < budget_s):
             batch = list(range(i, min(B, i + threads)))
             i += len(batch)
             list(ex.map(lambda j: oracle.bucket_values(keys[order[starts[j]:starts[j + 1]]], leaf), batch))

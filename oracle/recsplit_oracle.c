@@ -104,12 +104,23 @@ int oracle_parts(u32 leaf, u32 s, u32 *parts) {
     return (int)f;
 }
 
-/* Child index of key for a split node of size s with seed sigma:
- * lower levels: floor(remap(h, s) / unit) with unit = parts[0];
- * upper level:  [remap(h, s) >= c0] = floor(remap(h, s) / c0), since s <= 2 c0. */
-static u32 part_of(u32 s, const u32 *parts, int f, u64 lo, u64 sigma) {
+/* Child index of key for a split node of size s with seed sigma (P:114-119,
+ * SURVEY 8(c) part(k, sigma, s)):
+ *   lower levels (f parts of `unit` = parts[0], smaller last): floor(remap(h, s) / unit);
+ *   upper level (fanout 2, parts [c0, s - c0]): [remap(h, s) >= c0].
+ * (c0 can be < s/2 for odd s, e.g. s = 2 u2 + 1, so the upper rule is not a division.) */
+static u32 part_of(u32 s, const u32 *parts, int f, int upper, u64 lo, u64 sigma) {
+    u32 v = oracle_remap(node_hash(lo, sigma), s);
     (void)f;
-    return oracle_remap(node_hash(lo, sigma), s) / parts[0];
+    if (upper) return v >= parts[0] ? 1u : 0u;
+    return v / parts[0];
+}
+
+/* upper level <=> s > u2 */
+static int is_upper(u32 leaf, u32 s) {
+    u32 f1, f2, u1, u2;
+    oracle_shape(leaf, &f1, &f2, &u1, &u2);
+    return s > u2;
 }
 
 /* ------------------------------------------------------------------ search -- */
@@ -122,10 +133,11 @@ int oracle_find_split(u32 leaf, const u64 *lo, u32 s, u64 *out_sigma) {
     u32 parts[64];
     int f = oracle_parts(leaf, s, parts);
     if (f == 0) return ORC_E_INVALID;
+    int up = is_upper(leaf, s);
     for (u64 sigma = 0; sigma < SEED_CAP; sigma++) {
         u32 cnt[64];
         for (int j = 0; j < f; j++) cnt[j] = 0;
-        for (u32 k = 0; k < s; k++) cnt[part_of(s, parts, f, lo[k], sigma)]++;
+        for (u32 k = 0; k < s; k++) cnt[part_of(s, parts, f, up, lo[k], sigma)]++;
         int ok = 1;
         for (int j = 0; j < f; j++)
             if (cnt[j] != parts[j]) ok = 0;
@@ -383,7 +395,7 @@ static int emit(const tables *T, mhc_t *keys, u32 s, u64 *vals, u64 *pos, mhc_t 
     u32 w = 0;
     for (int j = 0; j < f; j++)
         for (u32 k = 0; k < s; k++)
-            if (part_of(s, parts, f, keys[k].lo, sigma) == (u32)j) tmp[w++] = keys[k];
+            if (part_of(s, parts, f, is_upper(leaf, s), keys[k].lo, sigma) == (u32)j) tmp[w++] = keys[k];
     memcpy(keys, tmp, (size_t)s * sizeof(mhc_t));
     u32 off = 0;
     for (int j = 0; j < f; j++) {
@@ -802,7 +814,7 @@ int oracle_query_many(const u8 *blob, u64 size, const u64 *keys, u64 nk, u64 *ou
             }
             u32 parts[64];
             int f = oracle_parts(leaf, cs, parts);
-            u32 j = part_of(cs, parts, f, lo, x);
+            u32 j = part_of(cs, parts, f, is_upper(leaf, cs), lo, x);
             for (u32 c = 0; c < j; c++) {
                 fc += T.F[parts[c]];
                 u64 skip = T.N[parts[c]]; /* skip N(c) unary codes */

@@ -93,7 +93,9 @@ __global__ void k_bucket_bits(const u64* __restrict__ C, u64 B, const u64* __res
                 acc += (v >> x.tau) + 1;
                 const u32 cs = x.size;
                 if (cs <= leaf) {
-                    ev[3] += rf ? (v / cs + 1) * cs : (v + 1) * cs;
+                    // RF: (floor(v/m) + 1) base seeds of m evaluations (32-bit division when it fits)
+                    const u64 k = v < (1ull << 32) ? (u64)((u32)v / cs) : v / cs;
+                    ev[3] += rf ? (k + 1) * cs : (v + 1) * cs;
                 } else {
                     ev[cs > u2 ? 0 : cs > u1 ? 1 : 2] += (v + 1) * cs;
                 }

@@ -22,18 +22,16 @@ void exscan_u32_to_u64(const u32* in, u64* out, size_t n, void* temp, cudaStream
 void exscan_u64(const u64* in, u64* out, size_t n, void* temp, cudaStream_t st);
 
 // ---- partition (partition.cu), steps A1-A2 of SURVEY section 8(a).
-// hi/lo master hash codes, bucket id, bucket histogram (must be zeroed).
-void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64* hi, u64* lo, u32* bkt, u32* hist,
-                 cudaStream_t st);
+// master hash code -> lo, A/B bit, bucket id; bucket histogram (zeroed); duplicate
+// detection through a zeroed open-addressing set of (set_mask+1) u64 slots (dup[0..1] zeroed).
+void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64* lo, u8* ab, u32* bkt, u32* hist,
+                 unsigned long long* set, u64 set_mask, u32* dup, cudaStream_t st);
 // max/min bucket size and presence bitmap of sizes (present must be zeroed, cap+1 bytes)
 void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u8* present, u32 cap,
                          cudaStream_t st);
-// scatter keys to bucket order (cursor = copy of exclusive offsets)
-void launch_scatter(const u64* hi, const u64* lo, const u32* bkt, u64 n, u64* cursor, u64* hi2,
-                    u64* lo2, cudaStream_t st);
-// per-bucket sort by hi + duplicate flag + lo/ab extraction; smax = largest bucket
-void launch_bucket_sort(const u64* hi2, const u64* lo2, const u64* C, u64 B, u32 smax, u64* lo_s,
-                        u8* ab_s, u32* dup, cudaStream_t st);
+// scatter (lo, ab) to bucket order (cursor = copy of exclusive offsets)
+void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cursor, u64* lo2,
+                    u8* ab2, cudaStream_t st);
 constexpr u32 kMaxBucketKeys = 8192;
 
 // ---- tree (encode.cu): node counts per bucket, node expansion into phase lists.

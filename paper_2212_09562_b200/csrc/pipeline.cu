@@ -211,31 +211,38 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
     Timer tm(st);
     const int e0 = tm.mark();
 
-    // ---- A1/A2: hash, histogram, counting sort, per-bucket sort ---------------
-    u64* hi = A.alloc<u64>(n);
-    u64* lo = A.alloc<u64>(n);
+    // ---- A1/A2: hash + duplicate set, histogram, counting sort by bucket -----------
+    u64* lo_t = A.alloc<u64>(n);
+    u8* ab_t = A.alloc<u8>(n);
     u32* bkt = A.alloc<u32>(n);
     u32* hist = A.alloc<u32>(B + 1);
     u64* C = A.alloc<u64>(B + 2);
     u64* cursor = A.alloc<u64>(B + 1);
-    u32* small = A.alloc<u32>(8);  // [0] max, [1] min bucket size, [2] dup, [3] seed-cap err
+    // [0] max, [1] min bucket size, [2] duplicate flag, [3] keys with MHC.hi == 0, [4] seed cap
+    u32* small = A.alloc<u32>(8);
     const uint32_t cap = kMaxBucketKeys;
     u8* present_d = A.alloc<u8>(cap + 1);
-    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(B + 1, 1) * 64) + 64);
+    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(B + 1, 1)) + 64);
+    uint64_t set_slots = 1024;
+    while (set_slots < 2 * n) set_slots <<= 1;
+    unsigned long long* dupset = A.alloc<unsigned long long>(set_slots);
+    CK(cudaMemsetAsync(dupset, 0, set_slots * 8, st));
     CK(cudaMemsetAsync(hist, 0, (B + 1) * 4, st));
     CK(cudaMemsetAsync(present_d, 0, cap + 1, st));
     const uint32_t small_init[8] = {0, 0xffffffffu, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(small, small_init, sizeof small_init, cudaMemcpyHostToDevice, st));
-    launch_hash(d_keys, n, p.g, B, hi, lo, bkt, hist, st);
+    launch_hash(d_keys, n, p.g, B, lo_t, ab_t, bkt, hist, dupset, set_slots - 1, small + 2, st);
     CKL();
     launch_bucket_stats(hist, B, small, present_d, cap, st);
     CKL();
     exscan_u32_to_u64(hist, C, B, scan_tmp, st);
     CKL();
     CK(cudaMemcpyAsync(cursor, C, (B + 1) * 8, cudaMemcpyDeviceToDevice, st));
-    u64* hi2 = A.alloc<u64>(n);
-    u64* lo2 = A.alloc<u64>(n);
-    launch_scatter(hi, lo, bkt, n, cursor, hi2, lo2, st);
+    u64* lo_a = A.alloc<u64>(n);
+    u8* ab_a = A.alloc<u8>(n);
+    u64* lo_b = A.alloc<u64>(n);
+    u8* ab_b = A.alloc<u8>(n);
+    launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
     CKL();
     // sync A: bucket-size range and the set of occurring sizes
     uint32_t mm[2];
@@ -249,12 +256,6 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
         throw Error(RECSPLIT_E_INVALID, "bucket of " + std::to_string(smax) + " keys exceeds the supported maximum " +
                                             std::to_string(cap) + " (use a smaller bucket_size)");
     present.resize(smax + 1);
-    u64* lo_a = A.alloc<u64>(n);
-    u8* ab_a = A.alloc<u8>(n);
-    u64* lo_b = A.alloc<u64>(n);
-    u8* ab_b = A.alloc<u8>(n);
-    launch_bucket_sort(hi2, lo2, C, B, smax, lo_a, ab_a, small + 2, st);
-    CKL();
     const int e1 = tm.mark();
 
     // ---- A3: node table --------------------------------------------------------
@@ -343,7 +344,7 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
         P.next_win = next_win;
         P.cursor = cursors + q;
         P.active = active;
-        P.err = small + 3;
+        P.err = small + 4;
         P.dup = small + 2;
         P.leaf = leaf;
         P.u1 = sh.u1;
@@ -381,14 +382,14 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
     exscan_u64(len, Pbits, B, scan_tmp, st);
     CKL();
     uint64_t D = 0;
-    uint32_t flags[2];
+    uint32_t flags[3];
     unsigned long long ev_h[4];
     CK(cudaMemcpyAsync(&D, Pbits + B, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(flags, small + 2, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(flags, small + 2, 12, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(ev_h, evals, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));  // sync C
-    if (flags[0]) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
-    if (flags[1]) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
+    if (flags[0] || flags[1] > 1) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
+    if (flags[2]) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
     for (int c = 0; c < 4; ++c) S.algo_evals[c] = ev_h[c];
     const uint64_t beta = (uint64_t)(((unsigned __int128)D << 20) / n);
     const uint64_t dC = smin;
@@ -533,13 +534,13 @@ static void search_nodes_host(const uint64_t* lo, const uint8_t* isb, const uint
         rsd::NodeRec* d_nodes = A.alloc<rsd::NodeRec>(groups[g].size());
         CK(cudaMemcpy(d_nodes, groups[g].data(), groups[g].size() * sizeof(rsd::NodeRec), cudaMemcpyHostToDevice));
         u32 cnt = (u32)groups[g].size();
-        CK(cudaMemcpy(small + 4, &cnt, 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(small + 6, &cnt, 4, cudaMemcpyHostToDevice));
         CK(cudaMemset(small, 0, 4));
         CK(cudaMemset(active, 0xff, nslots * 4));
         PhaseLaunch P{};
         P.kind = mode == 1 ? SK_LEAF_RF : mode == 2 ? SK_LEAF_BF : (g == 0 ? SK_UPPER : SK_LOWER);
         P.nodes = d_nodes;
-        P.n_nodes = small + 4;
+        P.n_nodes = small + 6;
         P.n_nodes_host = cnt;
         P.lo = d_lo;
         P.ab = d_ab;
@@ -547,7 +548,7 @@ static void search_nodes_host(const uint64_t* lo, const uint8_t* isb, const uint
         P.next_win = next_win;
         P.cursor = small;
         P.active = active;
-        P.err = small + 3;
+        P.err = small + 4;
         P.dup = small + 2;
         P.leaf = sh.leaf;
         P.u1 = sh.u1;
@@ -561,7 +562,7 @@ static void search_nodes_host(const uint64_t* lo, const uint8_t* isb, const uint
         CK(cudaDeviceSynchronize());
     }
     uint32_t err = 0;
-    CK(cudaMemcpy(&err, small + 3, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&err, small + 4, 4, cudaMemcpyDeviceToHost));
     if (err) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
     CK(cudaMemcpy(out, values, n_nodes * 8, cudaMemcpyDeviceToHost));
 }

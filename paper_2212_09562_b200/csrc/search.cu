@@ -46,6 +46,7 @@ struct Args {
     u32 iters;
     u32 warp_cap;
     int help;
+    u32 tab_cap;  // u32 table entries per warp after the key buffer
 };
 
 // ------------------------------------------------------------------ trials --
@@ -133,6 +134,102 @@ __device__ __forceinline__ bool trial_bf(const u64* __restrict__ sk, u32 m, u64 
     return a == full;
 }
 
+// ---- fast path (all seeds of the window < 2^32).  Keys are read two at a time with
+// 16-byte shared-memory broadcasts; the packed-counter increment 1 << (w * part) comes
+// from a per-warp shared-memory table (tab[part], at most f distinct words -> no bank
+// conflicts) instead of IMAD + SHF, moving work off the saturated ALU/FMA-heavy pipes.
+// Full nodes index by part = remap(h, f); nodes with a smaller last part index a
+// table over v = remap(h, s) (tab[v] = 1 << (w * floor(v / unit))).
+
+template <bool CARRY>
+__device__ __forceinline__ u32 count_lower_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 s,
+                                                u32 sigma, u32 r) {
+    u32 c0 = 0, c1 = 0;
+    u32 j = 0;
+#pragma unroll 1
+    for (; j + 4 <= s; j += 4) {
+        const uint4 a = *reinterpret_cast<const uint4*>(sk + j);
+        const uint4 b = *reinterpret_cast<const uint4*>(sk + j + 2);
+        const u32 h0 = remix_hi_fast<CARRY>(a.x, a.y, sigma);
+        const u32 h1 = remix_hi_fast<CARRY>(a.z, a.w, sigma);
+        const u32 h2 = remix_hi_fast<CARRY>(b.x, b.y, sigma);
+        const u32 h3 = remix_hi_fast<CARRY>(b.z, b.w, sigma);
+        c0 += tab[__umulhi(h0, r)] + tab[__umulhi(h1, r)];
+        c1 += tab[__umulhi(h2, r)] + tab[__umulhi(h3, r)];
+    }
+    for (; j < s; ++j) {
+        const uint2 a = *reinterpret_cast<const uint2*>(sk + j);
+        c0 += tab[__umulhi(remix_hi_fast<CARRY>(a.x, a.y, sigma), r)];
+    }
+    return c0 + c1;
+}
+
+template <bool CARRY>
+__device__ __forceinline__ u32 count_left_fast(const u64* __restrict__ sk, u32 s, u32 sigma, u32 T) {
+    u32 c = 0;
+    u32 j = 0;
+#pragma unroll 1
+    for (; j + 4 <= s; j += 4) {
+        const uint4 a = *reinterpret_cast<const uint4*>(sk + j);
+        const uint4 b = *reinterpret_cast<const uint4*>(sk + j + 2);
+        c += (remix_hi_fast<CARRY>(a.x, a.y, sigma) < T) + (remix_hi_fast<CARRY>(a.z, a.w, sigma) < T);
+        c += (remix_hi_fast<CARRY>(b.x, b.y, sigma) < T) + (remix_hi_fast<CARRY>(b.z, b.w, sigma) < T);
+    }
+    for (; j < s; ++j) {
+        const uint2 a = *reinterpret_cast<const uint2*>(sk + j);
+        c += remix_hi_fast<CARRY>(a.x, a.y, sigma) < T;
+    }
+    return c;
+}
+
+// OR of 2^{remap(h, m)} over keys sk[j0..j1); bit = tab[v] (tab[v] = 1 << v)
+template <bool CARRY>
+__device__ __forceinline__ u32 mask_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 j0, u32 j1,
+                                         u32 m, u32 base) {
+    u32 a0 = 0, a1 = 0;
+    u32 j = j0;
+    for (; j + 2 <= j1; j += 2) {
+        const uint2 x = *reinterpret_cast<const uint2*>(sk + j);
+        const uint2 y = *reinterpret_cast<const uint2*>(sk + j + 1);
+        a0 |= tab[__umulhi(remix_hi_fast<CARRY>(x.x, x.y, base), m)];
+        a1 |= tab[__umulhi(remix_hi_fast<CARRY>(y.x, y.y, base), m)];
+    }
+    if (j < j1) {
+        const uint2 x = *reinterpret_cast<const uint2*>(sk + j);
+        a0 |= tab[__umulhi(remix_hi_fast<CARRY>(x.x, x.y, base), m)];
+    }
+    return a0 | a1;
+}
+
+template <bool CARRY>
+__device__ __forceinline__ int trial_rf_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 m, u32 nA,
+                                             u32 base, u32 full) {
+    const u32 a = mask_fast<CARRY>(sk, tab, 0, nA, m, base);
+    const u32 b = mask_fast<CARRY>(sk, tab, nA, m, m, base);
+    if (__popc(a) + __popc(b) != (int)m) return -1;
+    const u32 na = ~a & full;
+    const u64 bb = (u64)b | ((u64)b << m);
+    for (u32 r = 0; r < m; ++r)
+        if (((u32)(bb >> (m - r)) & full) == na) return (int)r;
+    return -1;
+}
+
+// One fast-path trial of `sig` for the node in sk (kind-specific predicate).
+template <int KIND, bool CARRY>
+__device__ __forceinline__ bool trial_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 s, u32 sig,
+                                           u32 c_f, u32 c_full, u32 c_mask, u32 c_target, int& r) {
+    if (KIND == SK_LEAF_RF) {
+        r = trial_rf_fast<CARRY>(sk, tab, s, c_f, sig * s, c_full);
+        return r >= 0;
+    } else if (KIND == SK_LEAF_BF) {
+        return mask_fast<CARRY>(sk, tab, 0, s, s, sig) == c_full;
+    } else if (KIND == SK_UPPER) {
+        return count_left_fast<CARRY>(sk, s, sig, c_mask) == c_target;
+    } else {
+        return (count_lower_fast<CARRY>(sk, tab, s, sig, c_full ? c_f : s) & c_mask) == c_target;
+    }
+}
+
 // ------------------------------------------------------------- scheduling --
 
 __device__ u32 find_help(const Args& A, u32 gw, u32 lane, u32 nn) {
@@ -158,8 +255,9 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
     extern __shared__ __align__(16) u64 smem[];
     const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const u32 gw = blockIdx.x * (blockDim.x >> 5) + wib;
-    u64* sk = smem + (size_t)wib * A.warp_cap;
-    if (*A.dup) return;  // duplicate keys: nothing can be found (checked by the host)
+    u64* sk = smem + (size_t)wib * (A.warp_cap + A.tab_cap / 2);
+    u32* tab = reinterpret_cast<u32*>(sk + A.warp_cap);
+    if (A.dup[0] || A.dup[1] > 1) return;  // duplicate keys: nothing can be found (host reports)
     const u32 nn = *A.n_nodes;
     const u64 ws = 32ull * A.iters;
 
@@ -167,6 +265,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
     // per-node constants: lower: f, w, target, mask, mu, full?; upper: T, c0; leaf: nA, full
     u32 c_f = 0, c_w = 0, c_target = 0, c_mask = 0, c_mu = 0, c_full = 0, c_wide = 0;
     u64 c_target64 = 0, c_mask64 = 0;
+    u32 c_margin = 0;
 
     for (;;) {
         if (node == NONE) {
@@ -194,10 +293,12 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
                 if (valid) sk[isb ? nA + __popc(bm & lt) : __popc(~bm & vm & lt)] = k;
                 c_f = nA;
                 c_full = (1u << s) - 1u;
+                tab[lane] = 1u << lane;
                 (void)vm;
             } else if (KIND == SK_LEAF_BF) {
                 if (lane < s) sk[lane] = A.lo[r.key_off + lane];
                 c_full = (1u << s) - 1u;
+                tab[lane] = 1u << lane;
             } else {
                 for (u32 j = lane; j < s; j += 32) sk[j] = A.lo[r.key_off + j];
                 if (KIND == SK_UPPER) {
@@ -218,6 +319,16 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
                         for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
                         c_target = t;
                         c_mask = (f - 1) * w >= 32 ? FULL : ((1u << ((f - 1) * w)) - 1u);
+                        // increment table: full node -> tab[part], part < f; otherwise
+                        // tab[v] for v = remap(h, s) < s (the last part adds nothing)
+                        if (c_full) {
+                            if (lane < f) tab[lane] = lane + 1 < f ? 1u << (lane * w) : 0u;
+                        } else {
+                            for (u32 v = lane; v < s; v += 32) {
+                                const u32 p = v / unit;
+                                tab[v] = p + 1 < f ? 1u << (p * w) : 0u;
+                            }
+                        }
                     } else {
                         u64 t = 0;
                         for (u32 j = 0; j + 1 < f; ++j) t += (u64)unit << (j * w);
@@ -227,6 +338,12 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
                 }
             }
             __syncwarp();
+            {  // carry margin: min over keys of 2^32 - 1 - k_lo
+                u32 mg = FULL;
+                for (u32 j = lane; j < s; j += 32) mg = min(mg, ~(u32)sk[j]);
+                for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
+                c_margin = mg;
+            }
         }
         u32 w = 0;
         u64 f = 0;
@@ -250,11 +367,24 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
             node = NONE;
             continue;
         }
+        // fast path: every value of the window fits 32 bits; no-carry path: additionally
+        // k_lo + value < 2^32 for every key of the node (margin c_margin)
+        const u64 last = KIND == SK_LEAF_RF ? (wstart + ws - 1) * s : wstart + ws - 1;
+        const bool fast = last < (1ull << 32);
+        const bool nocarry = fast && last <= c_margin;
         for (u32 it = 0; it < A.iters; ++it) {
             const u64 idx = wstart + (u64)it * 32 + lane;
             bool ok;
             int r = 0;
-            if (KIND == SK_LEAF_RF) {
+            if (fast) {
+                const u32 sig = (u32)idx;
+                if (KIND == SK_LOWER && c_wide)
+                    ok = (count_lower_wide(sk, s, idx, c_mu, c_w) & c_mask64) == c_target64;
+                else if (nocarry)
+                    ok = trial_fast<KIND, false>(sk, tab, s, sig, c_f, c_full, c_mask, c_target, r);
+                else
+                    ok = trial_fast<KIND, true>(sk, tab, s, sig, c_f, c_full, c_mask, c_target, r);
+            } else if (KIND == SK_LEAF_RF) {
                 r = trial_rf(sk, s, c_f, idx * s, c_full);
                 ok = r >= 0;
             } else if (KIND == SK_LEAF_BF) {
@@ -310,10 +440,12 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.iters = P.iters ? P.iters : 1;
     A.help = P.help;
     // warp-private key buffer (even number of u64 for 16-byte vector loads)
-    u32 cap = (P.max_size + 1) & ~1u;
+    u32 cap = (P.max_size + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
-    const size_t per_warp = (size_t)cap * sizeof(u64);
+    // increment table: leaves 32 entries, lower splits one entry per remap value
+    A.tab_cap = P.kind == SK_LOWER ? cap : (P.kind == SK_UPPER ? 0 : 32);
+    const size_t per_warp = (size_t)cap * sizeof(u64) + (size_t)A.tab_cap * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;

@@ -398,7 +398,9 @@ def test_split_minimal_by_bruteforce():
     """the returned seed gives exactly the prescribed part sizes, and every
     smaller seed does not (lower levels and the fanout-2 upper level)."""
     rng = np.random.default_rng(3)
-    cases = [(2, 3), (2, 4), (2, 9), (3, 7), (4, 9), (4, 20), (5, 12), (8, 30), (8, 33), (8, 100)]
+    # includes odd upper sizes s = 2 u2 + 1 where c0 = u2 < s/2 (l=2: 17, l=3: 25, l=8: 193)
+    cases = [(2, 3), (2, 4), (2, 9), (2, 17), (3, 7), (3, 25), (4, 9), (4, 20), (5, 12), (8, 30), (8, 33),
+             (8, 100), (8, 193)]
     for leaf, s in cases * 3:
         lo = rng.integers(0, M64, size=s, dtype=np.uint64, endpoint=True)
         sig = oracle.find_split(leaf, lo)

@@ -10,8 +10,10 @@ import torch
 import paper_2212_09562_b200 as rs
 import synth
 
-cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C3"]
+cfg = dict(synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C3"])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+if len(sys.argv) > 3:
+    cfg["n"] = int(float(sys.argv[3]))
 keys = synth.keys(cfg["n"], cfg["seed"])
 kt = torch.from_numpy(keys.view(np.int64)).cuda()
 for r in range(reps):
