@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librecsplit_b200.so")
+LIB_PATH = os.environ.get("RECSPLIT_LIB", os.path.join(_HERE, "lib", "librecsplit_b200.so"))
 
 OK, E_INVALID, E_DUPLICATE, E_NOMEM, E_CUDA, E_FORMAT, E_SEED_CAP = 0, -1, -2, -3, -4, -5, -6
 

@@ -13,8 +13,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT_DIR = os.path.join(HERE, "lib")
+OUT_DIR = os.environ.get("RS_BUILD_DIR", os.path.join(HERE, "lib"))
 LIB = os.path.join(OUT_DIR, "librecsplit_b200.so")
+EXTRA = os.environ.get("RS_NVCC_FLAGS", "").split()  # development experiments only
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -42,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         obj = os.path.join(obj_dir, src + ".o")
-        cmd = [NVCC, *ARCH, *common, "-c", path, "-o", obj]
+        cmd = [NVCC, *ARCH, *common, *EXTRA, "-c", path, "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-lineinfo", "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -76,7 +76,6 @@ __device__ __forceinline__ u32 remix_hi_fast(u32 kl, u32 kh, u32 sigma) {
             : "=r"(h)
             : "r"(kl), "r"(kh), "r"(sigma));
     } else {
-        // caller guarantees kl + sigma < 2^32 (per-node carry margin), so x_hi = k_hi
         asm("{\n\t"
             ".reg .u32 tl, th, wl, wh, yl, yh, zl, zh, a;\n\t"
             ".reg .u64 p64;\n\t"
@@ -89,6 +88,74 @@ __device__ __forceinline__ u32 remix_hi_fast(u32 kl, u32 kh, u32 sigma) {
     return h;
 }
 
+// Variants of the two adds of the no-carry path (ptxas tends to place plain adds on the
+// FMA-heavy pipe, which the multiplies already saturate); selected at build time.
+#ifndef RS_NC_VARIANT
+#define RS_NC_VARIANT 0  // measured fastest on B200 (tools/variant_bench.sh, round 1)
+#endif
+#if RS_NC_VARIANT == 0
+#define RS_NC_ADD1 "add.u32 xl, %1, %4;\n\t"
+#define RS_NC_MUL1                               \
+    "mul.wide.u32 p64, wl, 0x1ce4e5b9;\n\t"     \
+    "mov.b64 {yl, yh}, p64;\n\t"                \
+    "add.u32 yh, yh, %3;\n\t"                   \
+    "mad.lo.u32 yh, wl, 0xbf58476d, yh;\n\t"
+#elif RS_NC_VARIANT == 1
+// sad.u32 d, a, 0, c = |a - 0| + c: an add the integer ALU executes
+#define RS_NC_ADD1 "sad.u32 xl, %1, 0, %4;\n\t"
+#define RS_NC_MUL1                               \
+    "mul.wide.u32 p64, wl, 0x1ce4e5b9;\n\t"     \
+    "mov.b64 {yl, yh}, p64;\n\t"                \
+    "sad.u32 yh, yh, 0, %3;\n\t"                \
+    "mad.lo.u32 yh, wl, 0xbf58476d, yh;\n\t"
+#elif RS_NC_VARIANT == 3
+// sigma add left to ptxas (it picks IMAD.IADD, FMA pipe), kc add on the ALU
+#define RS_NC_ADD1 "add.u32 xl, %1, %4;\n\t"
+#define RS_NC_MUL1                               \
+    "mul.wide.u32 p64, wl, 0x1ce4e5b9;\n\t"     \
+    "mov.b64 {yl, yh}, p64;\n\t"                \
+    "sad.u32 yh, yh, 0, %3;\n\t"                \
+    "mad.lo.u32 yh, wl, 0xbf58476d, yh;\n\t"
+#else
+// low word by mul.lo, high word by mad.hi with kc as addend (no separate add)
+#define RS_NC_ADD1 "sad.u32 xl, %1, 0, %4;\n\t"
+#define RS_NC_MUL1                               \
+    "mul.lo.u32 yl, wl, 0x1ce4e5b9;\n\t"        \
+    "mad.hi.u32 yh, wl, 0x1ce4e5b9, %3;\n\t"    \
+    "mad.lo.u32 yh, wl, 0xbf58476d, yh;\n\t"
+#endif
+
+// Per-key constant of the no-carry path: with x_hi = k_hi, the high word of
+// w = x ^ (x >> 30) is k_hi ^ (k_hi >> 30), and its contribution to (w * C1)_hi is
+// the constant kc = (k_hi ^ (k_hi >> 30)) * C1_lo (mod 2^32).
+__device__ __forceinline__ u32 key_const(u32 kh) { return (kh ^ (kh >> 30)) * 0x1ce4e5b9u; }
+
+// remix_hi(k + sigma) when k_lo + sigma < 2^32: 8 heavy-pipe cycles (x*C1: IMAD.WIDE with
+// the 64-bit addend {0, kc} + one IMAD; x*C2 high word: IMAD.HI + 2 IMAD) and 8 ALU ops.
+__device__ __forceinline__ u32 remix_hi_nc(u32 kl, u32 kh, u32 kc, u32 sigma) {
+    u32 h;
+    asm("{\n\t"
+        ".reg .u32 xl, tl, th, wl, yl, yh, zl, zh, a;\n\t"
+        ".reg .u64 p64;\n\t"
+        RS_NC_ADD1
+        "shf.r.wrap.b32 tl, xl, %2, 30;\n\t"
+        "xor.b32 wl, xl, tl;\n\t"
+        RS_NC_MUL1
+        "shf.r.wrap.b32 tl, yl, yh, 27;\n\t"
+        "shr.u32 th, yh, 27;\n\t"
+        "xor.b32 zl, yl, tl;\n\t"
+        "xor.b32 zh, yh, th;\n\t"
+        "mul.hi.u32 a, zl, 0x133111eb;\n\t"
+        "mad.lo.u32 a, zl, 0x94d049bb, a;\n\t"
+        "mad.lo.u32 a, zh, 0x133111eb, a;\n\t"
+        "shr.u32 th, a, 31;\n\t"
+        "xor.b32 %0, a, th;\n\t"
+        "}"
+        : "=r"(h)
+        : "r"(kl), "r"(kh), "r"(kc), "r"(sigma));
+    return h;
+}
+
 // remap(h, r) = floor(h_hi * r / 2^32)  (R3) given h_hi
 __device__ __forceinline__ u32 remap_hi(u32 hhi, u32 r) { return __umulhi(hhi, r); }
 
@@ -96,6 +163,13 @@ __device__ __forceinline__ u32 remap_hi(u32 hhi, u32 r) { return __umulhi(hhi, r
 __device__ __forceinline__ u32 shl_clamp(u32 x, u32 s) {
     u32 r;
     asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+
+// 1 << s with clamping (s >= 32 gives 0), immediate source operand
+__device__ __forceinline__ u32 bit_clamp(u32 s) {
+    u32 r;
+    asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(s));
     return r;
 }
 

@@ -46,80 +46,140 @@ struct Args {
     u32 iters;
     u32 warp_cap;
     int help;
-    u32 tab_cap;  // u32 table entries per warp after the key buffer
 };
 
 // ------------------------------------------------------------------ trials --
+//
+// Warp-private shared memory holds the node's keys in groups of four (48 bytes):
+// [k_lo x4 | k_hi x4 | kc x4], kc = key_const(k_hi), so one pointer and three 16-byte
+// broadcast loads feed four evaluations.  Key j lives at word 12*(j/4) + (j%4).  Then
+// a byte table: shift amounts of the packed-counter increments (lower splits).
+// (A 64-bit {0, kc} addend for IMAD.WIDE was tried: ptxas splits it into IADD3 + IMAD.X.)
+//
+// Fast path (every value of the window < 2^32): when additionally k_lo + value < 2^32
+// for all keys of the node (checked once per window against the node's carry margin)
+// the no-carry evaluation remix_hi_nc is used; otherwise remix_hi_fast<true>.  Values
+// >= 2^32 (never at the measured configurations) take the generic 64-bit path.
 
-// Lower split, full node (s = f * unit): part = remap(h, f) = floor(h_hi f / 2^32)
-// (equals floor(remap(h, s) / unit) exactly).  Packed w-bit fields for parts
-// 0..f-2; the last part's increments land above the compared mask.
-__device__ __forceinline__ u32 count_lower_full(const u64* __restrict__ sk, u32 s, u64 sigma, u32 f,
-                                                u32 w) {
-    u32 cnt = 0;
-    u32 j = 0;
-#pragma unroll 2
-    for (; j + 2 <= s; j += 2) {
-        const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(sk + j);
-        const u32 h0 = remix_hi(kk.x + sigma);
-        const u32 h1 = remix_hi(kk.y + sigma);
-        cnt += shl_clamp(1u, __umulhi(h0, f) * w);
-        cnt += shl_clamp(1u, __umulhi(h1, f) * w);
-    }
-    if (j < s) cnt += shl_clamp(1u, __umulhi(remix_hi(sk[j] + sigma), f) * w);
-    return cnt;
+struct KeysView {
+    const u32* __restrict__ G;  // groups
+    u32 tbase;                  // shared-space byte address of the shift table
+};
+
+__device__ __forceinline__ u32 key_lo(const KeysView& K, u32 j) { return K.G[12 * (j >> 2) + (j & 3)]; }
+__device__ __forceinline__ u32 key_hi(const KeysView& K, u32 j) { return K.G[12 * (j >> 2) + 4 + (j & 3)]; }
+__device__ __forceinline__ u32 key_kc(const KeysView& K, u32 j) { return K.G[12 * (j >> 2) + 8 + (j & 3)]; }
+
+// h_hi of node_hash(key j, sigma) (R4): generic 64-bit path
+__device__ __forceinline__ u32 hash_slow(const KeysView& K, u32 j, u64 sigma) {
+    return remix_hi((((u64)key_hi(K, j) << 32) | key_lo(K, j)) + sigma);
 }
 
-// Lower split with a smaller last part: part = floor(remap(h, s) / unit) computed as
-// umulhi(remap, ceil(2^32/unit)) (exact for remap < 2^12, unit < 2^8).
-__device__ __forceinline__ u32 count_lower_partial(const u64* __restrict__ sk, u32 s, u64 sigma, u32 mu,
-                                                   u32 w) {
-    u32 cnt = 0;
-    u32 j = 0;
-#pragma unroll 2
-    for (; j + 2 <= s; j += 2) {
-        const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(sk + j);
-        const u32 h0 = remix_hi(kk.x + sigma);
-        const u32 h1 = remix_hi(kk.y + sigma);
-        cnt += shl_clamp(1u, __umulhi(__umulhi(h0, s), mu) * w);
-        cnt += shl_clamp(1u, __umulhi(__umulhi(h1, s), mu) * w);
+// evaluate the four keys of group g
+template <int MODE>  // 0: no-carry, 1: carry
+__device__ __forceinline__ void hash4(const u32* __restrict__ g, u32 sigma, u32 h[4]) {
+    const uint4 kl = *reinterpret_cast<const uint4*>(g);
+    const uint4 kh = *reinterpret_cast<const uint4*>(g + 4);
+    if (MODE == 0) {
+        const uint4 kc = *reinterpret_cast<const uint4*>(g + 8);
+        h[0] = remix_hi_nc(kl.x, kh.x, kc.x, sigma);
+        h[1] = remix_hi_nc(kl.y, kh.y, kc.y, sigma);
+        h[2] = remix_hi_nc(kl.z, kh.z, kc.z, sigma);
+        h[3] = remix_hi_nc(kl.w, kh.w, kc.w, sigma);
+    } else {
+        h[0] = remix_hi_fast<true>(kl.x, kh.x, sigma);
+        h[1] = remix_hi_fast<true>(kl.y, kh.y, sigma);
+        h[2] = remix_hi_fast<true>(kl.z, kh.z, sigma);
+        h[3] = remix_hi_fast<true>(kl.w, kh.w, sigma);
     }
-    if (j < s) cnt += shl_clamp(1u, __umulhi(__umulhi(remix_hi(sk[j] + sigma), s), mu) * w);
-    return cnt;
 }
 
-// Wide variant (fields do not fit 32 bits; l >= 19): 64-bit packed counter.
-__device__ __forceinline__ u64 count_lower_wide(const u64* __restrict__ sk, u32 s, u64 sigma, u32 mu,
-                                                u32 w) {
-    u64 cnt = 0;
-    for (u32 j = 0; j < s; ++j) {
-        const u32 part = __umulhi(__umulhi(remix_hi(sk[j] + sigma), s), mu);
-        cnt += 1ull << (part * w);
-    }
-    return cnt;
+template <int MODE>
+__device__ __forceinline__ u32 hash1(const KeysView& K, u32 j, u32 sigma) {
+    return MODE == 0 ? remix_hi_nc(key_lo(K, j), key_hi(K, j), key_kc(K, j), sigma)
+                     : remix_hi_fast<true>(key_lo(K, j), key_hi(K, j), sigma);
 }
 
-// Upper split: number of keys with remap(h, s) < c0  <=>  h_hi < T = ceil(c0 2^32 / s).
-__device__ __forceinline__ u32 count_left(const u64* __restrict__ sk, u32 s, u64 sigma, u32 T) {
+// increment 1 << table[remap(h, r)]: the byte address comes straight out of mad.hi
+// (hi(h * r) + table base), the shift amount is >= 32 for the last part (adds 0).
+__device__ __forceinline__ u32 inc_of(u32 h, u32 r, u32 tbase) {
+    u32 sh;
+    asm volatile("{\n\t.reg .u32 ad;\n\tmad.hi.u32 ad, %1, %2, %3;\n\tld.shared.u8 %0, [ad];\n\t}"
+                 : "=r"(sh)
+                 : "r"(h), "r"(r), "r"(tbase));
+    return bit_clamp(sh);
+}
+
+// Lower split: packed counter.  r = f for full nodes (part = remap(h, f)),
+// r = s otherwise (table over remap(h, s)).  RS_LOWER_UNROLL groups per loop trip.
+#ifndef RS_LOWER_UNROLL
+#define RS_LOWER_UNROLL 1
+#endif
+template <int MODE>
+__device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, u32 r) {
+    u32 c0 = 0, c1 = 0;
+    const u32 ng = s >> 2;
+    const u32* __restrict__ g = K.G;
+    u32 q = 0;
+#if RS_LOWER_UNROLL == 2
+#pragma unroll 1
+    for (; q + 2 <= ng; q += 2, g += 24) {
+        u32 h[4], e[4];
+        hash4<MODE>(g, sigma, h);
+        hash4<MODE>(g + 12, sigma, e);
+        c0 += inc_of(h[0], r, K.tbase) + inc_of(h[1], r, K.tbase);
+        c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
+        c0 += inc_of(e[0], r, K.tbase) + inc_of(e[1], r, K.tbase);
+        c1 += inc_of(e[2], r, K.tbase) + inc_of(e[3], r, K.tbase);
+    }
+#endif
+#pragma unroll 1
+    for (; q < ng; ++q, g += 12) {
+        u32 h[4];
+        hash4<MODE>(g, sigma, h);
+        c0 += inc_of(h[0], r, K.tbase) + inc_of(h[1], r, K.tbase);
+        c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
+    }
+    for (u32 j = ng << 2; j < s; ++j) c0 += inc_of(hash1<MODE>(K, j, sigma), r, K.tbase);
+    return c0 + c1;
+}
+
+// Upper split: |{k : remap(h_k, s) < c0}| = |{k : h_k < T}|, T = ceil(c0 2^32 / s).
+template <int MODE>
+__device__ __forceinline__ u32 count_left(const KeysView& K, u32 s, u32 sigma, u32 T) {
     u32 c = 0;
-    u32 j = 0;
-#pragma unroll 2
-    for (; j + 2 <= s; j += 2) {
-        const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(sk + j);
-        c += remix_hi(kk.x + sigma) < T;
-        c += remix_hi(kk.y + sigma) < T;
+    const u32 ng = s >> 2;
+    const u32* __restrict__ g = K.G;
+#pragma unroll 1
+    for (u32 q = 0; q < ng; ++q, g += 12) {
+        u32 h[4];
+        hash4<MODE>(g, sigma, h);
+        c += (h[0] < T) + (h[1] < T) + (h[2] < T) + (h[3] < T);
     }
-    if (j < s) c += remix_hi(sk[j] + sigma) < T;
+    for (u32 j = ng << 2; j < s; ++j) c += hash1<MODE>(K, j, sigma) < T;
     return c;
 }
 
-// Rotation fitting for one base seed: masks of A and B; if neither has
-// a collision, b fits the holes of a iff some rotation of b equals ~a.  Returns the
-// smallest such r, or -1.
-__device__ __forceinline__ int trial_rf(const u64* __restrict__ sk, u32 m, u32 nA, u64 base, u32 full) {
-    u32 a = 0, b = 0;
-    for (u32 j = 0; j < nA; ++j) a |= 1u << __umulhi(remix_hi(sk[j] + base), m);
-    for (u32 j = nA; j < m; ++j) b |= 1u << __umulhi(remix_hi(sk[j] + base), m);
+// OR of 2^{remap(h, m)} over the cnt keys starting at group g0.
+template <int MODE>
+__device__ __forceinline__ u32 leaf_mask(const KeysView& K, u32 g0, u32 cnt, u32 m, u32 base) {
+    u32 a0 = 0, a1 = 0;
+    const u32 ng = cnt >> 2;
+    const u32* __restrict__ g = K.G + 12 * g0;
+    for (u32 q = 0; q < ng; ++q, g += 12) {
+        u32 h[4];
+        hash4<MODE>(g, base, h);
+        a0 |= (1u << __umulhi(h[0], m)) | (1u << __umulhi(h[1], m));
+        a1 |= (1u << __umulhi(h[2], m)) | (1u << __umulhi(h[3], m));
+    }
+    for (u32 j = 4 * (g0 + ng); j < 4 * (g0 + ng) + (cnt & 3); ++j) a0 |= 1u << __umulhi(hash1<MODE>(K, j, base), m);
+    return a0 | a1;
+}
+
+// Rotation fitting for one base seed: masks of A and B; with no collision
+// inside A or B, b fits the holes of a iff some rotation of b equals ~a; the smallest
+// such r, or -1.
+__device__ __forceinline__ int fit_rotation(u32 a, u32 b, u32 m, u32 full) {
     if (__popc(a) + __popc(b) != (int)m) return -1;  // popcount pruning
     const u32 na = ~a & full;
     const u64 bb = (u64)b | ((u64)b << m);  // rot_m^r(b) = (bb >> (m - r)) & full
@@ -128,105 +188,63 @@ __device__ __forceinline__ int trial_rf(const u64* __restrict__ sk, u32 m, u32 n
     return -1;
 }
 
-__device__ __forceinline__ bool trial_bf(const u64* __restrict__ sk, u32 m, u64 sigma, u32 full) {
-    u32 a = 0;
-    for (u32 j = 0; j < m; ++j) a |= 1u << __umulhi(remix_hi(sk[j] + sigma), m);
-    return a == full;
-}
-
-// ---- fast path (all seeds of the window < 2^32).  Keys are read two at a time with
-// 16-byte shared-memory broadcasts; the packed-counter increment 1 << (w * part) comes
-// from a per-warp shared-memory table (tab[part], at most f distinct words -> no bank
-// conflicts) instead of IMAD + SHF, moving work off the saturated ALU/FMA-heavy pipes.
-// Full nodes index by part = remap(h, f); nodes with a smaller last part index a
-// table over v = remap(h, s) (tab[v] = 1 << (w * floor(v / unit))).
-
-template <bool CARRY>
-__device__ __forceinline__ u32 count_lower_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 s,
-                                                u32 sigma, u32 r) {
-    u32 c0 = 0, c1 = 0;
-    u32 j = 0;
-#pragma unroll 1
-    for (; j + 4 <= s; j += 4) {
-        const uint4 a = *reinterpret_cast<const uint4*>(sk + j);
-        const uint4 b = *reinterpret_cast<const uint4*>(sk + j + 2);
-        const u32 h0 = remix_hi_fast<CARRY>(a.x, a.y, sigma);
-        const u32 h1 = remix_hi_fast<CARRY>(a.z, a.w, sigma);
-        const u32 h2 = remix_hi_fast<CARRY>(b.x, b.y, sigma);
-        const u32 h3 = remix_hi_fast<CARRY>(b.z, b.w, sigma);
-        c0 += tab[__umulhi(h0, r)] + tab[__umulhi(h1, r)];
-        c1 += tab[__umulhi(h2, r)] + tab[__umulhi(h3, r)];
-    }
-    for (; j < s; ++j) {
-        const uint2 a = *reinterpret_cast<const uint2*>(sk + j);
-        c0 += tab[__umulhi(remix_hi_fast<CARRY>(a.x, a.y, sigma), r)];
-    }
-    return c0 + c1;
-}
-
-template <bool CARRY>
-__device__ __forceinline__ u32 count_left_fast(const u64* __restrict__ sk, u32 s, u32 sigma, u32 T) {
-    u32 c = 0;
-    u32 j = 0;
-#pragma unroll 1
-    for (; j + 4 <= s; j += 4) {
-        const uint4 a = *reinterpret_cast<const uint4*>(sk + j);
-        const uint4 b = *reinterpret_cast<const uint4*>(sk + j + 2);
-        c += (remix_hi_fast<CARRY>(a.x, a.y, sigma) < T) + (remix_hi_fast<CARRY>(a.z, a.w, sigma) < T);
-        c += (remix_hi_fast<CARRY>(b.x, b.y, sigma) < T) + (remix_hi_fast<CARRY>(b.z, b.w, sigma) < T);
-    }
-    for (; j < s; ++j) {
-        const uint2 a = *reinterpret_cast<const uint2*>(sk + j);
-        c += remix_hi_fast<CARRY>(a.x, a.y, sigma) < T;
-    }
-    return c;
-}
-
-// OR of 2^{remap(h, m)} over keys sk[j0..j1); bit = tab[v] (tab[v] = 1 << v)
-template <bool CARRY>
-__device__ __forceinline__ u32 mask_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 j0, u32 j1,
-                                         u32 m, u32 base) {
-    u32 a0 = 0, a1 = 0;
-    u32 j = j0;
-    for (; j + 2 <= j1; j += 2) {
-        const uint2 x = *reinterpret_cast<const uint2*>(sk + j);
-        const uint2 y = *reinterpret_cast<const uint2*>(sk + j + 1);
-        a0 |= tab[__umulhi(remix_hi_fast<CARRY>(x.x, x.y, base), m)];
-        a1 |= tab[__umulhi(remix_hi_fast<CARRY>(y.x, y.y, base), m)];
-    }
-    if (j < j1) {
-        const uint2 x = *reinterpret_cast<const uint2*>(sk + j);
-        a0 |= tab[__umulhi(remix_hi_fast<CARRY>(x.x, x.y, base), m)];
-    }
-    return a0 | a1;
-}
-
-template <bool CARRY>
-__device__ __forceinline__ int trial_rf_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 m, u32 nA,
-                                             u32 base, u32 full) {
-    const u32 a = mask_fast<CARRY>(sk, tab, 0, nA, m, base);
-    const u32 b = mask_fast<CARRY>(sk, tab, nA, m, m, base);
-    if (__popc(a) + __popc(b) != (int)m) return -1;
-    const u32 na = ~a & full;
-    const u64 bb = (u64)b | ((u64)b << m);
-    for (u32 r = 0; r < m; ++r)
-        if (((u32)(bb >> (m - r)) & full) == na) return (int)r;
-    return -1;
-}
-
-// One fast-path trial of `sig` for the node in sk (kind-specific predicate).
-template <int KIND, bool CARRY>
-__device__ __forceinline__ bool trial_fast(const u64* __restrict__ sk, const u32* __restrict__ tab, u32 s, u32 sig,
-                                           u32 c_f, u32 c_full, u32 c_mask, u32 c_target, int& r) {
+// One trial of `sig` (32-bit fast path) for the node.  Leaves: A keys occupy groups
+// 0..gB-1, B keys start at group gB (c_f = |A|).
+template <int KIND, int MODE>
+__device__ __forceinline__ bool trial_fast(const KeysView& K, u32 s, u32 sig, u32 c_f, u32 c_full, u32 c_mask,
+                                           u32 c_target, u32 gB, int& r) {
     if (KIND == SK_LEAF_RF) {
-        r = trial_rf_fast<CARRY>(sk, tab, s, c_f, sig * s, c_full);
+        const u32 base = sig * s;
+        const u32 a = leaf_mask<MODE>(K, 0, c_f, s, base);
+        const u32 b = leaf_mask<MODE>(K, gB, s - c_f, s, base);
+        r = fit_rotation(a, b, s, c_full);
         return r >= 0;
     } else if (KIND == SK_LEAF_BF) {
-        return mask_fast<CARRY>(sk, tab, 0, s, s, sig) == c_full;
+        return leaf_mask<MODE>(K, 0, s, s, sig) == c_full;
     } else if (KIND == SK_UPPER) {
-        return count_left_fast<CARRY>(sk, s, sig, c_mask) == c_target;
+        return count_left<MODE>(K, s, sig, c_mask) == c_target;
     } else {
-        return (count_lower_fast<CARRY>(sk, tab, s, sig, c_full ? c_f : s) & c_mask) == c_target;
+        return (count_lower<MODE>(K, s, sig, c_f) & c_mask) == c_target;
+    }
+}
+
+// Generic 64-bit path (values >= 2^32; also the wide 64-bit packed counters, l >= 19).
+// Leaf key j of B is stored at position 4*gB + (j - |A|).
+template <int KIND>
+__device__ __forceinline__ bool trial_slow(const KeysView& K, u32 s, u64 idx, u32 c_f, u32 c_full, u32 c_mu,
+                                           u32 c_w, u32 c_wide, u32 c_unit, u32 c_mask, u32 c_target, u64 c_mask64,
+                                           u64 c_target64, u32 gB, int& r) {
+    if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
+        const u64 base = KIND == SK_LEAF_RF ? idx * s : idx;
+        u32 a = 0, b = 0;
+        for (u32 j = 0; j < s; ++j) {
+            const bool inB = KIND == SK_LEAF_RF && j >= c_f;
+            const u32 pos = inB ? 4 * gB + (j - c_f) : j;
+            const u32 bit = 1u << __umulhi(hash_slow(K, pos, base), s);
+            if (inB)
+                b |= bit;
+            else
+                a |= bit;
+        }
+        if (KIND == SK_LEAF_BF) return a == c_full;
+        r = fit_rotation(a, b, s, c_full);
+        return r >= 0;
+    } else if (KIND == SK_UPPER) {
+        u32 c = 0;
+        for (u32 j = 0; j < s; ++j) c += hash_slow(K, j, idx) < c_mask;
+        return c == c_target;
+    } else {
+        if (c_wide) {
+            u64 c = 0;
+            for (u32 j = 0; j < s; ++j) c += 1ull << (__umulhi(__umulhi(hash_slow(K, j, idx), s), c_mu) * c_w);
+            return (c & c_mask64) == c_target64;
+        }
+        u32 c = 0;
+        for (u32 j = 0; j < s; ++j) {
+            const u32 part = __umulhi(hash_slow(K, j, idx), s) / c_unit;
+            c += shl_clamp(1u, part * c_w);  // the last part's increment lands above c_mask
+        }
+        return (c & c_mask) == c_target;
     }
 }
 
@@ -250,22 +268,31 @@ __device__ u32 find_help(const Args& A, u32 gw, u32 lane, u32 nn) {
     return NONE;
 }
 
+#ifndef RS_MIN_BLOCKS
+#define RS_MIN_BLOCKS 1
+#endif
 template <int KIND>
-__global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A) {
-    extern __shared__ __align__(16) u64 smem[];
+__global__ void __launch_bounds__(kWarpsPerBlockMax * 32, RS_MIN_BLOCKS) k_search(const Args A) {
+    extern __shared__ __align__(16) u32 smem32[];
     const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const u32 gw = blockIdx.x * (blockDim.x >> 5) + wib;
-    u64* sk = smem + (size_t)wib * (A.warp_cap + A.tab_cap / 2);
-    u32* tab = reinterpret_cast<u32*>(sk + A.warp_cap);
+    const u32 cap = A.warp_cap;                 // keys (multiple of 4)
+    const u32 gwords = 12 * (cap / 4 + 2);      // key groups (+2 for the leaf B alignment)
+    const u32 twords = (cap + 32 + 15) / 16 * 4;  // byte table of >= cap + 32 entries (16-byte multiple)
+    u32* G = smem32 + (size_t)wib * (gwords + twords);
+    u8* T8 = reinterpret_cast<u8*>(G + gwords);
+    const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
     if (A.dup[0] || A.dup[1] > 1) return;  // duplicate keys: nothing can be found (host reports)
     const u32 nn = *A.n_nodes;
     const u64 ws = 32ull * A.iters;
 
     u32 node = NONE, s = 0, slot = 0;
-    // per-node constants: lower: f, w, target, mask, mu, full?; upper: T, c0; leaf: nA, full
-    u32 c_f = 0, c_w = 0, c_target = 0, c_mask = 0, c_mu = 0, c_full = 0, c_wide = 0;
+    // per-node constants. lower: f, w, unit, full?, mu, r (table index range), target,
+    // mask (64-bit if wide); upper: c_mask = T, c_target = c0; leaves: c_f = |A|,
+    // c_full = 2^m - 1, gB = first group of the B keys.
+    u32 c_f = 0, c_w = 0, c_target = 0, c_mask = 0, c_mu = 0, c_full = 0, c_wide = 0, c_margin = 0;
+    u32 c_unit = 1, c_r = 1, gB = 0;
     u64 c_target64 = 0, c_mask64 = 0;
-    u32 c_margin = 0;
 
     for (;;) {
         if (node == NONE) {
@@ -282,25 +309,37 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
             const NodeRec r = A.nodes[n];
             s = r.size;
             slot = r.slot;
-            if (KIND == SK_LEAF_RF) {
-                // A keys first, then B keys (global 1-bit hash)
+            u32 mg = FULL;  // carry margin: min over keys of 2^32 - 1 - k_lo
+            if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
+                // RF: A keys in groups 0.., B keys from group gB (global 1-bit hash)
                 const bool valid = lane < s;
                 const u64 k = valid ? A.lo[r.key_off + lane] : 0;
-                const bool isb = valid && A.ab[r.key_off + lane];
+                const bool isb = KIND == SK_LEAF_RF && valid && A.ab[r.key_off + lane];
                 const u32 bm = __ballot_sync(FULL, isb), vm = __ballot_sync(FULL, valid);
                 const u32 nA = s - __popc(bm);
                 const u32 lt = lanemask_lt();
-                if (valid) sk[isb ? nA + __popc(bm & lt) : __popc(~bm & vm & lt)] = k;
+                gB = (nA + 3) / 4;
+                if (valid) {
+                    const u32 p = isb ? 4 * gB + __popc(bm & lt) : __popc(~bm & vm & lt);
+                    const u32 gp = 12 * (p >> 2), q = p & 3;
+                    const u32 kh = (u32)(k >> 32);
+                    G[gp + q] = (u32)k;
+                    G[gp + 4 + q] = kh;
+                    G[gp + 8 + q] = key_const(kh);
+                    mg = ~(u32)k;
+                }
                 c_f = nA;
                 c_full = (1u << s) - 1u;
-                tab[lane] = 1u << lane;
-                (void)vm;
-            } else if (KIND == SK_LEAF_BF) {
-                if (lane < s) sk[lane] = A.lo[r.key_off + lane];
-                c_full = (1u << s) - 1u;
-                tab[lane] = 1u << lane;
             } else {
-                for (u32 j = lane; j < s; j += 32) sk[j] = A.lo[r.key_off + j];
+                for (u32 j = lane; j < s; j += 32) {
+                    const u64 k = A.lo[r.key_off + j];
+                    const u32 gp = 12 * (j >> 2), q = j & 3;
+                    const u32 kh = (u32)(k >> 32);
+                    G[gp + q] = (u32)k;
+                    G[gp + 4 + q] = kh;
+                    G[gp + 8 + q] = key_const(kh);
+                    mg = min(mg, ~(u32)k);
+                }
                 if (KIND == SK_UPPER) {
                     const u32 c0 = (s / 2 + A.u2 - 1) / A.u2 * A.u2;  // R6
                     c_target = c0;
@@ -311,23 +350,21 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
                     const u32 w = 32 - __clz(unit + 1);  // bitwidth(unit + 1)
                     c_f = f;
                     c_w = w;
+                    c_unit = unit;
                     c_full = (s == f * unit);
                     c_mu = (u32)(((1ull << 32) + unit - 1) / unit);
                     c_wide = (f - 1) * w > 32;
+                    c_r = c_full ? f : s;
                     if (!c_wide) {
                         u32 t = 0;
                         for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
                         c_target = t;
                         c_mask = (f - 1) * w >= 32 ? FULL : ((1u << ((f - 1) * w)) - 1u);
-                        // increment table: full node -> tab[part], part < f; otherwise
-                        // tab[v] for v = remap(h, s) < s (the last part adds nothing)
-                        if (c_full) {
-                            if (lane < f) tab[lane] = lane + 1 < f ? 1u << (lane * w) : 0u;
-                        } else {
-                            for (u32 v = lane; v < s; v += 32) {
-                                const u32 p = v / unit;
-                                tab[v] = p + 1 < f ? 1u << (p * w) : 0u;
-                            }
+                        // shift table: part p -> p*w for p < f-1, 32 (adds 0) for the last part;
+                        // full nodes index by part, others by v = remap(h, s) (part = v / unit)
+                        for (u32 v = lane; v < c_r; v += 32) {
+                            const u32 p = c_full ? v : v / unit;
+                            T8[v] = (u8)(p + 1 < f ? p * w : 32);
                         }
                     } else {
                         u64 t = 0;
@@ -337,13 +374,9 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
                     }
                 }
             }
+            for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
+            c_margin = mg;
             __syncwarp();
-            {  // carry margin: min over keys of 2^32 - 1 - k_lo
-                u32 mg = FULL;
-                for (u32 j = lane; j < s; j += 32) mg = min(mg, ~(u32)sk[j]);
-                for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
-                c_margin = mg;
-            }
         }
         u32 w = 0;
         u64 f = 0;
@@ -367,38 +400,23 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32) k_search(const Args A)
             node = NONE;
             continue;
         }
-        // fast path: every value of the window fits 32 bits; no-carry path: additionally
-        // k_lo + value < 2^32 for every key of the node (margin c_margin)
+        // largest value (seed, or base seed k*m) any lane tries in this window
         const u64 last = KIND == SK_LEAF_RF ? (wstart + ws - 1) * s : wstart + ws - 1;
-        const bool fast = last < (1ull << 32);
+        const bool fast = last < (1ull << 32) && !(KIND == SK_LOWER && c_wide);
         const bool nocarry = fast && last <= c_margin;
         for (u32 it = 0; it < A.iters; ++it) {
             const u64 idx = wstart + (u64)it * 32 + lane;
-            bool ok;
             int r = 0;
-            if (fast) {
-                const u32 sig = (u32)idx;
-                if (KIND == SK_LOWER && c_wide)
-                    ok = (count_lower_wide(sk, s, idx, c_mu, c_w) & c_mask64) == c_target64;
-                else if (nocarry)
-                    ok = trial_fast<KIND, false>(sk, tab, s, sig, c_f, c_full, c_mask, c_target, r);
-                else
-                    ok = trial_fast<KIND, true>(sk, tab, s, sig, c_f, c_full, c_mask, c_target, r);
-            } else if (KIND == SK_LEAF_RF) {
-                r = trial_rf(sk, s, c_f, idx * s, c_full);
-                ok = r >= 0;
-            } else if (KIND == SK_LEAF_BF) {
-                ok = trial_bf(sk, s, idx, c_full);
-            } else if (KIND == SK_UPPER) {
-                ok = count_left(sk, s, idx, c_mask) == c_target;
-            } else {
-                if (c_wide)
-                    ok = (count_lower_wide(sk, s, idx, c_mu, c_w) & c_mask64) == c_target64;
-                else if (c_full)
-                    ok = (count_lower_full(sk, s, idx, c_f, c_w) & c_mask) == c_target;
-                else
-                    ok = (count_lower_partial(sk, s, idx, c_mu, c_w) & c_mask) == c_target;
-            }
+            bool ok;
+            if (nocarry)
+                ok = trial_fast<KIND, 0>(K, s, (u32)idx, KIND == SK_LOWER ? c_r : c_f, c_full, c_mask, c_target,
+                                         gB, r);
+            else if (fast)
+                ok = trial_fast<KIND, 1>(K, s, (u32)idx, KIND == SK_LOWER ? c_r : c_f, c_full, c_mask, c_target,
+                                         gB, r);
+            else
+                ok = trial_slow<KIND>(K, s, idx, c_f, c_full, c_mu, c_w, c_wide, c_unit, c_mask, c_target,
+                                      c_mask64, c_target64, gB, r);
             const u32 bal = __ballot_sync(FULL, ok);
             if (bal) {
                 const int win = __ffs(bal) - 1;
@@ -439,13 +457,11 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.u2 = P.u2;
     A.iters = P.iters ? P.iters : 1;
     A.help = P.help;
-    // warp-private key buffer (even number of u64 for 16-byte vector loads)
+    // warp-private buffer: key groups (12 words per 4 keys, +2 groups) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
-    // increment table: leaves 32 entries, lower splits one entry per remap value
-    A.tab_cap = P.kind == SK_LOWER ? cap : (P.kind == SK_UPPER ? 0 : 32);
-    const size_t per_warp = (size_t)cap * sizeof(u64) + (size_t)A.tab_cap * sizeof(u32);
+    const size_t per_warp = ((size_t)12 * (cap / 4 + 2) + (cap + 32 + 15) / 16 * 4) * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;
