@@ -12,11 +12,14 @@
 // Execution model (B200-first, not the paper's block-per-node design P:342-355):
 // a persistent grid of warps; lanes = consecutive seeds ("each lane one hash
 // function"); the node's keys sit in warp-private shared memory and are broadcast.
-// Work items are (node, seed window): warps open nodes from a global cursor and take
-// windows from a per-node dispenser, so idle warps join unfinished nodes (geometric
-// tails).  The winner is committed with atomicMin, so the stored value is the minimum
-// over all tried seeds; every window below the final minimum is dispensed and fully
-// processed before the kernel ends, hence the result equals the sequential search.
+//  * phases of large nodes ("help" mode): work items are (node, seed window); warps open
+//    nodes from a global cursor and take windows from a per-node dispenser, so idle warps
+//    join unfinished nodes (geometric tails).  The winner is committed with atomicMin,
+//    so the stored value is the minimum over all tried seeds; every window below the
+//    final minimum is dispensed and fully processed before the kernel ends, hence the
+//    result equals the sequential search.
+//  * phases of small nodes ("batch" mode): a warp takes `batch` nodes per cursor atomic
+//    and searches each alone, windows in increasing order, first hit wins.
 #include <algorithm>
 
 #include "kernels.h"
@@ -46,14 +49,17 @@ struct Args {
     u32 iters;
     u32 warp_cap;
     int help;
+    u32 batch;  // nodes per cursor atomic in batch mode
 };
 
 // ------------------------------------------------------------------ trials --
 //
-// Warp-private shared memory holds the node's keys in groups of four (48 bytes):
-// [k_lo x4 | k_hi x4 | kc x4], kc = key_const(k_hi), so one pointer and three 16-byte
-// broadcast loads feed four evaluations.  Key j lives at word 12*(j/4) + (j%4).  Then
-// a byte table: shift amounts of the packed-counter increments (lower splits).
+// Warp-private shared memory holds the node's keys in groups of four:
+// [k_lo x4 | k_hi x4 | kc x4] for splits (48 bytes), plus [mA x4 | mB x4] for leaves
+// (80 bytes), kc = key_const(k_hi), mA / mB = all-ones if the key is in A / B (R7) and 0
+// for padding keys, so leaves too are processed in whole groups.  Key j lives at word
+// GW*(j/4) + (j%4), GW = 12 or 20.  Then a byte table: shift amounts of the packed
+// counter increments (lower splits).
 // (A 64-bit {0, kc} addend for IMAD.WIDE was tried: ptxas splits it into IADD3 + IMAD.X.)
 //
 // Fast path (every value of the window < 2^32): when additionally k_lo + value < 2^32
@@ -61,18 +67,25 @@ struct Args {
 // the no-carry evaluation remix_hi_nc is used; otherwise remix_hi_fast<true>.  Values
 // >= 2^32 (never at the measured configurations) take the generic 64-bit path.
 
+template <int KIND>
+struct Layout {
+    static constexpr u32 GW = (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) ? 20 : 12;
+};
+
 struct KeysView {
     const u32* __restrict__ G;  // groups
     u32 tbase;                  // shared-space byte address of the shift table
 };
 
-__device__ __forceinline__ u32 key_lo(const KeysView& K, u32 j) { return K.G[12 * (j >> 2) + (j & 3)]; }
-__device__ __forceinline__ u32 key_hi(const KeysView& K, u32 j) { return K.G[12 * (j >> 2) + 4 + (j & 3)]; }
-__device__ __forceinline__ u32 key_kc(const KeysView& K, u32 j) { return K.G[12 * (j >> 2) + 8 + (j & 3)]; }
+template <u32 GW>
+__device__ __forceinline__ u32 key_word(const KeysView& K, u32 j, u32 field) {
+    return K.G[GW * (j >> 2) + 4 * field + (j & 3)];
+}
 
 // h_hi of node_hash(key j, sigma) (R4): generic 64-bit path
+template <u32 GW>
 __device__ __forceinline__ u32 hash_slow(const KeysView& K, u32 j, u64 sigma) {
-    return remix_hi((((u64)key_hi(K, j) << 32) | key_lo(K, j)) + sigma);
+    return remix_hi((((u64)key_word<GW>(K, j, 1) << 32) | key_word<GW>(K, j, 0)) + sigma);
 }
 
 // evaluate the four keys of group g
@@ -94,10 +107,10 @@ __device__ __forceinline__ void hash4(const u32* __restrict__ g, u32 sigma, u32 
     }
 }
 
-template <int MODE>
+template <int MODE, u32 GW>
 __device__ __forceinline__ u32 hash1(const KeysView& K, u32 j, u32 sigma) {
-    return MODE == 0 ? remix_hi_nc(key_lo(K, j), key_hi(K, j), key_kc(K, j), sigma)
-                     : remix_hi_fast<true>(key_lo(K, j), key_hi(K, j), sigma);
+    return MODE == 0 ? remix_hi_nc(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), key_word<GW>(K, j, 2), sigma)
+                     : remix_hi_fast<true>(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), sigma);
 }
 
 // increment 1 << table[remap(h, r)]: the byte address comes straight out of mad.hi
@@ -111,36 +124,20 @@ __device__ __forceinline__ u32 inc_of(u32 h, u32 r, u32 tbase) {
 }
 
 // Lower split: packed counter.  r = f for full nodes (part = remap(h, f)),
-// r = s otherwise (table over remap(h, s)).  RS_LOWER_UNROLL groups per loop trip.
-#ifndef RS_LOWER_UNROLL
-#define RS_LOWER_UNROLL 1
-#endif
+// r = s otherwise (table over remap(h, s)).
 template <int MODE>
 __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, u32 r) {
     u32 c0 = 0, c1 = 0;
     const u32 ng = s >> 2;
     const u32* __restrict__ g = K.G;
-    u32 q = 0;
-#if RS_LOWER_UNROLL == 2
 #pragma unroll 1
-    for (; q + 2 <= ng; q += 2, g += 24) {
-        u32 h[4], e[4];
-        hash4<MODE>(g, sigma, h);
-        hash4<MODE>(g + 12, sigma, e);
-        c0 += inc_of(h[0], r, K.tbase) + inc_of(h[1], r, K.tbase);
-        c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
-        c0 += inc_of(e[0], r, K.tbase) + inc_of(e[1], r, K.tbase);
-        c1 += inc_of(e[2], r, K.tbase) + inc_of(e[3], r, K.tbase);
-    }
-#endif
-#pragma unroll 1
-    for (; q < ng; ++q, g += 12) {
+    for (u32 q = 0; q < ng; ++q, g += 12) {
         u32 h[4];
         hash4<MODE>(g, sigma, h);
         c0 += inc_of(h[0], r, K.tbase) + inc_of(h[1], r, K.tbase);
         c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
     }
-    for (u32 j = ng << 2; j < s; ++j) c0 += inc_of(hash1<MODE>(K, j, sigma), r, K.tbase);
+    for (u32 j = ng << 2; j < s; ++j) c0 += inc_of(hash1<MODE, 12>(K, j, sigma), r, K.tbase);
     return c0 + c1;
 }
 
@@ -156,24 +153,31 @@ __device__ __forceinline__ u32 count_left(const KeysView& K, u32 s, u32 sigma, u
         hash4<MODE>(g, sigma, h);
         c += (h[0] < T) + (h[1] < T) + (h[2] < T) + (h[3] < T);
     }
-    for (u32 j = ng << 2; j < s; ++j) c += hash1<MODE>(K, j, sigma) < T;
+    for (u32 j = ng << 2; j < s; ++j) c += hash1<MODE, 12>(K, j, sigma) < T;
     return c;
 }
 
-// OR of 2^{remap(h, m)} over the cnt keys starting at group g0.
+// Leaf masks over all groups: a = OR of 2^{remap(h, m)} over A keys, b over B keys
+// (padding keys have mA = mB = 0).
 template <int MODE>
-__device__ __forceinline__ u32 leaf_mask(const KeysView& K, u32 g0, u32 cnt, u32 m, u32 base) {
-    u32 a0 = 0, a1 = 0;
-    const u32 ng = cnt >> 2;
-    const u32* __restrict__ g = K.G + 12 * g0;
-    for (u32 q = 0; q < ng; ++q, g += 12) {
+__device__ __forceinline__ void leaf_masks(const KeysView& K, u32 ng, u32 m, u32 base, u32& a, u32& b) {
+    u32 a0 = 0, b0 = 0;
+    const u32* __restrict__ g = K.G;
+#pragma unroll 1
+    for (u32 q = 0; q < ng; ++q, g += 20) {
         u32 h[4];
         hash4<MODE>(g, base, h);
-        a0 |= (1u << __umulhi(h[0], m)) | (1u << __umulhi(h[1], m));
-        a1 |= (1u << __umulhi(h[2], m)) | (1u << __umulhi(h[3], m));
+        const uint4 ma = *reinterpret_cast<const uint4*>(g + 12);
+        const uint4 mb = *reinterpret_cast<const uint4*>(g + 16);
+        const u32 t0 = 1u << __umulhi(h[0], m), t1 = 1u << __umulhi(h[1], m);
+        const u32 t2 = 1u << __umulhi(h[2], m), t3 = 1u << __umulhi(h[3], m);
+        a0 |= (t0 & ma.x) | (t1 & ma.y);
+        b0 |= (t0 & mb.x) | (t1 & mb.y);
+        a0 |= (t2 & ma.z) | (t3 & ma.w);
+        b0 |= (t2 & mb.z) | (t3 & mb.w);
     }
-    for (u32 j = 4 * (g0 + ng); j < 4 * (g0 + ng) + (cnt & 3); ++j) a0 |= 1u << __umulhi(hash1<MODE>(K, j, base), m);
-    return a0 | a1;
+    a = a0;
+    b = b0;
 }
 
 // Rotation fitting for one base seed: masks of A and B; with no collision
@@ -188,64 +192,170 @@ __device__ __forceinline__ int fit_rotation(u32 a, u32 b, u32 m, u32 full) {
     return -1;
 }
 
-// One trial of `sig` (32-bit fast path) for the node.  Leaves: A keys occupy groups
-// 0..gB-1, B keys start at group gB (c_f = |A|).
+// Per-node search state (registers).
+struct NodeCtx {
+    u32 s, slot;
+    u32 f, w, unit, full, mu, r, wide, target, mask, margin;
+    u64 target64, mask64;
+};
+
+// One trial of `sig` (32-bit fast path).  For rotation fitting r receives the rotation.
 template <int KIND, int MODE>
-__device__ __forceinline__ bool trial_fast(const KeysView& K, u32 s, u32 sig, u32 c_f, u32 c_full, u32 c_mask,
-                                           u32 c_target, u32 gB, int& r) {
-    if (KIND == SK_LEAF_RF) {
-        const u32 base = sig * s;
-        const u32 a = leaf_mask<MODE>(K, 0, c_f, s, base);
-        const u32 b = leaf_mask<MODE>(K, gB, s - c_f, s, base);
-        r = fit_rotation(a, b, s, c_full);
+__device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, u32 sig, int& r) {
+    if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
+        const u32 base = KIND == SK_LEAF_RF ? sig * c.s : sig;
+        u32 a, b;
+        leaf_masks<MODE>(K, (c.s + 3) >> 2, c.s, base, a, b);
+        if (KIND == SK_LEAF_BF) return a == c.full;
+        r = fit_rotation(a, b, c.s, c.full);
         return r >= 0;
-    } else if (KIND == SK_LEAF_BF) {
-        return leaf_mask<MODE>(K, 0, s, s, sig) == c_full;
     } else if (KIND == SK_UPPER) {
-        return count_left<MODE>(K, s, sig, c_mask) == c_target;
+        return count_left<MODE>(K, c.s, sig, c.mask) == c.target;
     } else {
-        return (count_lower<MODE>(K, s, sig, c_f) & c_mask) == c_target;
+        return (count_lower<MODE>(K, c.s, sig, c.r) & c.mask) == c.target;
     }
 }
 
 // Generic 64-bit path (values >= 2^32; also the wide 64-bit packed counters, l >= 19).
-// Leaf key j of B is stored at position 4*gB + (j - |A|).
 template <int KIND>
-__device__ __forceinline__ bool trial_slow(const KeysView& K, u32 s, u64 idx, u32 c_f, u32 c_full, u32 c_mu,
-                                           u32 c_w, u32 c_wide, u32 c_unit, u32 c_mask, u32 c_target, u64 c_mask64,
-                                           u64 c_target64, u32 gB, int& r) {
+__device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, u64 idx, int& r) {
+    constexpr u32 GW = Layout<KIND>::GW;
+    const u32 s = c.s;
     if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
         const u64 base = KIND == SK_LEAF_RF ? idx * s : idx;
         u32 a = 0, b = 0;
         for (u32 j = 0; j < s; ++j) {
-            const bool inB = KIND == SK_LEAF_RF && j >= c_f;
-            const u32 pos = inB ? 4 * gB + (j - c_f) : j;
-            const u32 bit = 1u << __umulhi(hash_slow(K, pos, base), s);
-            if (inB)
-                b |= bit;
-            else
-                a |= bit;
+            const u32 bit = 1u << __umulhi(hash_slow<GW>(K, j, base), s);
+            a |= bit & key_word<GW>(K, j, 3);
+            b |= bit & key_word<GW>(K, j, 4);
         }
-        if (KIND == SK_LEAF_BF) return a == c_full;
-        r = fit_rotation(a, b, s, c_full);
+        if (KIND == SK_LEAF_BF) return a == c.full;
+        r = fit_rotation(a, b, s, c.full);
         return r >= 0;
     } else if (KIND == SK_UPPER) {
-        u32 c = 0;
-        for (u32 j = 0; j < s; ++j) c += hash_slow(K, j, idx) < c_mask;
-        return c == c_target;
+        u32 cnt = 0;
+        for (u32 j = 0; j < s; ++j) cnt += hash_slow<GW>(K, j, idx) < c.mask;
+        return cnt == c.target;
     } else {
-        if (c_wide) {
-            u64 c = 0;
-            for (u32 j = 0; j < s; ++j) c += 1ull << (__umulhi(__umulhi(hash_slow(K, j, idx), s), c_mu) * c_w);
-            return (c & c_mask64) == c_target64;
+        if (c.wide) {
+            u64 cnt = 0;
+            for (u32 j = 0; j < s; ++j) cnt += 1ull << (__umulhi(__umulhi(hash_slow<GW>(K, j, idx), s), c.mu) * c.w);
+            return (cnt & c.mask64) == c.target64;
         }
-        u32 c = 0;
+        u32 cnt = 0;
         for (u32 j = 0; j < s; ++j) {
-            const u32 part = __umulhi(hash_slow(K, j, idx), s) / c_unit;
-            c += shl_clamp(1u, part * c_w);  // the last part's increment lands above c_mask
+            const u32 part = __umulhi(hash_slow<GW>(K, j, idx), s) / c.unit;
+            cnt += shl_clamp(1u, part * c.w);  // the last part's increment lands above mask
         }
-        return (c & c_mask) == c_target;
+        return (cnt & c.mask) == c.target;
     }
+}
+
+// Load node n's keys into the warp's buffer and derive its constants.
+template <int KIND>
+__device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G, u8* T8, NodeCtx& c) {
+    constexpr u32 GW = Layout<KIND>::GW;
+    const NodeRec rec = A.nodes[n];
+    c.s = rec.size;
+    c.slot = rec.slot;
+    const u32 s = c.s;
+    u32 mg = FULL;  // carry margin: min over keys of 2^32 - 1 - k_lo
+    if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
+        // natural key order; A/B select masks (global 1-bit hash); padding keys to
+        // the next multiple of four get zero masks
+        const bool valid = lane < s;
+        const u64 k = valid ? A.lo[rec.key_off + lane] : 0;
+        const bool isb = KIND == SK_LEAF_RF && valid && A.ab[rec.key_off + lane];
+        if (lane < ((s + 3) & ~3u)) {
+            const u32 gp = GW * (lane >> 2), q = lane & 3;
+            const u32 kh = (u32)(k >> 32);
+            G[gp + q] = (u32)k;
+            G[gp + 4 + q] = kh;
+            G[gp + 8 + q] = key_const(kh);
+            G[gp + 12 + q] = valid && !isb ? FULL : 0u;
+            G[gp + 16 + q] = isb ? FULL : 0u;
+        }
+        if (valid) mg = ~(u32)k;
+        c.full = (1u << s) - 1u;
+    } else {
+        for (u32 j = lane; j < s; j += 32) {
+            const u64 k = A.lo[rec.key_off + j];
+            const u32 gp = GW * (j >> 2), q = j & 3;
+            const u32 kh = (u32)(k >> 32);
+            G[gp + q] = (u32)k;
+            G[gp + 4 + q] = kh;
+            G[gp + 8 + q] = key_const(kh);
+            mg = min(mg, ~(u32)k);
+        }
+        if (KIND == SK_UPPER) {
+            const u32 c0 = (s / 2 + A.u2 - 1) / A.u2 * A.u2;  // R6
+            c.target = c0;
+            c.mask = (u32)((((u64)c0 << 32) + s - 1) / s);  // T = ceil(c0 2^32 / s)
+        } else {
+            const u32 unit = s <= A.u1 ? A.leaf : A.u1;
+            const u32 f = (s + unit - 1) / unit;
+            const u32 w = 32 - __clz(unit + 1);  // bitwidth(unit + 1)
+            c.f = f;
+            c.w = w;
+            c.unit = unit;
+            c.full = (s == f * unit);
+            c.mu = (u32)(((1ull << 32) + unit - 1) / unit);
+            c.wide = (f - 1) * w > 32;
+            c.r = c.full ? f : s;
+            if (!c.wide) {
+                u32 t = 0;
+                for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
+                c.target = t;
+                c.mask = (f - 1) * w >= 32 ? FULL : ((1u << ((f - 1) * w)) - 1u);
+                // shift table: part p -> p*w for p < f-1, 32 (adds 0) for the last part;
+                // full nodes index by part, others by v = remap(h, s) (part = v / unit)
+                for (u32 v = lane; v < c.r; v += 32) {
+                    const u32 p = c.full ? v : v / unit;
+                    T8[v] = (u8)(p + 1 < f ? p * w : 32);
+                }
+            } else {
+                u64 t = 0;
+                for (u32 j = 0; j + 1 < f; ++j) t += (u64)unit << (j * w);
+                c.target64 = t;
+                c.mask64 = (1ull << ((f - 1) * w)) - 1ull;
+            }
+        }
+    }
+    for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
+    c.margin = mg;
+    __syncwarp();
+}
+
+// Search the window [wstart, wstart + 32*iters) of base values (seeds, or base seeds k for
+// RF) in order; on a hit returns true with the stored value in *val (warp-uniform).
+template <int KIND>
+__device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
+                                           u32 lane, u64* val) {
+    const u64 ws = 32ull * A.iters;
+    // largest value (seed, or base seed k*m) any lane tries in this window
+    const u64 last = KIND == SK_LEAF_RF ? (wstart + ws - 1) * c.s : wstart + ws - 1;
+    const bool fast = last < (1ull << 32) && !(KIND == SK_LOWER && c.wide);
+    const bool nocarry = fast && last <= c.margin;
+    for (u32 it = 0; it < A.iters; ++it) {
+        const u64 idx = wstart + (u64)it * 32 + lane;
+        int r = 0;
+        bool ok;
+        if (nocarry)
+            ok = trial_fast<KIND, 0>(K, c, (u32)idx, r);
+        else if (fast)
+            ok = trial_fast<KIND, 1>(K, c, (u32)idx, r);
+        else
+            ok = trial_slow<KIND>(K, c, idx, r);
+        const u32 bal = __ballot_sync(FULL, ok);
+        if (bal) {
+            const int win = __ffs(bal) - 1;
+            u64 v = wstart + (u64)it * 32 + win;
+            if (KIND == SK_LEAF_RF) v = v * c.s + (u32)__shfl_sync(FULL, r, win);
+            *val = v;
+            return true;
+        }
+    }
+    return false;
 }
 
 // ------------------------------------------------------------- scheduling --
@@ -272,122 +382,73 @@ __device__ u32 find_help(const Args& A, u32 gw, u32 lane, u32 nn) {
 #define RS_MIN_BLOCKS 1
 #endif
 template <int KIND>
-__global__ void __launch_bounds__(kWarpsPerBlockMax * 32, RS_MIN_BLOCKS) k_search(const Args A) {
+__global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 : RS_MIN_BLOCKS) k_search(const Args A) {
+    constexpr u32 GW = Layout<KIND>::GW;
     extern __shared__ __align__(16) u32 smem32[];
     const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const u32 gw = blockIdx.x * (blockDim.x >> 5) + wib;
-    const u32 cap = A.warp_cap;                 // keys (multiple of 4)
-    const u32 gwords = 12 * (cap / 4 + 2);      // key groups (+2 for the leaf B alignment)
-    const u32 twords = (cap + 32 + 15) / 16 * 4;  // byte table of >= cap + 32 entries (16-byte multiple)
+    const u32 cap = A.warp_cap;                    // keys (multiple of 4)
+    const u32 gwords = GW * (cap / 4 + 1);         // key groups
+    const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
     u32* G = smem32 + (size_t)wib * (gwords + twords);
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
     const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
     if (A.dup[0] || A.dup[1] > 1) return;  // duplicate keys: nothing can be found (host reports)
     const u32 nn = *A.n_nodes;
     const u64 ws = 32ull * A.iters;
+    NodeCtx c{};
 
-    u32 node = NONE, s = 0, slot = 0;
-    // per-node constants. lower: f, w, unit, full?, mu, r (table index range), target,
-    // mask (64-bit if wide); upper: c_mask = T, c_target = c0; leaves: c_f = |A|,
-    // c_full = 2^m - 1, gB = first group of the B keys.
-    u32 c_f = 0, c_w = 0, c_target = 0, c_mask = 0, c_mu = 0, c_full = 0, c_wide = 0, c_margin = 0;
-    u32 c_unit = 1, c_r = 1, gB = 0;
-    u64 c_target64 = 0, c_mask64 = 0;
+    if (!A.help) {
+        // batch mode: A.batch nodes per cursor atomic, each searched alone
+        for (;;) {
+            u32 n0 = 0;
+            if (lane == 0) n0 = atomicAdd(A.cursor, A.batch);
+            n0 = __shfl_sync(FULL, n0, 0);
+            if (n0 >= nn) break;
+            const u32 n1 = min(n0 + A.batch, nn);
+            for (u32 n = n0; n < n1; ++n) {
+                load_node<KIND>(A, n, lane, G, T8, c);
+                u64 val = 0;
+                for (u64 wstart = 0;; wstart += ws) {
+                    if (wstart >= kSeedCap) {
+                        if (lane == 0) atomicOr(A.err, 1u);
+                        val = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
+                        break;
+                    }
+                    if (run_window<KIND>(A, K, c, wstart, lane, &val)) break;
+                }
+                if (lane == 0) A.values[c.slot] = val;
+                __syncwarp();
+            }
+        }
+        return;
+    }
 
+    // help mode: per-node window dispenser + helping
+    u32 node = NONE;
     for (;;) {
         if (node == NONE) {
             u32 n = 0;
             if (lane == 0) n = atomicAdd(A.cursor, 1u);
             n = __shfl_sync(FULL, n, 0);
             if (n >= nn) {
-                if (!A.help) break;
                 n = find_help(A, gw, lane, nn);
                 if (n == NONE) break;
             }
             node = n;
             if (lane == 0) ((volatile int*)A.active)[gw] = (int)n;
-            const NodeRec r = A.nodes[n];
-            s = r.size;
-            slot = r.slot;
-            u32 mg = FULL;  // carry margin: min over keys of 2^32 - 1 - k_lo
-            if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
-                // RF: A keys in groups 0.., B keys from group gB (global 1-bit hash)
-                const bool valid = lane < s;
-                const u64 k = valid ? A.lo[r.key_off + lane] : 0;
-                const bool isb = KIND == SK_LEAF_RF && valid && A.ab[r.key_off + lane];
-                const u32 bm = __ballot_sync(FULL, isb), vm = __ballot_sync(FULL, valid);
-                const u32 nA = s - __popc(bm);
-                const u32 lt = lanemask_lt();
-                gB = (nA + 3) / 4;
-                if (valid) {
-                    const u32 p = isb ? 4 * gB + __popc(bm & lt) : __popc(~bm & vm & lt);
-                    const u32 gp = 12 * (p >> 2), q = p & 3;
-                    const u32 kh = (u32)(k >> 32);
-                    G[gp + q] = (u32)k;
-                    G[gp + 4 + q] = kh;
-                    G[gp + 8 + q] = key_const(kh);
-                    mg = ~(u32)k;
-                }
-                c_f = nA;
-                c_full = (1u << s) - 1u;
-            } else {
-                for (u32 j = lane; j < s; j += 32) {
-                    const u64 k = A.lo[r.key_off + j];
-                    const u32 gp = 12 * (j >> 2), q = j & 3;
-                    const u32 kh = (u32)(k >> 32);
-                    G[gp + q] = (u32)k;
-                    G[gp + 4 + q] = kh;
-                    G[gp + 8 + q] = key_const(kh);
-                    mg = min(mg, ~(u32)k);
-                }
-                if (KIND == SK_UPPER) {
-                    const u32 c0 = (s / 2 + A.u2 - 1) / A.u2 * A.u2;  // R6
-                    c_target = c0;
-                    c_mask = (u32)((((u64)c0 << 32) + s - 1) / s);  // T = ceil(c0 2^32 / s)
-                } else {
-                    const u32 unit = s <= A.u1 ? A.leaf : A.u1;
-                    const u32 f = (s + unit - 1) / unit;
-                    const u32 w = 32 - __clz(unit + 1);  // bitwidth(unit + 1)
-                    c_f = f;
-                    c_w = w;
-                    c_unit = unit;
-                    c_full = (s == f * unit);
-                    c_mu = (u32)(((1ull << 32) + unit - 1) / unit);
-                    c_wide = (f - 1) * w > 32;
-                    c_r = c_full ? f : s;
-                    if (!c_wide) {
-                        u32 t = 0;
-                        for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
-                        c_target = t;
-                        c_mask = (f - 1) * w >= 32 ? FULL : ((1u << ((f - 1) * w)) - 1u);
-                        // shift table: part p -> p*w for p < f-1, 32 (adds 0) for the last part;
-                        // full nodes index by part, others by v = remap(h, s) (part = v / unit)
-                        for (u32 v = lane; v < c_r; v += 32) {
-                            const u32 p = c_full ? v : v / unit;
-                            T8[v] = (u8)(p + 1 < f ? p * w : 32);
-                        }
-                    } else {
-                        u64 t = 0;
-                        for (u32 j = 0; j + 1 < f; ++j) t += (u64)unit << (j * w);
-                        c_target64 = t;
-                        c_mask64 = (1ull << ((f - 1) * w)) - 1ull;
-                    }
-                }
-            }
-            for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
-            c_margin = mg;
-            __syncwarp();
+            load_node<KIND>(A, n, lane, G, T8, c);
         }
         u32 w = 0;
         u64 f = 0;
         if (lane == 0) {
-            w = atomicAdd(A.next_win + slot, 1u);
-            f = ld_volatile_u64(A.values + slot);
+            w = atomicAdd(A.next_win + c.slot, 1u);
+            f = ld_volatile_u64(A.values + c.slot);
         }
         w = __shfl_sync(FULL, w, 0);
         f = shfl64(f, 0);
         const u64 wstart = (u64)w * ws;
-        const u64 lb = KIND == SK_LEAF_RF ? wstart * s : wstart;
+        const u64 lb = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
         if (lb >= f) {  // a smaller value is already committed: node finished for us
             node = NONE;
             continue;
@@ -395,37 +456,14 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, RS_MIN_BLOCKS) k_searc
         if (wstart >= kSeedCap) {
             if (lane == 0) {
                 atomicOr(A.err, 1u);
-                atomicMin((unsigned long long*)(A.values + slot), (unsigned long long)lb);
+                atomicMin((unsigned long long*)(A.values + c.slot), (unsigned long long)lb);
             }
             node = NONE;
             continue;
         }
-        // largest value (seed, or base seed k*m) any lane tries in this window
-        const u64 last = KIND == SK_LEAF_RF ? (wstart + ws - 1) * s : wstart + ws - 1;
-        const bool fast = last < (1ull << 32) && !(KIND == SK_LOWER && c_wide);
-        const bool nocarry = fast && last <= c_margin;
-        for (u32 it = 0; it < A.iters; ++it) {
-            const u64 idx = wstart + (u64)it * 32 + lane;
-            int r = 0;
-            bool ok;
-            if (nocarry)
-                ok = trial_fast<KIND, 0>(K, s, (u32)idx, KIND == SK_LOWER ? c_r : c_f, c_full, c_mask, c_target,
-                                         gB, r);
-            else if (fast)
-                ok = trial_fast<KIND, 1>(K, s, (u32)idx, KIND == SK_LOWER ? c_r : c_f, c_full, c_mask, c_target,
-                                         gB, r);
-            else
-                ok = trial_slow<KIND>(K, s, idx, c_f, c_full, c_mu, c_w, c_wide, c_unit, c_mask, c_target,
-                                      c_mask64, c_target64, gB, r);
-            const u32 bal = __ballot_sync(FULL, ok);
-            if (bal) {
-                const int win = __ffs(bal) - 1;
-                u64 val = wstart + (u64)it * 32 + win;
-                if (KIND == SK_LEAF_RF) val = val * s + (u32)__shfl_sync(FULL, r, win);
-                if (lane == 0) atomicMin((unsigned long long*)(A.values + slot), (unsigned long long)val);
-                break;
-            }
-        }
+        u64 val;
+        if (run_window<KIND>(A, K, c, wstart, lane, &val) && lane == 0)
+            atomicMin((unsigned long long*)(A.values + c.slot), (unsigned long long)val);
     }
 }
 
@@ -457,11 +495,12 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.u2 = P.u2;
     A.iters = P.iters ? P.iters : 1;
     A.help = P.help;
-    // warp-private buffer: key groups (12 words per 4 keys, +2 groups) + byte shift table
+    // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
-    const size_t per_warp = ((size_t)12 * (cap / 4 + 2) + (cap + 32 + 15) / 16 * 4) * sizeof(u32);
+    const u32 GW = (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) ? 20 : 12;
+    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4) * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;
@@ -476,8 +515,14 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     if (occ < 1) occ = 1;
     int max_blocks = (int)(search_active_slots(P.sm_count) / wpb);
     u32 grid = (u32)std::min(occ * P.sm_count, max_blocks);
-    // no point in more warps than nodes when helping is off
-    if (!P.help) grid = std::min<u32>(grid, (P.n_nodes_host + wpb - 1) / wpb);
+    // batch mode: about 8 batches per resident warp, at most 8 nodes per batch
+    A.batch = 1;
+    if (!P.help) {
+        const u64 slots = (u64)grid * wpb;
+        u64 b = P.n_nodes_host / (slots * 8);
+        A.batch = (u32)std::max<u64>(1, std::min<u64>(8, b));
+        grid = std::min<u32>(grid, (P.n_nodes_host + A.batch * wpb - 1) / (A.batch * wpb));
+    }
     if (grid == 0) grid = 1;
     A.n_warps = grid * wpb;
     switch (P.kind) {
