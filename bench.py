@@ -180,26 +180,38 @@ def main():
 
     import paper_2212_09562_b200 as rs
 
+    backend = os.environ.get("RS_BENCH_BACKEND", "nccl")  # gloo: functional runs of N ranks on 1 GPU
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dev_index = 0 if os.environ.get("RS_BENCH_SAME_DEVICE") else local
+        torch.cuda.set_device(dev_index)
+        dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    # weak scaling: each rank builds its own 5e6-key MPHF (independent key sets)
-    keys = synth.keys(cfg["n"], cfg["seed"] + 1000 * rank)
+    # weak scaling: N ranks build ONE MPHF of N x n keys, each rank owning 1/N of the
+    # buckets (bucket-range sharding); every rank holds all keys in HBM
+    n_total = cfg["n"] * world
+    keys = synth.keys(n_total, cfg["seed"])
     kt = torch.from_numpy(keys.view(np.int64)).cuda()
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
+    def build_once(keys_tensor):
+        if world == 1:
+            return rs.build_device(keys_tensor, cfg["leaf"], cfg["bucket"], stream=stream, stats=True)
+        blob = rs.build_sharded(keys_tensor, cfg["leaf"], cfg["bucket"], stream=stream)
+        return blob, None
+
     def one_step():
         flush.zero_()  # L2 flush (inputs are 40 MB < 126 MB L2)
+        if world > 1:
+            torch.distributed.barrier()
         a = torch.cuda.Event(enable_timing=True)
         z = torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        blob, st = rs.build_device(kt, cfg["leaf"], cfg["bucket"], stream=stream, stats=True)
+        blob, st = build_once(kt)
         z.record(stream)
         z.synchronize()
         return a.elapsed_time(z) * 1e-3, blob, st
@@ -213,42 +225,59 @@ def main():
     times, stats = [], []
     blob = None
     for _ in range(args.steps):
-        t, blob, st = one_step()
+        t, b, st = one_step()
         times.append(t)
         stats.append(st)
+        blob = b if b is not None else blob
     torch.cuda.synchronize()
     clocks = clk.stop()
     if world > 1:
         torch.distributed.barrier()
     mean_t = float(np.mean(times))
-    t_all = torch.tensor([mean_t], dtype=torch.float64, device="cuda")
+    t_all = torch.tensor([mean_t], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
     if world > 1:
         torch.distributed.all_reduce(t_all, op=torch.distributed.ReduceOp.MAX)
     t_max = float(t_all.item())
-    value = cfg["n"] * world / t_max
+    value = n_total / t_max
 
-    # ---- e2e: host keys through recsplit_build, H2D + D2H inside the timed region
+    # ---- e2e: host keys through the public API, H2D + D2H inside the timed region
     pinned = torch.from_numpy(keys.view(np.int64)).pin_memory()
     pkeys = pinned.numpy().view(np.uint64)
-    rs.build(pkeys, cfg["leaf"], cfg["bucket"])  # warm
+
+    def e2e_once():
+        if world == 1:
+            return rs.build(pkeys, cfg["leaf"], cfg["bucket"])
+        kd = pinned.to("cuda", non_blocking=True)
+        return rs.build_sharded(kd, cfg["leaf"], cfg["bucket"], stream=stream)
+
+    e2e_once()  # warm
     e2e_times = []
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        eb = rs.build(pkeys, cfg["leaf"], cfg["bucket"])
+        eb = e2e_once()
         e2e_times.append(time.perf_counter() - t0)
-    e2e_t = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64, device="cuda")
+    e2e_t = torch.tensor([float(np.mean(e2e_times))], dtype=torch.float64,
+                         device="cuda" if backend == "nccl" else "cpu")
     if world > 1:
         torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = cfg["n"] * world / float(e2e_t.item())
-    assert eb == blob, "host-input and device-input builds differ"
+    e2e_value = n_total / float(e2e_t.item())
+    if rank == 0:
+        assert eb == blob, "host-input and device-input builds differ"
 
     if rank != 0:
         torch.distributed.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (lower-level-1 split search)
+    # ---- roofline of the dominant kernel (lower-level-1 split search), from the
+    # single-GPU build's own CUDA events (N > 1: measured by one extra 1-GPU build)
+    if stats[0] is None:
+        blob1, st1 = rs.build_device(kt[: cfg["n"]].contiguous(), cfg["leaf"], cfg["bucket"], stream=stream,
+                                     stats=True)
+        stats = [st1]
     cls = 2
     evals = float(np.mean([s["algo_evals"][cls] for s in stats]))
     kt_s = float(np.mean([s["t_search"][cls] for s in stats]))
@@ -270,12 +299,13 @@ def main():
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": (value / world / PAPER_KEYS_PER_S[args.config]) if args.config in PAPER_KEYS_PER_S else None,
         "dtype": "u64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_TEXT[args.config], "n": cfg["n"], "leaf": cfg["leaf"],
+        "config": {"workload": WORKLOAD_TEXT[args.config], "n": n_total, "leaf": cfg["leaf"],
                    "bucket": cfg["bucket"], "keys_per_rank": cfg["n"], "l2": "flushed between steps",
-                   "bits_per_key": rs.bits_per_key(blob), "parallelism": f"replicas{world}" if world > 1 else "1gpu"},
-        "e2e": {"value": e2e_value, "unit": "keys/s", "h2d_bytes_per_step": int(cfg["n"] * 8),
+                   "bits_per_key": rs.bits_per_key(blob),
+                   "parallelism": f"bucket-range shards x{world} (one MPHF)" if world > 1 else "1gpu"},
+        "e2e": {"value": e2e_value, "unit": "keys/s", "h2d_bytes_per_step": int(n_total * 8),
                 "d2h_bytes_per_step": len(blob)},
-        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) * (args.steps if world > 1 else 1),
         "roofline": {"bound": "alu", "kernel": "k_search<SK_LOWER> (lower level 1 splits)",
                      "achieved": achieved, "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
                      "traffic": traffic,
@@ -286,7 +316,7 @@ def main():
         "algo_evals_per_step": [int(x) for x in st0["algo_evals"]],
         "clocks": clocks,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only
         k, t, nb = cpu_sample(cfg, keys, args.cpu_budget, threads)
         line["cpu_baseline"] = {"value": k / t, "unit": "keys/s", "cores": threads, "kind": "oracle",
                                 "sample": f"{nb} whole buckets ({k} keys) of the {args.config} workload, "

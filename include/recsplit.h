@@ -160,6 +160,37 @@ RECSPLIT_API int recsplit_search_splits(const uint64_t *lo, const uint32_t *off,
  * (leaf if s <= leaf_size), computed by the library's own host code. */
 RECSPLIT_API int recsplit_tau(uint32_t leaf_size, uint32_t s, uint32_t rotation_fitting);
 
+/*
+ * Sharded construction (buckets are independent; contiguous bucket ranges per
+ * worker; per-worker sequences concatenated and one Elias-Fano index over all buckets).
+ * Rank r of `world` owns buckets [floor(r B / W), floor((r+1) B / W)), B = ceil(n / b).
+ * Every rank passes ALL n keys (DEVICE pointer, on its own device); the output bytes are
+ * identical to recsplit_build's for any world size.  Protocol (collectives are the
+ * caller's, e.g. torch.distributed over NCCL):
+ *   1. recsplit_shard_begin            -> 8-word summary of this rank
+ *   2. allgather the summaries (world x 8 u64, rank order)
+ *   3. recsplit_shard_min_step(all)    -> this rank's minimum residual step (int64)
+ *   4. allreduce-min of the steps
+ *   5. recsplit_shard_finish(min)      -> this rank's part (bytes)
+ *   6. gather the parts; recsplit_stitch(parts of ranks 0..W-1) -> serialized MPHF
+ * A duplicate key or a seed-cap error on any rank makes step 3 fail on every rank.
+ * The handle owns device memory until recsplit_shard_free.
+ */
+typedef struct recsplit_shard recsplit_shard;
+RECSPLIT_API int recsplit_shard_begin(const uint64_t *d_keys, size_t n, uint32_t leaf_size,
+                                      uint32_t bucket_size, const recsplit_options *opt, int32_t rank,
+                                      int32_t world, void *stream, recsplit_shard **out,
+                                      uint64_t summary[8]);
+RECSPLIT_API int recsplit_shard_min_step(recsplit_shard *sh, const uint64_t *summaries,
+                                         int64_t *min_step);
+RECSPLIT_API int recsplit_shard_finish(recsplit_shard *sh, int64_t min_step, recsplit_bytes *part);
+RECSPLIT_API int recsplit_stitch(const uint8_t *const *parts, const size_t *sizes, int32_t count,
+                                 recsplit_bytes *out);
+RECSPLIT_API void recsplit_shard_free(recsplit_shard *sh); /* NULL-safe */
+/* Host arithmetic of step 3 (tests): out = {n, D, delta_C, beta, key_base, bit_base}. */
+RECSPLIT_API int recsplit_shard_globals(const uint64_t *summaries, int32_t world, int32_t rank,
+                                        uint64_t out[6]);
+
 RECSPLIT_API void recsplit_free(recsplit_bytes *b); /* NULL-safe; zeroes *b */
 RECSPLIT_API void recsplit_free_ptr(void *p);
 RECSPLIT_API const char *recsplit_last_error(void);

@@ -22,7 +22,9 @@ SYMBOLS = [
     "recsplit_version", "recsplit_max_bucket_keys", "recsplit_build", "recsplit_build_ex",
     "recsplit_build_device", "recsplit_build_values", "recsplit_query", "recsplit_query_many",
     "recsplit_bits_per_key", "recsplit_search_leaves", "recsplit_search_splits", "recsplit_tau",
-    "recsplit_free", "recsplit_free_ptr", "recsplit_last_error",
+    "recsplit_free", "recsplit_free_ptr", "recsplit_last_error", "recsplit_shard_begin",
+    "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch", "recsplit_shard_free",
+    "recsplit_shard_globals",
 ]
 
 
@@ -90,6 +92,17 @@ def lib():
         L.recsplit_free_ptr.argtypes = [C.c_void_p]
         L.recsplit_free_ptr.restype = None
         L.recsplit_last_error.restype = C.c_char_p
+        L.recsplit_shard_begin.argtypes = [C.c_void_p, sz, u32, u32, C.POINTER(Options), C.c_int32, C.c_int32,
+                                           C.c_void_p, C.POINTER(C.c_void_p), P64]
+        L.recsplit_shard_min_step.argtypes = [C.c_void_p, P64, C.POINTER(C.c_int64)]
+        L.recsplit_shard_finish.argtypes = [C.c_void_p, C.c_int64, C.POINTER(Bytes)]
+        L.recsplit_stitch.argtypes = [C.POINTER(C.c_void_p), C.POINTER(C.c_size_t), C.c_int32, C.POINTER(Bytes)]
+        L.recsplit_shard_free.argtypes = [C.c_void_p]
+        L.recsplit_shard_free.restype = None
+        L.recsplit_shard_globals.argtypes = [P64, C.c_int32, C.c_int32, P64]
+        for name in ("recsplit_shard_begin", "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch",
+                     "recsplit_shard_globals"):
+            getattr(L, name).restype = i32
         for name in ("recsplit_build", "recsplit_build_ex", "recsplit_build_device", "recsplit_build_values",
                      "recsplit_query", "recsplit_query_many", "recsplit_bits_per_key",
                      "recsplit_search_leaves", "recsplit_search_splits", "recsplit_tau"):
@@ -210,3 +223,128 @@ def search_splits(lo, offsets, leaf_size: int) -> np.ndarray:
 
 def tau(leaf_size: int, s: int, rotation_fitting: bool = True) -> int:
     return _check(lib().recsplit_tau(leaf_size, s, int(rotation_fitting)))
+
+
+# ---------------------------------------------------------------- sharded builds --
+
+class Shard:
+    """One rank's share of a sharded build (include/recsplit.h, recsplit_shard_*)."""
+
+    def __init__(self, keys_tensor, leaf_size: int, bucket_size: int, rank: int, world: int,
+                 rotation_fitting: bool = True, global_seed: int = 0, stream=None):
+        import torch
+
+        if not keys_tensor.is_cuda or not keys_tensor.is_contiguous() or keys_tensor.element_size() != 8:
+            raise ValueError("keys_tensor must be a contiguous 8-byte CUDA tensor")
+        if stream is None:
+            stream = torch.cuda.current_stream(keys_tensor.device)
+        self._h = C.c_void_p()
+        self.summary = np.zeros(8, dtype=np.uint64)
+        o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, 0)
+        _check(lib().recsplit_shard_begin(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), leaf_size,
+                                          bucket_size, C.byref(o), rank, world, C.c_void_p(stream.cuda_stream),
+                                          C.byref(self._h), _p64(self.summary)))
+
+    def min_step(self, summaries: np.ndarray) -> int:
+        s = np.ascontiguousarray(summaries, dtype=np.uint64).reshape(-1)
+        out = C.c_int64()
+        _check(lib().recsplit_shard_min_step(self._h, _p64(s), C.byref(out)))
+        return out.value
+
+    def finish(self, min_step: int) -> bytes:
+        b = Bytes()
+        _check(lib().recsplit_shard_finish(self._h, min_step, C.byref(b)))
+        return _take(b)
+
+    def close(self):
+        if self._h:
+            lib().recsplit_shard_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def stitch(parts) -> bytes:
+    """Serialized MPHF from the parts of ranks 0..W-1 (host)."""
+    bufs = [np.frombuffer(p, dtype=np.uint8) for p in parts]
+    ptrs = (C.c_void_p * len(bufs))(*[b.ctypes.data for b in bufs])
+    sizes = (C.c_size_t * len(bufs))(*[len(b) for b in bufs])
+    out = Bytes()
+    _check(lib().recsplit_stitch(ptrs, sizes, len(bufs), C.byref(out)))
+    return _take(out)
+
+
+def shard_globals(summaries, world: int, rank: int) -> dict:
+    s = np.ascontiguousarray(summaries, dtype=np.uint64).reshape(-1)
+    out = np.zeros(6, dtype=np.uint64)
+    _check(lib().recsplit_shard_globals(_p64(s), world, rank, _p64(out)))
+    return dict(zip(("n", "D", "delta_C", "beta", "key_base", "bit_base"), (int(x) for x in out)))
+
+
+def exchange_summaries(summary: np.ndarray, group=None) -> np.ndarray:
+    """allgather of the 8-word summaries over torch.distributed (NCCL or gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.from_numpy(summary.view(np.int64).copy()).to(dev)
+    out = torch.empty(world * 8, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out.cpu().numpy().view(np.uint64).reshape(world, 8)
+
+
+def allreduce_min(x: int, group=None) -> int:
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return int(t.item())
+
+
+def gather_parts(part: bytes, dst: int = 0, group=None):
+    """Variable-length byte parts to rank dst (list on dst, None elsewhere)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    n = torch.tensor([len(part)], dtype=torch.int64, device=dev)
+    sizes = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(sizes, n, group=group)
+    sizes = sizes.cpu().tolist()
+    mx = max(sizes)
+    buf = torch.zeros(mx, dtype=torch.uint8)
+    buf[:len(part)] = torch.frombuffer(bytearray(part), dtype=torch.uint8)
+    buf = buf.to(dev)
+    out = torch.empty(world * mx, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    if dist.get_rank(group) != dst:
+        return None
+    host = out.cpu().numpy()
+    return [host[r * mx: r * mx + sizes[r]].tobytes() for r in range(world)]
+
+
+def build_sharded(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
+                  global_seed: int = 0, group=None, stream=None):
+    """Multi-GPU build of ONE MPHF over the torch.distributed group (one rank per GPU):
+    bucket ranges per rank, allgather of summaries, allreduce-min of the residual step,
+    parts gathered to rank 0 and stitched.  Returns the bytes on rank 0, None elsewhere."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    sh = Shard(keys_tensor, leaf_size, bucket_size, rank, world, rotation_fitting, global_seed, stream)
+    try:
+        allsum = exchange_summaries(sh.summary, group)
+        step = allreduce_min(sh.min_step(allsum), group)
+        part = sh.finish(step)
+    finally:
+        sh.close()
+    parts = gather_parts(part, 0, group)
+    return stitch(parts) if parts is not None else None

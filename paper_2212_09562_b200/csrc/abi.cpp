@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -473,6 +474,87 @@ int recsplit_tau(uint32_t leaf_size, uint32_t s, uint32_t rotation_fitting) {
     if (s == 0) return 0;
     auto T = rs::get_tables(leaf_size, rotation_fitting != 0, s);
     return (int)T->tau[s];
+}
+
+struct recsplit_shard {
+    std::unique_ptr<rs::Shard> shard;
+    int device = -1;
+};
+
+int recsplit_shard_begin(const uint64_t* d_keys, size_t n, uint32_t leaf_size, uint32_t bucket_size,
+                         const recsplit_options* opt, int32_t rank, int32_t world, void* stream, recsplit_shard** out,
+                         uint64_t summary[8]) {
+    if (!out || !summary || !d_keys) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(RECSPLIT_E_INVALID, "bad rank/world");
+    int rc = check_args(n, leaf_size, bucket_size);
+    if (rc) return rc;
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        rs::BuildParams p = params_of(n, leaf_size, bucket_size, opt);
+        select_device(p.device);
+        auto* h = new recsplit_shard;
+        try {
+            h->shard.reset(new rs::Shard(d_keys, p, rank, world, (cudaStream_t)stream, false));
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        cudaGetDevice(&h->device);
+        memcpy(summary, h->shard->summary, 64);
+        *out = h;
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_shard_min_step(recsplit_shard* sh, const uint64_t* summaries, int64_t* min_step) {
+    if (!sh || !summaries || !min_step) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        cudaSetDevice(sh->device);
+        *min_step = sh->shard->min_step(summaries);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_shard_finish(recsplit_shard* sh, int64_t min_step, recsplit_bytes* part) {
+    if (!sh || !part) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    part->data = nullptr;
+    part->size = 0;
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        cudaSetDevice(sh->device);
+        rs::BuildOutput o;
+        sh->shard->finish(min_step == INT64_MAX ? 0 : min_step, o.bytes);
+        return emit(o, part);
+    });
+}
+
+int recsplit_stitch(const uint8_t* const* parts, const size_t* sizes, int32_t count, recsplit_bytes* out) {
+    if (!parts || !sizes || !out || count < 1) return fail(RECSPLIT_E_INVALID, "bad arguments");
+    out->data = nullptr;
+    out->size = 0;
+    return guarded([&]() -> int {
+        std::vector<std::pair<const uint8_t*, size_t>> v;
+        for (int i = 0; i < count; ++i) v.emplace_back(parts[i], sizes[i]);
+        rs::BuildOutput o;
+        rs::stitch(v, o.bytes);
+        return emit(o, out);
+    });
+}
+
+void recsplit_shard_free(recsplit_shard* sh) {
+    if (!sh) return;
+    cudaSetDevice(sh->device);
+    delete sh;
+}
+
+int recsplit_shard_globals(const uint64_t* summaries, int32_t world, int32_t rank, uint64_t out[6]) {
+    if (!summaries || !out || world < 1 || rank < 0 || rank >= world) return fail(RECSPLIT_E_INVALID, "bad arguments");
+    rs::Globals G = rs::compute_globals(summaries, world, rank);
+    const uint64_t v[6] = {G.n, G.D, G.dC, G.beta, G.key_base, G.bit_base};
+    memcpy(out, v, sizeof v);
+    return RECSPLIT_OK;
 }
 
 void recsplit_free(recsplit_bytes* b) {

@@ -187,19 +187,20 @@ void launch_write_data(const u64* C, u64 B, const u64* nodebase, const u32* tsta
 
 // ------------------------------------------------------------ Elias-Fano --
 
-__device__ __forceinline__ long long resid(const u64* C, const u64* P, u64 i, u64 beta) {
-    // R[i] = P[i] - floor(beta C[i] / 2^20) (128-bit product)
-    const u64 c = C[i] - C[0];
-    const u64 p = P[i] - P[0];
-    const u64 lo = beta * c, hi = __umul64hi(beta, c);
+__device__ __forceinline__ u64 glob_C(const u64* C, const IndexView& v, u64 l) { return v.key_base + C[l]; }
+
+__device__ __forceinline__ long long resid(const u64* C, const u64* P, const IndexView& v, u64 l) {
+    // R[i] = P[i] - floor(beta C[i] / 2^20) with the global C, P (128-bit product)
+    const u64 c = glob_C(C, v, l);
+    const u64 p = v.bit_base + P[l];
+    const u64 lo = v.beta * c, hi = __umul64hi(v.beta, c);
     return (long long)p - (long long)((lo >> 20) | (hi << 44));
 }
 
-__global__ void k_min_residual(const u64* __restrict__ C, const u64* __restrict__ P, u64 B, u64 beta,
-                               long long* out) {
+__global__ void k_min_residual(const u64* __restrict__ C, const u64* __restrict__ P, IndexView v, long long* out) {
     long long m = LLONG_MAX;
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += (u64)gridDim.x * blockDim.x) {
-        const long long d = resid(C, P, i + 1, beta) - resid(C, P, i, beta);
+    for (u64 l = (u64)blockIdx.x * blockDim.x + threadIdx.x; l < v.nb; l += (u64)gridDim.x * blockDim.x) {
+        const long long d = resid(C, P, v, l + 1) - resid(C, P, v, l);
         m = d < m ? d : m;
     }
     for (int dd = 16; dd; dd >>= 1) {
@@ -209,35 +210,34 @@ __global__ void k_min_residual(const u64* __restrict__ C, const u64* __restrict_
     if ((threadIdx.x & 31) == 0) atomicMin(out, m);
 }
 
-void launch_min_residual(const u64* C, const u64* P, u64 B, u64 beta, long long* out, cudaStream_t st) {
-    unsigned grid = (unsigned)((B + 255) / 256);
+void launch_min_residual(const u64* C, const u64* P, IndexView v, long long* out, cudaStream_t st) {
+    if (v.nb == 0) return;
+    unsigned grid = (unsigned)((v.nb + 255) / 256);
     if (grid > 1024) grid = 1024;
-    if (grid == 0) grid = 1;
-    k_min_residual<<<grid, 256, 0, st>>>(C, P, B, beta, out);
+    k_min_residual<<<grid, 256, 0, st>>>(C, P, v, out);
     g_launches++;
 }
 
-// EF: lower L bits of v_i at i*L; upper bit (v_i >> L) + i.
-__global__ void k_ef_write(const u64* __restrict__ C, const u64* __restrict__ P, u64 B, u64 dC, u64 beta,
-                           long long dR, u32 LC, u32 LP, unsigned long long* c_low, unsigned long long* c_up,
-                           unsigned long long* p_low, unsigned long long* p_up) {
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i <= B; i += (u64)gridDim.x * blockDim.x) {
-        const u64 cp = (C[i] - C[0]) - i * dC;
-        const u64 pp = (u64)(resid(C, P, i, beta) - (long long)i * dR);
-        or_bits(c_low, i * LC, cp, LC);
-        or_bits(p_low, i * LP, pp, LP);
-        const u64 uc = (cp >> LC) + i, up = (pp >> LP) + i;
-        atomicOr(c_up + (uc >> 6), 1ull << (uc & 63));
-        atomicOr(p_up + (up >> 6), 1ull << (up & 63));
+// EF: lower L bits of v_i at i*L; upper bit (v_i >> L) + i (global positions,
+// stored relative to the slice start).
+__global__ void k_ef_write(const u64* __restrict__ C, const u64* __restrict__ P, IndexView v, u64 cnt, EfSlices e) {
+    for (u64 l = (u64)blockIdx.x * blockDim.x + threadIdx.x; l < cnt; l += (u64)gridDim.x * blockDim.x) {
+        const u64 i = v.b0 + l;
+        const u64 cp = glob_C(C, v, l) - i * e.dC;
+        const u64 pp = (u64)(resid(C, P, v, l) - (long long)i * e.dR);
+        or_bits(e.cl, i * e.LC - e.cl_start, cp, e.LC);
+        or_bits(e.pl, i * e.LP - e.pl_start, pp, e.LP);
+        const u64 uc = (cp >> e.LC) + i - e.cu_start, up = (pp >> e.LP) + i - e.pu_start;
+        atomicOr(e.cu + (uc >> 6), 1ull << (uc & 63));
+        atomicOr(e.pu + (up >> 6), 1ull << (up & 63));
     }
 }
 
-void launch_ef_write(const u64* C, const u64* P, u64 B, u64 dC, u64 beta, long long dR, u32 LC, u32 LP,
-                     unsigned long long* c_low, unsigned long long* c_up, unsigned long long* p_low,
-                     unsigned long long* p_up, cudaStream_t st) {
-    unsigned grid = (unsigned)((B + 256) / 256);
+void launch_ef_write(const u64* C, const u64* P, IndexView v, u64 cnt, EfSlices e, cudaStream_t st) {
+    if (cnt == 0) return;
+    unsigned grid = (unsigned)((cnt + 255) / 256);
     if (grid > 4096) grid = 4096;
-    k_ef_write<<<grid, 256, 0, st>>>(C, P, B, dC, beta, dR, LC, LP, c_low, c_up, p_low, p_up);
+    k_ef_write<<<grid, 256, 0, st>>>(C, P, v, cnt, e);
     g_launches++;
 }
 

@@ -24,7 +24,8 @@ void exscan_u64(const u64* in, u64* out, size_t n, void* temp, cudaStream_t st);
 // ---- partition (partition.cu), steps A1-A2 of SURVEY section 8(a).
 // master hash code -> lo, A/B bit, bucket id; bucket histogram (zeroed); duplicate
 // detection through a zeroed open-addressing set of (set_mask+1) u64 slots (dup[0..1] zeroed).
-void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64* lo, u8* ab, u32* bkt, u32* hist,
+// keys of buckets [b0, b1) only (local bucket ids; others get bkt = NONE)
+void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt, u32* hist,
                  unsigned long long* set, u64 set_mask, u32* dup, cudaStream_t st);
 // max/min bucket size and presence bitmap of sizes (present must be zeroed, cap+1 bytes)
 void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u8* present, u32 cap,
@@ -79,12 +80,26 @@ void launch_bucket_bits(const u64* C, u64 B, const u64* nodebase, const u32* tst
 void launch_write_data(const u64* C, u64 B, const u64* nodebase, const u32* tstart,
                        const rsd::TNodeD* tnodes, const u64* F, const u64* values, const u64* P,
                        unsigned long long* words, cudaStream_t st);
-// min over i of R[i+1]-R[i], R[i] = P[i] - floor(beta C[i] / 2^20)
-void launch_min_residual(const u64* C, const u64* P, u64 B, u64 beta, long long* out,
-                         cudaStream_t st);
-// EF lower/upper bits of C'[i] = C[i] - i dC and P'[i] = R[i] - i dR
-void launch_ef_write(const u64* C, const u64* P, u64 B, u64 dC, u64 beta, long long dR, u32 LC,
-                     u32 LP, unsigned long long* c_low, unsigned long long* c_up,
-                     unsigned long long* p_low, unsigned long long* p_up, cudaStream_t st);
+// Global view of a shard's bucket range for the index (R13): global bucket i = b0 + l,
+// C_g = key_base + C_l, P_g = bit_base + P_l, R[i] = P_g[i] - floor(beta C_g[i] / 2^20).
+struct IndexView {
+    u64 b0;        // first global bucket of the shard
+    u64 nb;        // local buckets (local arrays have nb + 1 entries)
+    u64 key_base;  // keys before the shard
+    u64 bit_base;  // Golomb-Rice bits before the shard
+    u64 beta;      // floor(D 2^20 / n)
+};
+// min over local steps l in [0, nb) of R[l+1] - R[l] (atomicMin into *out)
+void launch_min_residual(const u64* C, const u64* P, IndexView v, long long* out, cudaStream_t st);
+// EF slices of entries l in [0, cnt): C'[i] = C_g[i] - i dC and P'[i] = R[i] - i dR; lower bits
+// at global bit i*L, upper bit at (v >> L) + i; written relative to each slice's start bit.
+struct EfSlices {
+    u32 LC, LP;
+    u64 dC;
+    long long dR;
+    u64 cl_start, cu_start, pl_start, pu_start;  // global start bit of each slice
+    unsigned long long *cl, *cu, *pl, *pu;
+};
+void launch_ef_write(const u64* C, const u64* P, IndexView v, u64 cnt, EfSlices e, cudaStream_t st);
 
 }  // namespace rs

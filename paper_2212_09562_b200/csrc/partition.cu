@@ -14,20 +14,29 @@ using namespace rsd;
 // (the set replaces a per-bucket sort: the output depends only on the key set of each
 // node, never on the order of keys inside a bucket).  Bucket histogram in shared
 // memory when B is small (one global atomic per bucket per block), else global.
-__global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64 n, u64 g, u64 B,
-                                               u64* __restrict__ lo, u8* __restrict__ ab, u32* __restrict__ bkt,
-                                               u32* __restrict__ hist, unsigned long long* __restrict__ set,
-                                               u64 set_mask, u32* dup, int smem_hist) {
+// Only buckets in [b0, b1) (this shard, P:320 contiguous bucket ranges) are kept; their
+// local index b - b0 goes to bkt, other keys get bkt = NONE.
+__global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u64 b0,
+                                               u64 b1, u64* __restrict__ lo, u8* __restrict__ ab,
+                                               u32* __restrict__ bkt, u32* __restrict__ hist,
+                                               unsigned long long* __restrict__ set, u64 set_mask, u32* dup,
+                                               int smem_hist) {
     extern __shared__ u32 sh[];
+    const u64 Bl = b1 - b0;
     if (smem_hist) {
-        for (u32 i = threadIdx.x; i < B; i += blockDim.x) sh[i] = 0;
+        for (u32 i = threadIdx.x; i < Bl; i += blockDim.x) sh[i] = 0;
         __syncthreads();
     }
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 k = keys[i] ^ g;
         const u64 h = remix64(k ^ MHC_SALT_HI);
+        const u64 bg = ((h >> 32) * B) >> 32;
+        if (bg < b0 || bg >= b1) {
+            bkt[i] = NONE;
+            continue;
+        }
+        const u32 b = (u32)(bg - b0);
         const u64 l = remix64(k ^ MHC_SALT_LO);
-        const u32 b = (u32)(((h >> 32) * B) >> 32);
         lo[i] = l;
         ab[i] = (u8)(h & 1);
         bkt[i] = b;
@@ -54,21 +63,22 @@ __global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64
     }
     if (smem_hist) {
         __syncthreads();
-        for (u32 i = threadIdx.x; i < B; i += blockDim.x)
+        for (u32 i = threadIdx.x; i < Bl; i += blockDim.x)
             if (sh[i]) atomicAdd(hist + i, sh[i]);
     }
 }
 
-void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64* lo, u8* ab, u32* bkt, u32* hist,
+void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt, u32* hist,
                  unsigned long long* set, u64 set_mask, u32* dup, cudaStream_t st) {
-    const int smem_hist = B <= 12288;
-    const size_t smem = smem_hist ? B * 4 : 0;
+    const u64 Bl = b1 - b0;
+    const int smem_hist = Bl <= 12288;
+    const size_t smem = smem_hist ? Bl * 4 : 0;
     unsigned grid = (unsigned)((n + 1023) / 1024);
     const unsigned cap = smem_hist ? 148u * 2u : 148u * 8u;
     if (grid > cap) grid = cap;
     if (grid == 0) grid = 1;
     cudaFuncSetAttribute(k_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    k_hash<<<grid, 1024, smem, st>>>(keys, n, g, B, lo, ab, bkt, hist, set, set_mask, dup, smem_hist);
+    k_hash<<<grid, 1024, smem, st>>>(keys, n, g, B, b0, b1, lo, ab, bkt, hist, set, set_mask, dup, smem_hist);
     g_launches++;
 }
 
@@ -110,17 +120,17 @@ __global__ void k_scatter(const u64* __restrict__ lo, const u8* __restrict__ ab,
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const u64 i = i0 + k * stride;
-            b[k] = i < n ? bkt[i] : 0;
+            b[k] = i < n ? bkt[i] : NONE;
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const u64 i = i0 + k * stride;
-            if (i < n) p[k] = atomicAdd(cursor + b[k], 1ull);
+            if (i < n && b[k] != NONE) p[k] = atomicAdd(cursor + b[k], 1ull);
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const u64 i = i0 + k * stride;
-            if (i < n) {
+            if (i < n && b[k] != NONE) {
                 lo2[p[k]] = lo[i];
                 ab2[p[k]] = ab[i];
             }

@@ -158,17 +158,6 @@ const DevTables& device_tables(int dev, uint32_t leaf, bool rf, uint32_t smax, c
     return D;
 }
 
-uint32_t ef_L(uint64_t U, uint64_t k) {
-    if (U < k) return 0;
-    uint64_t q = U / k;
-    uint32_t w = 0;
-    while (q) {
-        ++w;
-        q >>= 1;
-    }
-    return w - 1;
-}
-
 void put_le(std::vector<uint8_t>& b, uint64_t x, int bytes) {
     for (int i = 0; i < bytes; ++i) b.push_back((uint8_t)(x >> (8 * i)));
 }
@@ -192,22 +181,99 @@ void phase_policy(const Tables& T, SearchKind kind, uint32_t typical, uint32_t& 
 
 }  // namespace
 
-void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, bool want_values,
-                     BuildOutput& out) {
+// ====================================================================== shards ==
+//
+// A shard owns the contiguous bucket range [b0, b1) = [floor(r B / W), floor((r+1) B / W))
+// (P:320).  Phase 1 hashes all keys, keeps its buckets, searches every node and computes
+// the Golomb-Rice length of each bucket; its summary is exchanged (allgather).  Phase 2
+// derives the global bases and the shard's minimum residual step (allreduce-min gives
+// delta_R, R13).  Phase 3 writes the shard's slices of the data bits and of both
+// Elias-Fano sequences at their global bit positions.  stitch() ORs the slices of all
+// shards into the serialized MPHF; with one shard this is the plain single-GPU build.
+
+Globals compute_globals(const uint64_t* all, int world, int rank) {
+    Globals G{};
+    uint64_t mn = UINT64_MAX;
+    for (int q = 0; q < world; ++q) {
+        const uint64_t* x = all + 8 * q;
+        if (q < rank) {
+            G.key_base += x[SUM_KEYS];
+            G.bit_base += x[SUM_BITS];
+        }
+        G.n += x[SUM_KEYS];
+        G.D += x[SUM_BITS];
+        if (x[SUM_MINB] < mn) mn = x[SUM_MINB];
+        if (x[SUM_DUP]) G.dup = 1;
+        if (x[SUM_ERR]) G.err = 1;
+    }
+    G.dC = mn == UINT64_MAX ? 0 : mn;
+    G.beta = G.n ? (uint64_t)(((unsigned __int128)G.D << 20) / G.n) : 0;
+    return G;
+}
+
+static uint32_t ef_L(uint64_t U, uint64_t k) {
+    if (U < k) return 0;
+    uint64_t q = U / k;
+    uint32_t w = 0;
+    while (q) {
+        ++w;
+        q >>= 1;
+    }
+    return w - 1;
+}
+
+void finalize_globals(Globals& G, uint64_t B, long long dR) {
+    G.dR = dR;
+    const uint64_t k = B + 1;
+    G.UC = G.n - B * G.dC;
+    const long long RB = (long long)G.D - (long long)(((unsigned __int128)G.beta * G.n) >> 20);
+    G.UP = (uint64_t)(RB - (long long)B * dR);
+    G.LC = ef_L(G.UC, k);
+    G.LP = ef_L(G.UP, k);
+}
+
+struct Shard::Impl {
+    BuildParams p;
+    int rank = 0, world = 1;
+    cudaStream_t st;
+    Arena A;
+    uint64_t B = 0, b0 = 0, b1 = 0, Bl = 0, nl = 0, Dl = 0;
+    u64* C = nullptr;      // local key offsets (Bl + 1)
+    u64* Pbits = nullptr;  // local bit offsets (Bl + 1)
+    Globals G{};
+    explicit Impl(cudaStream_t s) : st(s), A(s) {}
+};
+
+Shard::~Shard() { delete impl_; }
+
+Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, cudaStream_t st, bool want_values)
+    : impl_(new Impl(st)) {
     auto t_start = std::chrono::steady_clock::now();
     g_launches = 0;
+    Impl& I = *impl_;
+    I.p = p;
+    I.rank = rank;
+    I.world = world;
     const uint64_t n = p.n;
     const uint32_t leaf = p.leaf;
     const uint64_t B = (n + p.bucket - 1) / p.bucket;  // R12
+    I.B = B;
+    I.b0 = B * (uint64_t)rank / (uint64_t)world;
+    I.b1 = B * (uint64_t)(rank + 1) / (uint64_t)world;
+    const uint64_t Bl = I.b1 - I.b0;
+    I.Bl = Bl;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     init_device(dev);
     const int sms = sm_count(dev);
     const Shape sh = make_shape(leaf);
-    recsplit_stats& S = out.stats;
+    recsplit_stats& S = stats;
     memset(&S, 0, sizeof S);
-
-    Arena A(st);
+    memset(summary, 0, sizeof summary);
+    summary[SUM_B0] = I.b0;
+    summary[SUM_B1] = I.b1;
+    summary[SUM_MINB] = UINT64_MAX;
+    Arena& A = I.A;
     Timer tm(st);
     const int e0 = tm.mark();
 
@@ -215,64 +281,79 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
     u64* lo_t = A.alloc<u64>(n);
     u8* ab_t = A.alloc<u8>(n);
     u32* bkt = A.alloc<u32>(n);
-    u32* hist = A.alloc<u32>(B + 1);
-    u64* C = A.alloc<u64>(B + 2);
-    u64* cursor = A.alloc<u64>(B + 1);
+    u32* hist = A.alloc<u32>(Bl + 1);
+    u64* C = A.alloc<u64>(Bl + 2);
+    I.C = C;
+    u64* cursor = A.alloc<u64>(Bl + 1);
     // [0] max, [1] min bucket size, [2] duplicate flag, [3] keys with MHC.hi == 0, [4] seed cap
     u32* small = A.alloc<u32>(8);
     const uint32_t cap = kMaxBucketKeys;
     u8* present_d = A.alloc<u8>(cap + 1);
-    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(B + 1, 1)) + 64);
+    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(Bl + 1, 1)) + 64);
     uint64_t set_slots = 1024;
-    while (set_slots < 2 * n) set_slots <<= 1;
+    while (set_slots < 2 * ((n + world - 1) / world + 1024)) set_slots <<= 1;
     unsigned long long* dupset = A.alloc<unsigned long long>(set_slots);
     CK(cudaMemsetAsync(dupset, 0, set_slots * 8, st));
-    CK(cudaMemsetAsync(hist, 0, (B + 1) * 4, st));
+    CK(cudaMemsetAsync(hist, 0, (Bl + 1) * 4, st));
     CK(cudaMemsetAsync(present_d, 0, cap + 1, st));
     const uint32_t small_init[8] = {0, 0xffffffffu, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(small, small_init, sizeof small_init, cudaMemcpyHostToDevice, st));
-    launch_hash(d_keys, n, p.g, B, lo_t, ab_t, bkt, hist, dupset, set_slots - 1, small + 2, st);
+    if (Bl == 0) {  // no buckets: only index entry B (last shard) may remain, with zero offsets
+        I.C = A.alloc<u64>(2);
+        I.Pbits = A.alloc<u64>(2);
+        CK(cudaMemsetAsync(I.C, 0, 16, st));
+        CK(cudaMemsetAsync(I.Pbits, 0, 16, st));
+        CK(cudaStreamSynchronize(st));
+        S.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+        return;
+    }
+    launch_hash(d_keys, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt, hist, dupset, set_slots - 1, small + 2, st);
     CKL();
-    launch_bucket_stats(hist, B, small, present_d, cap, st);
+    launch_bucket_stats(hist, Bl, small, present_d, cap, st);
     CKL();
-    exscan_u32_to_u64(hist, C, B, scan_tmp, st);
+    exscan_u32_to_u64(hist, C, Bl, scan_tmp, st);
     CKL();
-    CK(cudaMemcpyAsync(cursor, C, (B + 1) * 8, cudaMemcpyDeviceToDevice, st));
-    u64* lo_a = A.alloc<u64>(n);
-    u8* ab_a = A.alloc<u8>(n);
-    u64* lo_b = A.alloc<u64>(n);
-    u8* ab_b = A.alloc<u8>(n);
-    launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
-    CKL();
-    // sync A: bucket-size range and the set of occurring sizes
+    CK(cudaMemcpyAsync(cursor, C, (Bl + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    // sync A: keys of the shard, bucket-size range and the set of occurring sizes
     uint32_t mm[2];
+    uint64_t nl = 0;
     std::vector<uint8_t> present(cap + 1);
     CK(cudaMemcpyAsync(mm, small, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&nl, C + Bl, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(present.data(), present_d, cap + 1, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    I.nl = nl;
     const uint32_t smax = mm[0], smin = mm[1];
+    summary[SUM_KEYS] = nl;
+    summary[SUM_MINB] = smin;
     S.max_bucket = smax;
     if (smax > cap)
         throw Error(RECSPLIT_E_INVALID, "bucket of " + std::to_string(smax) + " keys exceeds the supported maximum " +
                                             std::to_string(cap) + " (use a smaller bucket_size)");
     present.resize(smax + 1);
+    u64* lo_a = A.alloc<u64>(nl);
+    u8* ab_a = A.alloc<u8>(nl);
+    u64* lo_b = A.alloc<u64>(nl);
+    u8* ab_b = A.alloc<u8>(nl);
+    launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
+    CKL();
     const int e1 = tm.mark();
 
     // ---- A3: node table --------------------------------------------------------
     const DevTables& DT = device_tables(dev, leaf, p.rf, smax, present, st);
     const Tables& T = *DT.T;
     const uint32_t NP = T.NP;
-    const uint64_t rows = (uint64_t)(NP + 1) * (B + 1);
+    const uint64_t rows = (uint64_t)(NP + 1) * (Bl + 1);
     u64* M = A.alloc<u64>(rows);
     u64* Ms = A.alloc<u64>(rows + 1);
     void* scan_tmp2 = A.alloc<u8>(scan_temp_bytes(rows) + 64);
-    launch_bucket_counts(C, B, DT.N, DT.phase_cnt, NP, M, st);
+    launch_bucket_counts(C, Bl, DT.N, DT.phase_cnt, NP, M, st);
     CKL();
     exscan_u64(M, Ms, rows, scan_tmp2, st);
     CKL();
     std::vector<uint64_t> rowstart(NP + 2);
     for (uint32_t r = 0; r <= NP; ++r)
-        CK(cudaMemcpyAsync(&rowstart[r], Ms + (uint64_t)r * (B + 1), 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&rowstart[r], Ms + (uint64_t)r * (Bl + 1), 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&rowstart[NP + 1], Ms + rows, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));  // sync B: node counts
     const uint64_t total_nodes = rowstart[1] - rowstart[0];
@@ -284,19 +365,19 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
         acc += pcount[q];
     }
     rsd::NodeRec* nodes = A.alloc<rsd::NodeRec>(total_nodes);
-    u64* values = A.alloc<u64>(total_nodes);
+    u64* values_d = A.alloc<u64>(total_nodes);
     u32* next_win = A.alloc<u32>(total_nodes);
     u32* pcnt_d = A.alloc<u32>(NP + 32);
     const u32 nslots = search_active_slots(sms);
     int* active = A.alloc<int>(nslots);
     u32* cursors = A.alloc<u32>(NP + 1);
-    CK(cudaMemsetAsync(values, 0xff, total_nodes * 8, st));
+    CK(cudaMemsetAsync(values_d, 0xff, total_nodes * 8, st));
     CK(cudaMemsetAsync(next_win, 0, total_nodes * 4, st));
     CK(cudaMemsetAsync(cursors, 0, (NP + 1) * 4, st));
     std::vector<u32> pc32(NP);
     for (uint32_t q = 0; q < NP; ++q) pc32[q] = (u32)pcount[q];
     CK(cudaMemcpyAsync(pcnt_d, pc32.data(), NP * 4, cudaMemcpyHostToDevice, st));
-    launch_expand(C, B, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st);
+    launch_expand(C, Bl, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st);
     CKL();
     const int e2 = tm.mark();
 
@@ -340,7 +421,7 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
         P.n_nodes_host = (u32)pcount[q];
         P.lo = lo_a;
         P.ab = ab_a;
-        P.values = values;
+        P.values = values_d;
         P.next_win = next_win;
         P.cursor = cursors + q;
         P.active = active;
@@ -358,9 +439,9 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
         CKL();
         const int b = tm.mark();
         if (kind == SK_UPPER || kind == SK_LOWER) {
-            CK(cudaMemcpyAsync(lo_b, lo_a, n * 8, cudaMemcpyDeviceToDevice, st));
-            CK(cudaMemcpyAsync(ab_b, ab_a, n, cudaMemcpyDeviceToDevice, st));
-            launch_reorder(nodes + poff[q], (u32)pcount[q], values, lo_a, ab_a, lo_b, ab_b, leaf, sh.u1, sh.u2, st);
+            CK(cudaMemcpyAsync(lo_b, lo_a, nl * 8, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(ab_b, ab_a, nl, cudaMemcpyDeviceToDevice, st));
+            launch_reorder(nodes + poff[q], (u32)pcount[q], values_d, lo_a, ab_a, lo_b, ab_b, leaf, sh.u1, sh.u2, st);
             CKL();
             std::swap(lo_a, lo_b);
             std::swap(ab_a, ab_b);
@@ -370,112 +451,45 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
     }
     const int e3 = tm.mark();
 
-    // ---- A10-A11: encode --------------------------------------------------------
-    u64* len = A.alloc<u64>(B + 1);
-    u64* Pbits = A.alloc<u64>(B + 2);
+    // ---- A10: Golomb-Rice lengths and data bits (local bit positions) -------------
+    u64* len = A.alloc<u64>(Bl + 1);
+    u64* Pbits = A.alloc<u64>(Bl + 2);
+    I.Pbits = Pbits;
     unsigned long long* evals = A.alloc<unsigned long long>(4);
     CK(cudaMemsetAsync(evals, 0, 32, st));
     u64* nodebase = Ms;  // row 0 of the scanned count matrix
-    launch_bucket_bits(C, B, nodebase, DT.tstart, DT.tnodes, DT.F, values, leaf, sh.u1, sh.u2, p.rf ? 1 : 0, len,
+    launch_bucket_bits(C, Bl, nodebase, DT.tstart, DT.tnodes, DT.F, values_d, leaf, sh.u1, sh.u2, p.rf ? 1 : 0, len,
                        evals, st);
     CKL();
-    exscan_u64(len, Pbits, B, scan_tmp, st);
+    exscan_u64(len, Pbits, Bl, scan_tmp, st);
     CKL();
     uint64_t D = 0;
     uint32_t flags[3];
     unsigned long long ev_h[4];
-    CK(cudaMemcpyAsync(&D, Pbits + B, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&D, Pbits + Bl, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(flags, small + 2, 12, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(ev_h, evals, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));  // sync C
-    if (flags[0] || flags[1] > 1) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
-    if (flags[2]) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
+    summary[SUM_DUP] = (flags[0] || flags[1] > 1) ? 1 : 0;
+    summary[SUM_ERR] = flags[2] ? 1 : 0;
+    if (summary[SUM_DUP] || summary[SUM_ERR]) D = 0;  // values are meaningless; the build fails in phase 2
+    summary[SUM_BITS] = D;
+    I.Dl = D;
     for (int c = 0; c < 4; ++c) S.algo_evals[c] = ev_h[c];
-    const uint64_t beta = (uint64_t)(((unsigned __int128)D << 20) / n);
-    const uint64_t dC = smin;
     const uint64_t nwords = (D + 63) / 64;
+    data_words_.assign(nwords, 0);
     unsigned long long* data = A.alloc<unsigned long long>(nwords + 1);
-    CK(cudaMemsetAsync(data, 0, (nwords + 1) * 8, st));
-    launch_write_data(C, B, nodebase, DT.tstart, DT.tnodes, DT.F, values, Pbits, data, st);
-    CKL();
-    long long* dR_d = A.alloc<long long>(1);
-    const long long llmax = INT64_MAX;
-    CK(cudaMemcpyAsync(dR_d, &llmax, 8, cudaMemcpyHostToDevice, st));
-    launch_min_residual(C, Pbits, B, beta, dR_d, st);
-    CKL();
-    long long dR = 0;
-    CK(cudaMemcpyAsync(&dR, dR_d, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));  // sync D
-    const uint64_t k = B + 1;
-    const uint64_t UC = n - B * dC;
-    const long long RB = (long long)D - (long long)(((unsigned __int128)beta * n) >> 20);
-    const uint64_t UP = (uint64_t)(RB - (long long)B * dR);
-    const uint32_t LC = ef_L(UC, k), LP = ef_L(UP, k);
-    const uint64_t c_low_bits = k * LC, c_up_bits = (UC >> LC) + k;
-    const uint64_t p_low_bits = k * LP, p_up_bits = (UP >> LP) + k;
-    auto words_of = [](uint64_t bits) { return (bits + 63) / 64; };
-    unsigned long long* c_low = A.alloc<unsigned long long>(words_of(c_low_bits) + 1);
-    unsigned long long* c_up = A.alloc<unsigned long long>(words_of(c_up_bits) + 1);
-    unsigned long long* p_low = A.alloc<unsigned long long>(words_of(p_low_bits) + 1);
-    unsigned long long* p_up = A.alloc<unsigned long long>(words_of(p_up_bits) + 1);
-    CK(cudaMemsetAsync(c_low, 0, (words_of(c_low_bits) + 1) * 8, st));
-    CK(cudaMemsetAsync(c_up, 0, (words_of(c_up_bits) + 1) * 8, st));
-    CK(cudaMemsetAsync(p_low, 0, (words_of(p_low_bits) + 1) * 8, st));
-    CK(cudaMemsetAsync(p_up, 0, (words_of(p_up_bits) + 1) * 8, st));
-    launch_ef_write(C, Pbits, B, dC, beta, dR, LC, LP, c_low, c_up, p_low, p_up, st);
-    CKL();
-    const int e4 = tm.mark();
-
-    // ---- A12: serialize (R14) ---------------------------------------------------
-    std::vector<uint8_t>& blob = out.bytes;
-    blob.clear();
-    const size_t total = 72 + 2 * 16 + 8 * (words_of(c_low_bits) + words_of(c_up_bits)) + 2 * 16 +
-                         8 * (words_of(p_low_bits) + words_of(p_up_bits)) + 8 * nwords - 16;
-    blob.reserve(total + 64);
-    blob.push_back('R');
-    blob.push_back('S');
-    blob.push_back('R');
-    blob.push_back('F');
-    put_le(blob, 1, 2);
-    blob.push_back((uint8_t)leaf);
-    blob.push_back(p.rf ? 1 : 0);
-    put_le(blob, p.bucket, 4);
-    put_le(blob, 0, 4);
-    put_le(blob, p.g, 8);
-    put_le(blob, n, 8);
-    put_le(blob, B, 8);
-    put_le(blob, D, 8);
-    put_le(blob, dC, 8);
-    put_le(blob, beta, 8);
-    put_le(blob, (uint64_t)dR, 8);
-    struct Seg {
-        size_t off;
-        const void* src;
-        size_t bytes;
-    };
-    std::vector<Seg> segs;
-    auto ef_seg = [&](uint32_t L, uint64_t lowbits, unsigned long long* low, uint64_t upbits,
-                      unsigned long long* up) {
-        blob.push_back((uint8_t)L);
-        for (int z = 0; z < 7; ++z) blob.push_back(0);
-        put_le(blob, lowbits, 8);
-        segs.push_back({blob.size(), low, 8 * words_of(lowbits)});
-        blob.resize(blob.size() + 8 * words_of(lowbits));
-        put_le(blob, upbits, 8);
-        segs.push_back({blob.size(), up, 8 * words_of(upbits)});
-        blob.resize(blob.size() + 8 * words_of(upbits));
-    };
-    ef_seg(LC, c_low_bits, c_low, c_up_bits, c_up);
-    ef_seg(LP, p_low_bits, p_low, p_up_bits, p_up);
-    segs.push_back({blob.size(), data, 8 * nwords});
-    blob.resize(blob.size() + 8 * nwords);
-    for (const Seg& sgm : segs)
-        if (sgm.bytes) CK(cudaMemcpyAsync(blob.data() + sgm.off, sgm.src, sgm.bytes, cudaMemcpyDeviceToHost, st));
-    if (want_values) {
-        out.values.resize(total_nodes);
-        if (total_nodes) CK(cudaMemcpyAsync(out.values.data(), values, total_nodes * 8, cudaMemcpyDeviceToHost, st));
+    if (!summary[SUM_DUP] && !summary[SUM_ERR]) {
+        CK(cudaMemsetAsync(data, 0, (nwords + 1) * 8, st));
+        launch_write_data(C, Bl, nodebase, DT.tstart, DT.tnodes, DT.F, values_d, Pbits, data, st);
+        CKL();
+        if (nwords) CK(cudaMemcpyAsync(data_words_.data(), data, nwords * 8, cudaMemcpyDeviceToHost, st));
     }
-    const int e5 = tm.mark();
+    if (want_values) {
+        values.resize(total_nodes);
+        if (total_nodes) CK(cudaMemcpyAsync(values.data(), values_d, total_nodes * 8, cudaMemcpyDeviceToHost, st));
+    }
+    const int e4 = tm.mark();
     CK(cudaStreamSynchronize(st));
     S.t_partition = tm.secs(e0, e1);
     S.t_tree = tm.secs(e1, e2);
@@ -485,10 +499,224 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
     }
     (void)e3;
     S.t_encode = tm.secs(e3, e4);
-    S.t_d2h = tm.secs(e4, e5);
     S.data_bits = D;
-    S.index_bits = c_low_bits + c_up_bits + p_low_bits + p_up_bits;
     S.kernel_launches = g_launches;
+    S.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+const Globals& Shard::globals() const { return impl_->G; }
+
+long long Shard::min_step(const uint64_t* all) {
+    Impl& I = *impl_;
+    I.G = compute_globals(all, I.world, I.rank);
+    if (I.G.dup) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
+    if (I.G.err) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
+    if (I.G.n != I.p.n) throw Error(RECSPLIT_E_CUDA, "shard summaries do not add up to n");
+    if (I.Bl == 0) return LLONG_MAX;
+    IndexView v{I.b0, I.Bl, I.G.key_base, I.G.bit_base, I.G.beta};
+    long long* d = I.A.alloc<long long>(1);
+    const long long llmax = LLONG_MAX;
+    CK(cudaMemcpyAsync(d, &llmax, 8, cudaMemcpyHostToDevice, I.st));
+    launch_min_residual(I.C, I.Pbits, v, d, I.st);
+    CKL();
+    long long r = 0;
+    CK(cudaMemcpyAsync(&r, d, 8, cudaMemcpyDeviceToHost, I.st));
+    CK(cudaStreamSynchronize(I.st));
+    return r;
+}
+
+static void put_slice(std::vector<uint8_t>& out, uint64_t start, uint64_t nbits, const uint64_t* words) {
+    put_le(out, start, 8);
+    put_le(out, nbits, 8);
+    const size_t nw = (nbits + 63) / 64;
+    const size_t at = out.size();
+    out.resize(at + 8 * nw);
+    if (nw) memcpy(out.data() + at, words, 8 * nw);
+}
+
+void Shard::finish(long long dR, std::vector<uint8_t>& part) {
+    Impl& I = *impl_;
+    auto t0 = std::chrono::steady_clock::now();
+    Globals& G = I.G;
+    finalize_globals(G, I.B, dR);
+    const uint64_t B = I.B, k = B + 1;
+    const bool last = I.rank == I.world - 1;
+    const uint64_t cnt = I.Bl + (last ? 1 : 0);  // index entries of this shard
+    const uint64_t e0 = I.b0, e1 = I.b0 + cnt;
+    // global bit ranges of the shard's slices (exact partitions of each bit vector)
+    auto cprime = [&](uint64_t i, uint64_t Cg) { return Cg - i * G.dC; };
+    auto rres = [&](uint64_t Pg, uint64_t Cg) {
+        return (long long)Pg - (long long)(((unsigned __int128)G.beta * Cg) >> 20);
+    };
+    auto pprime = [&](uint64_t i, uint64_t Pg, uint64_t Cg) { return (uint64_t)(rres(Pg, Cg) - (long long)i * dR); };
+    const uint64_t c_up_total = (G.UC >> G.LC) + k, p_up_total = (G.UP >> G.LP) + k;
+    const uint64_t Kb = G.key_base, Ob = G.bit_base;
+    const uint64_t cu_start = (cprime(I.b0, Kb) >> G.LC) + I.b0;
+    const uint64_t pu_start = (pprime(I.b0, Ob, Kb) >> G.LP) + I.b0;
+    const uint64_t cu_end = last ? c_up_total : (cprime(I.b1, Kb + I.nl) >> G.LC) + I.b1;
+    const uint64_t pu_end = last ? p_up_total : (pprime(I.b1, Ob + I.Dl, Kb + I.nl) >> G.LP) + I.b1;
+    const uint64_t cl_start = e0 * G.LC, cl_bits = cnt * G.LC;
+    const uint64_t pl_start = e0 * G.LP, pl_bits = cnt * G.LP;
+    const uint64_t cu_bits = cnt ? cu_end - cu_start : 0, pu_bits = cnt ? pu_end - pu_start : 0;
+    (void)e1;
+    auto words = [](uint64_t bits) { return (bits + 63) / 64; };
+    std::vector<uint64_t> cl(words(cl_bits)), cu(words(cu_bits)), pl(words(pl_bits)), pu(words(pu_bits));
+    if (cnt) {
+        Arena& A = I.A;
+        unsigned long long* d_cl = A.alloc<unsigned long long>(cl.size() + 1);
+        unsigned long long* d_cu = A.alloc<unsigned long long>(cu.size() + 1);
+        unsigned long long* d_pl = A.alloc<unsigned long long>(pl.size() + 1);
+        unsigned long long* d_pu = A.alloc<unsigned long long>(pu.size() + 1);
+        CK(cudaMemsetAsync(d_cl, 0, (cl.size() + 1) * 8, I.st));
+        CK(cudaMemsetAsync(d_cu, 0, (cu.size() + 1) * 8, I.st));
+        CK(cudaMemsetAsync(d_pl, 0, (pl.size() + 1) * 8, I.st));
+        CK(cudaMemsetAsync(d_pu, 0, (pu.size() + 1) * 8, I.st));
+        IndexView v{I.b0, I.Bl, Kb, Ob, G.beta};
+        EfSlices e{G.LC, G.LP, G.dC, dR, cl_start, cu_start, pl_start, pu_start, d_cl, d_cu, d_pl, d_pu};
+        launch_ef_write(I.C, I.Pbits, v, cnt, e, I.st);
+        CKL();
+        if (!cl.empty()) CK(cudaMemcpyAsync(cl.data(), d_cl, cl.size() * 8, cudaMemcpyDeviceToHost, I.st));
+        if (!cu.empty()) CK(cudaMemcpyAsync(cu.data(), d_cu, cu.size() * 8, cudaMemcpyDeviceToHost, I.st));
+        if (!pl.empty()) CK(cudaMemcpyAsync(pl.data(), d_pl, pl.size() * 8, cudaMemcpyDeviceToHost, I.st));
+        if (!pu.empty()) CK(cudaMemcpyAsync(pu.data(), d_pu, pu.size() * 8, cudaMemcpyDeviceToHost, I.st));
+        CK(cudaStreamSynchronize(I.st));
+    }
+    // part = global header fields + five slices
+    part.clear();
+    part.insert(part.end(), {'R', 'S', 'P', 'T'});
+    put_le(part, 1, 4);
+    const uint64_t hdr[16] = {I.p.leaf, I.p.rf ? 1u : 0u, I.p.bucket, I.p.g, G.n, B, G.D, G.dC, G.beta,
+                              (uint64_t)dR, G.LC, G.LP, k * G.LC, c_up_total, k * G.LP, p_up_total};
+    for (uint64_t x : hdr) put_le(part, x, 8);
+    put_slice(part, Ob, I.Dl, data_words_.data());
+    put_slice(part, cl_start, cl_bits, cl.data());
+    put_slice(part, cu_start, cu_bits, cu.data());
+    put_slice(part, pl_start, pl_bits, pl.data());
+    put_slice(part, pu_start, pu_bits, pu.data());
+    stats.index_bits = 0;
+    stats.t_d2h += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// OR a slice (local words = global bits [start, start + nbits)) into a global bit vector.
+static void or_slice(uint64_t* dst, uint64_t dst_bits, uint64_t start, uint64_t nbits, const uint8_t* src) {
+    const uint64_t nw = (nbits + 63) / 64;
+    const uint64_t base = start >> 6, sh = start & 63;
+    const uint64_t dst_words = (dst_bits + 63) / 64;
+    for (uint64_t w = 0; w < nw; ++w) {
+        uint64_t x;
+        memcpy(&x, src + 8 * w, 8);
+        if (!x) continue;
+        if (base + w < dst_words) dst[base + w] |= x << sh;
+        if (sh && base + w + 1 < dst_words) dst[base + w + 1] |= x >> (64 - sh);
+    }
+}
+
+void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::vector<uint8_t>& blob) {
+    if (parts.empty()) throw Error(RECSPLIT_E_INVALID, "no parts");
+    struct View {
+        uint64_t hdr[16];
+        uint64_t start[5], nbits[5];
+        const uint8_t* words[5];
+    };
+    std::vector<View> vs(parts.size());
+    for (size_t q = 0; q < parts.size(); ++q) {
+        const uint8_t* p = parts[q].first;
+        const uint8_t* end = p + parts[q].second;
+        if (parts[q].second < 8 + 128 || memcmp(p, "RSPT", 4) != 0) throw Error(RECSPLIT_E_FORMAT, "bad shard part");
+        p += 8;
+        View& v = vs[q];
+        memcpy(v.hdr, p, 128);
+        p += 128;
+        for (int s = 0; s < 5; ++s) {
+            if (end - p < 16) throw Error(RECSPLIT_E_FORMAT, "truncated shard part");
+            memcpy(&v.start[s], p, 8);
+            memcpy(&v.nbits[s], p + 8, 8);
+            p += 16;
+            const uint64_t nb = 8 * ((v.nbits[s] + 63) / 64);
+            if ((uint64_t)(end - p) < nb) throw Error(RECSPLIT_E_FORMAT, "truncated shard part");
+            v.words[s] = p;
+            p += nb;
+        }
+        if (memcmp(v.hdr, vs[0].hdr, sizeof v.hdr) != 0) throw Error(RECSPLIT_E_FORMAT, "shard headers differ");
+    }
+    const uint64_t* h = vs[0].hdr;
+    const uint64_t leaf = h[0], rf = h[1], bucket = h[2], g = h[3], n = h[4], B = h[5], D = h[6], dC = h[7],
+                   beta = h[8], dR = h[9], LC = h[10], LP = h[11];
+    const uint64_t len[5] = {D, h[12], h[13], h[14], h[15]};  // data, C low, C up, P low, P up
+    std::vector<std::vector<uint64_t>> vec(5);
+    for (int s = 0; s < 5; ++s) vec[s].assign((len[s] + 63) / 64, 0);
+    for (const View& v : vs)
+        for (int s = 0; s < 5; ++s) or_slice(vec[s].data(), len[s], v.start[s], v.nbits[s], v.words[s]);
+    blob.clear();
+    blob.push_back('R');
+    blob.push_back('S');
+    blob.push_back('R');
+    blob.push_back('F');
+    put_le(blob, 1, 2);
+    blob.push_back((uint8_t)leaf);
+    blob.push_back((uint8_t)rf);
+    put_le(blob, bucket, 4);
+    put_le(blob, 0, 4);
+    for (uint64_t x : {g, n, B, D, dC, beta, dR}) put_le(blob, x, 8);
+    auto ef = [&](uint64_t L, int lo, int up) {
+        blob.push_back((uint8_t)L);
+        for (int z = 0; z < 7; ++z) blob.push_back(0);
+        for (int s : {lo, up}) {
+            put_le(blob, len[s], 8);
+            const size_t at = blob.size();
+            blob.resize(at + 8 * vec[s].size());
+            if (!vec[s].empty()) memcpy(blob.data() + at, vec[s].data(), 8 * vec[s].size());
+        }
+    };
+    ef(LC, 1, 2);
+    ef(LP, 3, 4);
+    const size_t at = blob.size();
+    blob.resize(at + 8 * vec[0].size());
+    if (!vec[0].empty()) memcpy(blob.data() + at, vec[0].data(), 8 * vec[0].size());
+}
+
+void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, bool want_values,
+                     BuildOutput& out) {
+    auto t_start = std::chrono::steady_clock::now();
+    const int world = (int)std::max<uint32_t>(1, p.shards);
+    std::vector<std::unique_ptr<Shard>> shards;
+    std::vector<uint64_t> all(8 * world);
+    for (int r = 0; r < world; ++r) {  // virtual shards run one after the other
+        shards.emplace_back(new Shard(d_keys, p, r, world, st, want_values));
+        memcpy(&all[8 * r], shards.back()->summary, 64);
+    }
+    long long dR = LLONG_MAX;  // allreduce-min (local exchange)
+    for (auto& s : shards) dR = std::min(dR, s->min_step(all.data()));
+    if (dR == LLONG_MAX) dR = 0;
+    std::vector<std::vector<uint8_t>> parts(world);
+    std::vector<std::pair<const uint8_t*, size_t>> views;
+    for (int r = 0; r < world; ++r) {
+        shards[r]->finish(dR, parts[r]);
+        views.emplace_back(parts[r].data(), parts[r].size());
+    }
+    stitch(views, out.bytes);
+    recsplit_stats& S = out.stats;
+    memset(&S, 0, sizeof S);
+    for (auto& s : shards) {
+        const recsplit_stats& x = s->stats;
+        S.t_partition += x.t_partition;
+        S.t_tree += x.t_tree;
+        for (int c = 0; c < 4; ++c) {
+            S.t_search[c] += x.t_search[c];
+            S.algo_evals[c] += x.algo_evals[c];
+            S.nodes[c] += x.nodes[c];
+        }
+        S.t_reorder += x.t_reorder;
+        S.t_encode += x.t_encode;
+        S.t_d2h += x.t_d2h;
+        S.data_bits += x.data_bits;
+        S.kernel_launches += x.kernel_launches;
+        S.max_bucket = std::max(S.max_bucket, x.max_bucket);
+        if (want_values) out.values.insert(out.values.end(), s->values.begin(), s->values.end());
+    }
+    const Globals& G = shards[0]->globals();
+    const uint64_t k = G.n ? (p.n + p.bucket - 1) / p.bucket + 1 : 0;
+    S.index_bits = k * G.LC + (G.UC >> G.LC) + k + k * G.LP + (G.UP >> G.LP) + k;
     S.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
 }
 

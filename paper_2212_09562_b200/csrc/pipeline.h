@@ -31,6 +31,43 @@ struct BuildOutput {
     recsplit_stats stats{};
 };
 
+// ---- shards (multi-GPU / virtual shards), DESIGN.md section 13
+enum { SUM_KEYS = 0, SUM_BITS = 1, SUM_MINB = 2, SUM_B0 = 3, SUM_B1 = 4, SUM_DUP = 5, SUM_ERR = 6 };
+
+struct Globals {
+    uint64_t n = 0, D = 0, dC = 0, beta = 0, key_base = 0, bit_base = 0, UC = 0, UP = 0;
+    long long dR = 0;
+    uint32_t LC = 0, LP = 0;
+    int dup = 0, err = 0;
+};
+// global sizes and this rank's bases from all ranks' 8-word summaries
+Globals compute_globals(const uint64_t* all, int world, int rank);
+// EF parameters once delta_R is known
+void finalize_globals(Globals& G, uint64_t B, long long dR);
+
+class Shard {
+   public:
+    // phase 1: hash all keys, keep buckets [floor(rB/W), floor((r+1)B/W)), search, lengths
+    Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, cudaStream_t st, bool want_values);
+    ~Shard();
+    uint64_t summary[8];  // SUM_* fields
+    // phase 2: global bases from all summaries; returns this shard's min residual step
+    long long min_step(const uint64_t* all_summaries);
+    // phase 3: EF and data slices at their global bit positions -> serialized part
+    void finish(long long dR, std::vector<uint8_t>& part);
+    const Globals& globals() const;
+    std::vector<uint64_t> values;  // node values of the shard (want_values)
+    recsplit_stats stats{};
+
+   private:
+    struct Impl;
+    Impl* impl_;
+    std::vector<uint64_t> data_words_;
+};
+
+// OR all parts' slices into the serialized MPHF
+void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::vector<uint8_t>& blob);
+
 // d_keys: device pointer (n keys) on params.device; work ordered on st.
 void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, bool want_values,
                      BuildOutput& out);

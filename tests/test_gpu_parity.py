@@ -216,3 +216,69 @@ def test_c3_sampled_bucket_parity_and_properties():
     with ThreadPoolExecutor(len(sample)) as ex:
         for i, want in ex.map(one, sample):
             assert vals[nb[i]:nb[i + 1]].tolist() == want.tolist(), f"bucket {i}"
+
+
+# ------------------------------------------------------------------ sharding --
+
+@pytest.mark.parametrize("shards", [2, 3, 8, 150])
+def test_virtual_shards_identical_bytes(shards):
+    """bucket ranges per worker, concatenated sequences, one index: the
+    sharded build (virtual shards on one GPU, same code as multi-GPU) is byte-identical
+    to the unsharded build and to the oracle (150 shards > B = 100 -> empty shards)."""
+    keys = synth.keys(10_000, 1)
+    ref = oracle.build(keys, 8, 100, threads=os.cpu_count())
+    assert rs.build(keys, 8, 100, virtual_shards=shards) == ref
+
+
+def test_shard_protocol_in_process():
+    """The multi-GPU ABI protocol (begin / allgather / min step / allreduce / finish /
+    stitch) run for world = 3 in one process with a local exchange."""
+    import torch
+    keys = synth.keys(60_000, 4)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    world = 3
+    shards = [rs.Shard(kt, 12, 1000, r, world) for r in range(world)]
+    allsum = np.stack([s.summary for s in shards])
+    step = min(s.min_step(allsum) for s in shards)
+    parts = [s.finish(step) for s in shards]
+    for s in shards:
+        s.close()
+    assert rs.stitch(parts) == rs.build(keys, 12, 1000) == oracle.build(keys, 12, 1000, threads=os.cpu_count())
+
+
+def _sharded_worker(rank, world, port, q):
+    import sys as _sys
+    _sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import paper_2212_09562_b200 as rs_
+    import synth as synth_
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # both ranks on the one GPU; collectives over gloo
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        keys = synth_.keys(200_000, 12)
+        kt = torch.from_numpy(keys.view(np.int64)).cuda()
+        blob = rs_.build_sharded(kt, 12, 1000)
+        if rank == 0:
+            q.put(blob == rs_.build(keys, 12, 1000))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_build_sharded_two_ranks_gloo():
+    """build_sharded over torch.distributed (2 ranks on one GPU, gloo collectives):
+    same bytes as the single-GPU build."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
