@@ -113,6 +113,15 @@ __device__ __forceinline__ u32 hash1(const KeysView& K, u32 j, u32 sigma) {
                      : remix_hi_fast<true>(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), sigma);
 }
 
+// Block-wide shift tables of the FULL lower-level nodes of a phase (all share f and w):
+// index 0 = lower level 1 (f1 parts of l), 1 = lower level 2 (f2 parts of u1).  Static
+// shared arrays have link-time addresses, so the lookup is LDS [part + imm].
+__shared__ u8 s_full_tab[2][32];
+
+// increment 1 << s_full_tab[c][remap(h, f)]
+template <int CL>
+__device__ __forceinline__ u32 inc_full(u32 h, u32 f) { return bit_clamp(s_full_tab[CL][__umulhi(h, f)]); }
+
 // increment 1 << table[remap(h, r)]: the byte address comes straight out of mad.hi
 // (hi(h * r) + table base), the shift amount is >= 32 for the last part (adds 0).
 __device__ __forceinline__ u32 inc_of(u32 h, u32 r, u32 tbase) {
@@ -123,9 +132,10 @@ __device__ __forceinline__ u32 inc_of(u32 h, u32 r, u32 tbase) {
     return bit_clamp(sh);
 }
 
-// Lower split: packed counter.  r = f for full nodes (part = remap(h, f)),
-// r = s otherwise (table over remap(h, s)).
-template <int MODE>
+// Lower split: packed counter.  CL = 0/1: full node of lower level 1/2,
+// part = remap(h, f) looked up in the block-wide static table; CL = 2: node with a smaller
+// last part, warp table over v = remap(h, s) (r = s).
+template <int MODE, int CL>
 __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, u32 r) {
     u32 c0 = 0, c1 = 0;
     const u32 ng = s >> 2;
@@ -134,10 +144,18 @@ __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, 
     for (u32 q = 0; q < ng; ++q, g += 12) {
         u32 h[4];
         hash4<MODE>(g, sigma, h);
-        c0 += inc_of(h[0], r, K.tbase) + inc_of(h[1], r, K.tbase);
-        c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
+        if (CL < 2) {
+            c0 += inc_full<CL>(h[0], r) + inc_full<CL>(h[1], r);
+            c1 += inc_full<CL>(h[2], r) + inc_full<CL>(h[3], r);
+        } else {
+            c0 += inc_of(h[0], r, K.tbase) + inc_of(h[1], r, K.tbase);
+            c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
+        }
     }
-    for (u32 j = ng << 2; j < s; ++j) c0 += inc_of(hash1<MODE, 12>(K, j, sigma), r, K.tbase);
+    for (u32 j = ng << 2; j < s; ++j) {
+        const u32 h = hash1<MODE, 12>(K, j, sigma);
+        c0 += CL < 2 ? inc_full<(CL < 2 ? CL : 0)>(h, r) : inc_of(h, r, K.tbase);
+    }
     return c0 + c1;
 }
 
@@ -196,8 +214,10 @@ __device__ __forceinline__ int fit_rotation(u32 a, u32 b, u32 m, u32 full) {
 struct NodeCtx {
     u32 s, slot;
     u32 f, w, unit, full, mu, r, wide, target, mask, margin;
+    u32 l2;  // lower level 2 node (s > u1)
     u64 target64, mask64;
 };
+
 
 // One trial of `sig` (32-bit fast path).  For rotation fitting r receives the rotation.
 template <int KIND, int MODE>
@@ -212,7 +232,10 @@ __device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, 
     } else if (KIND == SK_UPPER) {
         return count_left<MODE>(K, c.s, sig, c.mask) == c.target;
     } else {
-        return (count_lower<MODE>(K, c.s, sig, c.r) & c.mask) == c.target;
+        const u32 cnt = !c.full ? count_lower<MODE, 2>(K, c.s, sig, c.r)
+                        : c.l2 ? count_lower<MODE, 1>(K, c.s, sig, c.r)
+                                        : count_lower<MODE, 0>(K, c.s, sig, c.r);
+        return (cnt & c.mask) == c.target;
     }
 }
 
@@ -302,6 +325,7 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
             c.mu = (u32)(((1ull << 32) + unit - 1) / unit);
             c.wide = (f - 1) * w > 32;
             c.r = c.full ? f : s;
+            c.l2 = s > A.u1;
             if (!c.wide) {
                 u32 t = 0;
                 for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
@@ -393,6 +417,15 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     u32* G = smem32 + (size_t)wib * (gwords + twords);
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
     const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
+    if (KIND == SK_LOWER) {  // shift tables of full nodes: part p -> p*w (p < f-1), 32 for the last
+        for (u32 t = threadIdx.x; t < 64; t += blockDim.x) {
+            const u32 cl = t >> 5, p = t & 31;
+            const u32 unit = cl ? A.u1 : A.leaf, f = cl ? A.u2 / A.u1 : A.u1 / A.leaf;
+            const u32 w = 32 - __clz(unit + 1);
+            s_full_tab[cl][p] = (u8)(p + 1 < f ? p * w : 32);
+        }
+        __syncthreads();
+    }
     if (A.dup[0] || A.dup[1] > 1) return;  // duplicate keys: nothing can be found (host reports)
     const u32 nn = *A.n_nodes;
     const u64 ws = 32ull * A.iters;
@@ -469,7 +502,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
 
 template <int KIND>
 void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 grid, cudaStream_t st) {
-    cudaFuncSetAttribute(k_search<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_search<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     k_search<KIND><<<grid, wpb * 32, smem, st>>>(A);
 }
 
@@ -510,7 +543,7 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
                : P.kind == SK_LOWER ? (const void*)k_search<SK_LOWER>
                : P.kind == SK_LEAF_RF ? (const void*)k_search<SK_LEAF_RF>
                                       : (const void*)k_search<SK_LEAF_BF>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, (int)(wpb * 32), smem);
     if (occ < 1) occ = 1;
     int max_blocks = (int)(search_active_slots(P.sm_count) / wpb);
