@@ -140,6 +140,12 @@ RECSPLIT_API int recsplit_query(const uint8_t *mphf, size_t size, uint64_t key, 
 RECSPLIT_API int recsplit_query_many(const uint8_t *mphf, size_t size, const uint64_t *keys, size_t n,
                         uint64_t *out);
 
+/* Evaluate on n keys on the GPU: mphf is HOST memory (parsed and uploaded
+ * per call), d_keys / d_out are DEVICE arrays of n u64 on the current device; ordered on
+ * `stream`, returns after completion.  Same results as recsplit_query_many. */
+RECSPLIT_API int recsplit_query_device(const uint8_t *mphf, size_t size, const uint64_t *d_keys,
+                                       size_t n, uint64_t *d_out, void *stream);
+
 /* bits/object of a serialized MPHF: (Golomb-Rice bits + Elias-Fano bits) / n,
  * excluding the fixed header and word padding (reading R14). */
 RECSPLIT_API int recsplit_bits_per_key(const uint8_t *mphf, size_t size, double *out);

@@ -24,7 +24,7 @@ SYMBOLS = [
     "recsplit_bits_per_key", "recsplit_search_leaves", "recsplit_search_splits", "recsplit_tau",
     "recsplit_free", "recsplit_free_ptr", "recsplit_last_error", "recsplit_shard_begin",
     "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch", "recsplit_shard_free",
-    "recsplit_shard_globals",
+    "recsplit_shard_globals", "recsplit_query_device",
 ]
 
 
@@ -84,6 +84,8 @@ def lib():
         L.recsplit_query.argtypes = [P8, sz, u64, P64]
         L.recsplit_query_many.argtypes = [P8, sz, P64, sz, P64]
         L.recsplit_bits_per_key.argtypes = [P8, sz, C.POINTER(C.c_double)]
+        L.recsplit_query_device.argtypes = [P8, sz, C.c_void_p, sz, C.c_void_p, C.c_void_p]
+        L.recsplit_query_device.restype = i32
         L.recsplit_search_leaves.argtypes = [P64, P8, P32, u32, u32, P64]
         L.recsplit_search_splits.argtypes = [P64, P32, u32, u32, P64]
         L.recsplit_tau.argtypes = [u32, u32, u32]
@@ -191,6 +193,20 @@ def query_many(blob: bytes, keys) -> np.ndarray:
     buf = np.frombuffer(blob, dtype=np.uint8)
     _check(lib().recsplit_query_many(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob), _p64(keys),
                                      len(keys), _p64(out)))
+    return out
+
+
+def query_device(blob: bytes, keys_tensor, stream=None):
+    """Evaluate on a CUDA tensor of keys on the GPU; returns an int64 CUDA tensor."""
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream(keys_tensor.device)
+    out = torch.empty_like(keys_tensor)
+    buf = np.frombuffer(blob, dtype=np.uint8)
+    _check(lib().recsplit_query_device(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob),
+                                       C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(),
+                                       C.c_void_p(out.data_ptr()), C.c_void_p(stream.cuda_stream)))
     return out
 
 

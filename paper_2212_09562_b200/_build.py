@@ -19,8 +19,9 @@ EXTRA = os.environ.get("RS_NVCC_FLAGS", "").split()  # development experiments o
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["scan.cu", "partition.cu", "search.cu", "encode.cu", "pipeline.cu", "tables.cpp", "abi.cpp"]
-HEADERS = ["device.cuh", "kernels.h", "pipeline.h", "tables.h"]
+SOURCES = ["scan.cu", "partition.cu", "search.cu", "encode.cu", "pipeline.cu", "query.cu", "tables.cpp", "format.cpp",
+           "abi.cpp"]
+HEADERS = ["device.cuh", "kernels.h", "pipeline.h", "tables.h", "format.h"]
 
 
 def _stale() -> bool:

@@ -14,6 +14,7 @@
 
 #include "../../include/recsplit.h"
 #include "pipeline.h"
+#include "format.h"
 #include "tables.h"
 
 namespace {
@@ -138,117 +139,18 @@ int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, c
 
 // ------------------------------------------------------------- host query --
 
-uint64_t rd64(const uint8_t* p) {
+using rs::Parsed;
+
+uint64_t word_at(const uint8_t* base, uint64_t i) {
     uint64_t x;
-    memcpy(&x, p, 8);
+    memcpy(&x, base + 8 * i, 8);
     return x;
 }
 
-struct EFView {
-    uint32_t L;
-    uint64_t nlow, nup;
-    const uint8_t* low;
-    const uint8_t* up;
-};
-
-struct Parsed {
-    uint32_t leaf;
-    bool rf;
-    uint64_t g, n, B, D, dC, beta;
-    int64_t dR;
-    EFView ec, ep;
-    const uint8_t* data;
-    std::vector<uint64_t> C, P;  // decoded index
-    std::shared_ptr<const rs::Tables> T;
-};
-
-uint64_t word_at(const uint8_t* base, uint64_t i) { return rd64(base + 8 * i); }
-
-bool parse_ef(const uint8_t*& p, const uint8_t* end, EFView& e) {
-    if (end - p < 16) return false;
-    e.L = p[0];
-    if (e.L > 63) return false;
-    for (int i = 1; i < 8; ++i)
-        if (p[i]) return false;
-    e.nlow = rd64(p + 8);
-    p += 16;
-    if ((uint64_t)(end - p) / 8 < (e.nlow + 63) / 64) return false;
-    e.low = p;
-    p += 8 * ((e.nlow + 63) / 64);
-    if (end - p < 8) return false;
-    e.nup = rd64(p);
-    p += 8;
-    if ((uint64_t)(end - p) / 8 < (e.nup + 63) / 64) return false;
-    e.up = p;
-    p += 8 * ((e.nup + 63) / 64);
-    return true;
-}
-
-bool ef_decode(const EFView& e, uint64_t k, std::vector<uint64_t>& v) {
-    if (e.nlow != k * e.L) return false;
-    v.assign(k, 0);
-    uint64_t i = 0;
-    const uint64_t words = (e.nup + 63) / 64;
-    for (uint64_t w = 0; w < words && i < k; ++w) {
-        uint64_t x = word_at(e.up, w);
-        while (x && i < k) {
-            const uint64_t pos = w * 64 + __builtin_ctzll(x);
-            x &= x - 1;
-            if (pos >= e.nup) return false;
-            uint64_t lo = 0;
-            if (e.L) {
-                const uint64_t bp = i * e.L;
-                const uint64_t a = word_at(e.low, bp >> 6);
-                const uint64_t sh = bp & 63;
-                lo = a >> sh;
-                if (sh + e.L > 64) lo |= word_at(e.low, (bp >> 6) + 1) << (64 - sh);
-                lo &= (e.L == 64) ? ~0ull : ((1ull << e.L) - 1);
-            }
-            v[i] = ((pos - i) << e.L) | lo;
-            ++i;
-        }
-    }
-    return i == k;
-}
-
 int parse(const uint8_t* blob, size_t size, Parsed& M) {
-    if (!blob || size < 72 || memcmp(blob, "RSRF", 4) != 0) return fail(RECSPLIT_E_FORMAT, "bad magic / size");
-    uint16_t ver;
-    memcpy(&ver, blob + 4, 2);
-    if (ver != 1) return fail(RECSPLIT_E_FORMAT, "unsupported format version");
-    M.leaf = blob[6];
-    M.rf = blob[7] & 1;
-    if (M.leaf < 2 || M.leaf > 24) return fail(RECSPLIT_E_FORMAT, "bad leaf size");
-    M.g = rd64(blob + 16);
-    M.n = rd64(blob + 24);
-    M.B = rd64(blob + 32);
-    M.D = rd64(blob + 40);
-    M.dC = rd64(blob + 48);
-    M.beta = rd64(blob + 56);
-    M.dR = (int64_t)rd64(blob + 64);
-    if (M.n == 0 || M.B == 0 || M.B > M.n + 1) return fail(RECSPLIT_E_FORMAT, "bad n / B");
-    const uint8_t* p = blob + 72;
-    const uint8_t* end = blob + size;
-    if (!parse_ef(p, end, M.ec) || !parse_ef(p, end, M.ep)) return fail(RECSPLIT_E_FORMAT, "truncated index");
-    if ((uint64_t)(end - p) != 8 * ((M.D + 63) / 64)) return fail(RECSPLIT_E_FORMAT, "data length mismatch");
-    M.data = p;
-    std::vector<uint64_t> c, q;
-    if (!ef_decode(M.ec, M.B + 1, c) || !ef_decode(M.ep, M.B + 1, q)) return fail(RECSPLIT_E_FORMAT, "bad index");
-    M.C.resize(M.B + 1);
-    M.P.resize(M.B + 1);
-    uint64_t smax = 1;
-    for (uint64_t i = 0; i <= M.B; ++i) {
-        M.C[i] = c[i] + i * M.dC;
-        M.P[i] = (uint64_t)((int64_t)q[i] + (int64_t)i * M.dR) +
-                 (uint64_t)(((unsigned __int128)M.beta * M.C[i]) >> 20);
-        if (i) {
-            if (M.C[i] < M.C[i - 1] || M.P[i] < M.P[i - 1]) return fail(RECSPLIT_E_FORMAT, "index not monotone");
-            smax = std::max<uint64_t>(smax, M.C[i] - M.C[i - 1]);
-        }
-    }
-    if (M.C[0] != 0 || M.C[M.B] != M.n || M.P[0] != 0 || M.P[M.B] != M.D) return fail(RECSPLIT_E_FORMAT, "bad index ends");
-    if (smax > (1u << 20)) return fail(RECSPLIT_E_FORMAT, "bucket too large");
-    M.T = rs::get_tables(M.leaf, M.rf, (uint32_t)smax);
+    std::string e;
+    int rc = rs::parse_mphf(blob, size, M, &e);
+    if (rc) return fail(rc, e);
     return RECSPLIT_OK;
 }
 
@@ -422,6 +324,19 @@ int recsplit_query_many(const uint8_t* mphf, size_t size, const uint64_t* keys, 
         }
         for (unsigned t = 0; t < nt; ++t)
             if (rcs[t]) return fail(rcs[t], errs[t]);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_query_device(const uint8_t* mphf, size_t size, const uint64_t* d_keys, size_t n, uint64_t* d_out,
+                          void* stream) {
+    if ((!d_keys || !d_out) && n) return fail(RECSPLIT_E_INVALID, "NULL keys/out");
+    return guarded([&]() -> int {
+        Parsed M;
+        int rc = parse(mphf, size, M);
+        if (rc) return rc;
+        select_device(-1);
+        rs::query_on_device(M, d_keys, n, d_out, (cudaStream_t)stream);
         return RECSPLIT_OK;
     });
 }

@@ -72,6 +72,10 @@ void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::ve
 void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, bool want_values,
                      BuildOutput& out);
 
+// Batched query on the device; d_keys / d_out device arrays of n.
+struct Parsed;
+void query_on_device(const Parsed& M, const uint64_t* d_keys, uint64_t n, uint64_t* d_out, cudaStream_t st);
+
 // Kernel-level entry points for parity tests (host arrays).
 void search_leaves_host(const uint64_t* lo, const uint8_t* isb, const uint32_t* off, uint32_t n_nodes, bool rf,
                         uint64_t* out);

@@ -198,16 +198,26 @@ __device__ __forceinline__ void leaf_masks(const KeysView& K, u32 ng, u32 m, u32
     b = b0;
 }
 
-// Rotation fitting for one base seed: masks of A and B; with no collision
-// inside A or B, b fits the holes of a iff some rotation of b equals ~a; the smallest
-// such r, or -1.
-__device__ __forceinline__ int fit_rotation(u32 a, u32 b, u32 m, u32 full) {
-    if (__popc(a) + __popc(b) != (int)m) return -1;  // popcount pruning
-    const u32 na = ~a & full;
-    const u64 bb = (u64)b | ((u64)b << m);  // rot_m^r(b) = (bb >> (m - r)) & full
-    for (u32 r = 0; r < m; ++r)
-        if (((u32)(bb >> (m - r)) & full) == na) return (int)r;
-    return -1;
+// Rotation fitting for the warp's 32 base seeds: lane masks a (A keys) and b
+// (B keys).  With no collision inside A or B (popcount pruning), b fits the holes of
+// a iff some rotation of b equals ~a.  Passing lanes are checked in lane (= base seed)
+// order, all lanes testing one rotation each, and the first lane with a fit wins with its
+// smallest r (minimal value rule P:297-300).  Returns true on the winning lane only (r set).
+__device__ __forceinline__ bool fit_rotation_warp(u32 a, u32 b, u32 m, u32 full, u32 lane, int& r) {
+    u32 pm = __ballot_sync(FULL, __popc(a) + __popc(b) == (int)m);
+    while (pm) {
+        const int i = __ffs(pm) - 1;
+        const u32 ai = __shfl_sync(FULL, a, i), bi = __shfl_sync(FULL, b, i);
+        const u32 na = ~ai & full;
+        const u64 bb = (u64)bi | ((u64)bi << m);  // rot_m^r(b) = (bb >> (m - r)) & full
+        const u32 hm = __ballot_sync(FULL, lane < m && ((u32)(bb >> (m - lane)) & full) == na);
+        if (hm) {
+            r = __ffs(hm) - 1;
+            return (int)lane == i;
+        }
+        pm &= pm - 1;
+    }
+    return false;
 }
 
 // Per-node search state (registers).
@@ -221,14 +231,13 @@ struct NodeCtx {
 
 // One trial of `sig` (32-bit fast path).  For rotation fitting r receives the rotation.
 template <int KIND, int MODE>
-__device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, u32 sig, int& r) {
+__device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, u32 sig, u32 lane, int& r) {
     if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
         const u32 base = KIND == SK_LEAF_RF ? sig * c.s : sig;
         u32 a, b;
         leaf_masks<MODE>(K, (c.s + 3) >> 2, c.s, base, a, b);
         if (KIND == SK_LEAF_BF) return a == c.full;
-        r = fit_rotation(a, b, c.s, c.full);
-        return r >= 0;
+        return fit_rotation_warp(a, b, c.s, c.full, lane, r);
     } else if (KIND == SK_UPPER) {
         return count_left<MODE>(K, c.s, sig, c.mask) == c.target;
     } else {
@@ -241,7 +250,7 @@ __device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, 
 
 // Generic 64-bit path (values >= 2^32; also the wide 64-bit packed counters, l >= 19).
 template <int KIND>
-__device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, u64 idx, int& r) {
+__device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, u64 idx, u32 lane, int& r) {
     constexpr u32 GW = Layout<KIND>::GW;
     const u32 s = c.s;
     if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
@@ -253,8 +262,7 @@ __device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, 
             b |= bit & key_word<GW>(K, j, 4);
         }
         if (KIND == SK_LEAF_BF) return a == c.full;
-        r = fit_rotation(a, b, s, c.full);
-        return r >= 0;
+        return fit_rotation_warp(a, b, s, c.full, lane, r);
     } else if (KIND == SK_UPPER) {
         u32 cnt = 0;
         for (u32 j = 0; j < s; ++j) cnt += hash_slow<GW>(K, j, idx) < c.mask;
@@ -365,11 +373,11 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, con
         int r = 0;
         bool ok;
         if (nocarry)
-            ok = trial_fast<KIND, 0>(K, c, (u32)idx, r);
+            ok = trial_fast<KIND, 0>(K, c, (u32)idx, lane, r);
         else if (fast)
-            ok = trial_fast<KIND, 1>(K, c, (u32)idx, r);
+            ok = trial_fast<KIND, 1>(K, c, (u32)idx, lane, r);
         else
-            ok = trial_slow<KIND>(K, c, idx, r);
+            ok = trial_slow<KIND>(K, c, idx, lane, r);
         const u32 bal = __ballot_sync(FULL, ok);
         if (bal) {
             const int win = __ffs(bal) - 1;

@@ -282,3 +282,21 @@ def test_build_sharded_two_ranks_gloo():
         p.join(600)
         assert p.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+# -------------------------------------------------------------- device query --
+
+@pytest.mark.parametrize("leaf,b,rf,n", [(8, 100, True, 10_000), (16, 2000, True, 20_000), (5, 5, False, 20_000),
+                                          (24, 24, True, 200), (12, 1000, True, 300_000)])
+def test_query_device_matches_host_and_oracle(leaf, b, rf, n):
+    """the GPU batched query equals the host query (and the oracle's on
+    the oracle's bytes), is a bijection on S and stays in [0, n) for non-members."""
+    import torch
+    keys = synth.keys(n, 77 + leaf)
+    blob = oracle.build(keys, leaf, b, rf=rf, threads=os.cpu_count()) if n <= 20_000 else rs.build(keys, leaf, b)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    got = rs.query_device(blob, kt).cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, rs.query_many(blob, keys))
+    assert np.array_equal(np.sort(got), np.arange(n, dtype=np.uint64))
+    other = torch.from_numpy(synth.keys(5000, 991).view(np.int64)).cuda()
+    assert (rs.query_device(blob, other).cpu().numpy().view(np.uint64) < n).all()
