@@ -27,8 +27,8 @@ void exscan_u64(const u64* in, u64* out, size_t n, void* temp, cudaStream_t st);
 // keys of buckets [b0, b1) only (local bucket ids; others get bkt = NONE)
 void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt, u32* hist,
                  unsigned long long* set, u64 set_mask, u32* dup, cudaStream_t st);
-// max/min bucket size and presence bitmap of sizes (present must be zeroed, cap+1 bytes)
-void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u8* present, u32 cap,
+// max/min bucket size and the histogram of bucket sizes (size_hist zeroed, cap+1 entries)
+void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u32* size_hist, u32 cap,
                          cudaStream_t st);
 // scatter (lo, ab) to bucket order (cursor = copy of exclusive offsets)
 void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cursor, u64* lo2,

@@ -82,13 +82,14 @@ void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, 
     g_launches++;
 }
 
-__global__ void k_bucket_stats(const u32* __restrict__ hist, u64 B, u32* maxmin, u8* present, u32 cap) {
+// max / min bucket size and the histogram of bucket sizes (sizes > cap counted at cap)
+__global__ void k_bucket_stats(const u32* __restrict__ hist, u64 B, u32* maxmin, u32* size_hist, u32 cap) {
     u32 mx = 0, mn = 0xffffffffu;
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += (u64)gridDim.x * blockDim.x) {
         u32 s = hist[i];
         mx = s > mx ? s : mx;
         mn = s < mn ? s : mn;
-        present[s <= cap ? s : cap] = 1;
+        atomicAdd(size_hist + (s <= cap ? s : cap), 1u);
     }
     for (int d = 16; d; d >>= 1) {
         mx = max(mx, __shfl_xor_sync(FULL, mx, d));
@@ -100,11 +101,11 @@ __global__ void k_bucket_stats(const u32* __restrict__ hist, u64 B, u32* maxmin,
     }
 }
 
-void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin, u8* present, u32 cap, cudaStream_t st) {
+void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin, u32* size_hist, u32 cap, cudaStream_t st) {
     unsigned grid = (unsigned)((B + 255) / 256);
     if (grid > 1024) grid = 1024;
     if (grid == 0) grid = 1;
-    k_bucket_stats<<<grid, 256, 0, st>>>(hist, B, maxmin, present, cap);
+    k_bucket_stats<<<grid, 256, 0, st>>>(hist, B, maxmin, size_hist, cap);
     g_launches++;
 }
 

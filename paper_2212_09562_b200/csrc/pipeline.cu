@@ -64,25 +64,35 @@ int sm_count(int dev) {
     return v;
 }
 
+// CUDA-event timer; events come from a per-thread pool (creation costs ~us each).
 struct Timer {
     cudaStream_t st;
-    std::vector<cudaEvent_t> ev;
-    explicit Timer(cudaStream_t s) : st(s) {}
+    size_t first;
+    static std::vector<cudaEvent_t>& pool() {
+        static thread_local std::vector<cudaEvent_t> p;
+        return p;
+    }
+    static size_t& used() {
+        static thread_local size_t u = 0;
+        return u;
+    }
+    explicit Timer(cudaStream_t s) : st(s), first(used()) {}
     int mark() {
-        cudaEvent_t e;
-        CK(cudaEventCreate(&e));
-        CK(cudaEventRecord(e, st));
-        ev.push_back(e);
-        return (int)ev.size() - 1;
+        auto& p = pool();
+        if (used() == p.size()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            p.push_back(e);
+        }
+        CK(cudaEventRecord(p[used()], st));
+        return (int)(used()++ - first);
     }
     double secs(int a, int b) {
         float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+        CK(cudaEventElapsedTime(&ms, pool()[first + a], pool()[first + b]));
         return ms * 1e-3;
     }
-    ~Timer() {
-        for (auto e : ev) cudaEventDestroy(e);
-    }
+    ~Timer() { used() = first; }
 };
 
 // Device copy of the per-size tables for sizes <= smax that occur (cached).
@@ -288,14 +298,14 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     // [0] max, [1] min bucket size, [2] duplicate flag, [3] keys with MHC.hi == 0, [4] seed cap
     u32* small = A.alloc<u32>(8);
     const uint32_t cap = kMaxBucketKeys;
-    u8* present_d = A.alloc<u8>(cap + 1);
+    u32* size_hist_d = A.alloc<u32>(cap + 1);
     void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(Bl + 1, 1)) + 64);
     uint64_t set_slots = 1024;
     while (set_slots < 2 * ((n + world - 1) / world + 1024)) set_slots <<= 1;
     unsigned long long* dupset = A.alloc<unsigned long long>(set_slots);
     CK(cudaMemsetAsync(dupset, 0, set_slots * 8, st));
     CK(cudaMemsetAsync(hist, 0, (Bl + 1) * 4, st));
-    CK(cudaMemsetAsync(present_d, 0, cap + 1, st));
+    CK(cudaMemsetAsync(size_hist_d, 0, (cap + 1) * 4, st));
     const uint32_t small_init[8] = {0, 0xffffffffu, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(small, small_init, sizeof small_init, cudaMemcpyHostToDevice, st));
     if (Bl == 0) {  // no buckets: only index entry B (last shard) may remain, with zero offsets
@@ -309,18 +319,19 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     }
     launch_hash(d_keys, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt, hist, dupset, set_slots - 1, small + 2, st);
     CKL();
-    launch_bucket_stats(hist, Bl, small, present_d, cap, st);
+    launch_bucket_stats(hist, Bl, small, size_hist_d, cap, st);
     CKL();
     exscan_u32_to_u64(hist, C, Bl, scan_tmp, st);
     CKL();
     CK(cudaMemcpyAsync(cursor, C, (Bl + 1) * 8, cudaMemcpyDeviceToDevice, st));
-    // sync A: keys of the shard, bucket-size range and the set of occurring sizes
+    // sync A: keys of the shard, bucket-size range and the histogram of bucket sizes
+    // (the whole node table -- counts per phase -- follows from it on the host)
     uint32_t mm[2];
     uint64_t nl = 0;
-    std::vector<uint8_t> present(cap + 1);
+    std::vector<uint32_t> size_hist(cap + 1);
     CK(cudaMemcpyAsync(mm, small, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&nl, C + Bl, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(present.data(), present_d, cap + 1, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(size_hist.data(), size_hist_d, (cap + 1) * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     I.nl = nl;
     const uint32_t smax = mm[0], smin = mm[1];
@@ -330,7 +341,8 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     if (smax > cap)
         throw Error(RECSPLIT_E_INVALID, "bucket of " + std::to_string(smax) + " keys exceeds the supported maximum " +
                                             std::to_string(cap) + " (use a smaller bucket_size)");
-    present.resize(smax + 1);
+    std::vector<uint8_t> present(smax + 1);
+    for (uint32_t x = 0; x <= smax; ++x) present[x] = size_hist[x] != 0;
     u64* lo_a = A.alloc<u64>(nl);
     u8* ab_a = A.alloc<u8>(nl);
     u64* lo_b = A.alloc<u64>(nl);
@@ -351,16 +363,17 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     CKL();
     exscan_u64(M, Ms, rows, scan_tmp2, st);
     CKL();
-    std::vector<uint64_t> rowstart(NP + 2);
-    for (uint32_t r = 0; r <= NP; ++r)
-        CK(cudaMemcpyAsync(&rowstart[r], Ms + (uint64_t)r * (Bl + 1), 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&rowstart[NP + 1], Ms + rows, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));  // sync B: node counts
-    const uint64_t total_nodes = rowstart[1] - rowstart[0];
-    std::vector<uint64_t> pcount(NP), poff(NP);
+    // node counts per phase from the size histogram (no device round trip)
+    uint64_t total_nodes = 0;
+    std::vector<uint64_t> pcount(NP, 0), poff(NP);
+    for (uint32_t x = 1; x <= smax; ++x) {
+        if (!size_hist[x]) continue;
+        total_nodes += (uint64_t)size_hist[x] * T.N[x];
+        const Tables::Tmpl& tp = T.tmpl(x);
+        for (uint32_t q = 0; q < NP; ++q) pcount[q] += (uint64_t)size_hist[x] * tp.phase_cnt[q];
+    }
     uint64_t acc = 0;
     for (uint32_t q = 0; q < NP; ++q) {
-        pcount[q] = rowstart[q + 2] - rowstart[q + 1];
         poff[q] = acc;
         acc += pcount[q];
     }
