@@ -105,11 +105,17 @@ __global__ void k_bucket_bits(const u64* __restrict__ C, u64 B, const u64* __res
         }
         if (lane == 0) len[i] = acc;
     }
+    // block-level reduction, then one atomic per block and class
+    __shared__ unsigned long long red[4];
+    if (threadIdx.x < 4) red[threadIdx.x] = 0;
+    __syncthreads();
     for (int c = 0; c < 4; ++c) {
         unsigned long long v = ev[c];
         for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
-        if (lane == 0 && v) atomicAdd(evals + c, v);
+        if (lane == 0 && v) atomicAdd(red + c, v);
     }
+    __syncthreads();
+    if (threadIdx.x < 4 && red[threadIdx.x]) atomicAdd(evals + threadIdx.x, red[threadIdx.x]);
 }
 
 void launch_bucket_bits(const u64* C, u64 B, const u64* nodebase, const u32* tstart, const TNodeD* tnodes,

@@ -22,11 +22,12 @@ void exscan_u32_to_u64(const u32* in, u64* out, size_t n, void* temp, cudaStream
 void exscan_u64(const u64* in, u64* out, size_t n, void* temp, cudaStream_t st);
 
 // ---- partition (partition.cu), steps A1-A2 of SURVEY section 8(a).
-// master hash code -> lo, A/B bit, bucket id; bucket histogram (zeroed); duplicate
-// detection through a zeroed open-addressing set of (set_mask+1) u64 slots (dup[0..1] zeroed).
-// keys of buckets [b0, b1) only (local bucket ids; others get bkt = NONE)
+// master hash code -> lo, A/B bit, bucket id; bucket histogram (zeroed); keys of buckets
+// [b0, b1) only (local bucket ids; others get bkt = NONE)
 void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt, u32* hist,
-                 unsigned long long* set, u64 set_mask, u32* dup, cudaStream_t st);
+                 cudaStream_t st);
+// exact duplicate check per bucket after the scatter (dup[0..1] zeroed)
+void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, cudaStream_t st);
 // max/min bucket size and the histogram of bucket sizes (size_hist zeroed, cap+1 entries)
 void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u32* size_hist, u32 cap,
                          cudaStream_t st);

@@ -9,18 +9,13 @@ namespace rs {
 using namespace rsd;
 
 // A1: hi = remix(key^g^salt_hi), lo = remix(key^g^salt_lo) (R2); bucket = remap(hi, B)
-// (R3); A/B bit = hi & 1 (R7).  Also inserts hi into an open-addressing hash set: two
-// equal keys have equal hi (remix is a bijection), so a duplicate is detected exactly
-// (the set replaces a per-bucket sort: the output depends only on the key set of each
-// node, never on the order of keys inside a bucket).  Bucket histogram in shared
-// memory when B is small (one global atomic per bucket per block), else global.
+// (R3); A/B bit = hi & 1 (R7).  Bucket histogram in shared memory when the shard has few
+// buckets (one global atomic per bucket per block), else global.
 // Only buckets in [b0, b1) (this shard, P:320 contiguous bucket ranges) are kept; their
 // local index b - b0 goes to bkt, other keys get bkt = NONE.
 __global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u64 b0,
                                                u64 b1, u64* __restrict__ lo, u8* __restrict__ ab,
-                                               u32* __restrict__ bkt, u32* __restrict__ hist,
-                                               unsigned long long* __restrict__ set, u64 set_mask, u32* dup,
-                                               int smem_hist) {
+                                               u32* __restrict__ bkt, u32* __restrict__ hist, int smem_hist) {
     extern __shared__ u32 sh[];
     const u64 Bl = b1 - b0;
     if (smem_hist) {
@@ -44,22 +39,6 @@ __global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64
             atomicAdd(sh + b, 1u);
         else
             atomicAdd(hist + b, 1u);
-        // duplicate detection: insert h into the set (0 marks an empty slot, so keys with
-        // h == 0 are counted instead: more than one of them is a duplicate)
-        if (h == 0) {
-            atomicAdd(dup + 1, 1u);
-        } else {
-            u64 slot = (h ^ (h >> 29)) & set_mask;
-            for (;;) {
-                const unsigned long long old = atomicCAS(set + slot, 0ull, (unsigned long long)h);
-                if (old == 0ull) break;
-                if (old == h) {
-                    atomicOr(dup, 1u);
-                    break;
-                }
-                slot = (slot + 1) & set_mask;
-            }
-        }
     }
     if (smem_hist) {
         __syncthreads();
@@ -69,7 +48,7 @@ __global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64
 }
 
 void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt, u32* hist,
-                 unsigned long long* set, u64 set_mask, u32* dup, cudaStream_t st) {
+                 cudaStream_t st) {
     const u64 Bl = b1 - b0;
     const int smem_hist = Bl <= 12288;
     const size_t smem = smem_hist ? Bl * 4 : 0;
@@ -78,7 +57,7 @@ void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, 
     if (grid > cap) grid = cap;
     if (grid == 0) grid = 1;
     cudaFuncSetAttribute(k_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    k_hash<<<grid, 1024, smem, st>>>(keys, n, g, B, b0, b1, lo, ab, bkt, hist, set, set_mask, dup, smem_hist);
+    k_hash<<<grid, 1024, smem, st>>>(keys, n, g, B, b0, b1, lo, ab, bkt, hist, smem_hist);
     g_launches++;
 }
 
@@ -145,6 +124,54 @@ void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cur
     if (grid > 148u * 8u) grid = 148u * 8u;
     if (grid == 0) grid = 1;
     k_scatter<<<grid, 256, 0, st>>>(lo, ab, bkt, n, (unsigned long long*)cursor, lo2, ab2);
+    g_launches++;
+}
+
+// Exact duplicate check after the scatter: equal keys have equal lo (remix is a bijection,
+// R2) and land in the same bucket, so each bucket inserts its lo values into an open-
+// addressing set in shared memory (0 marks an empty slot; lo == 0 is counted instead).
+// dup[0] |= 1 on a repeated value, dup[1] += keys with lo == 0 (> 1 is a duplicate).
+__global__ void __launch_bounds__(256) k_dedupe(const u64* __restrict__ lo, const u64* __restrict__ C, u64 nb,
+                                                u32 slots, u32* dup) {
+    extern __shared__ unsigned long long tab[];
+    for (u64 b = blockIdx.x; b < nb; b += gridDim.x) {
+        const u64 c0 = C[b], s = C[b + 1] - c0;
+        __syncthreads();
+        if (s < 2) continue;
+        u32 ts = 64;
+        while (ts < 2 * s) ts <<= 1;
+        for (u32 i = threadIdx.x; i < ts; i += blockDim.x) tab[i] = 0;
+        __syncthreads();
+        for (u32 i = threadIdx.x; i < s; i += blockDim.x) {
+            const u64 v = lo[c0 + i];
+            if (v == 0) {
+                atomicAdd(dup + 1, 1u);
+                continue;
+            }
+            u32 slot = (u32)(v ^ (v >> 32)) & (ts - 1);
+            for (;;) {
+                const unsigned long long old = atomicCAS(tab + slot, 0ull, (unsigned long long)v);
+                if (old == 0ull) break;
+                if (old == v) {
+                    atomicOr(dup, 1u);
+                    break;
+                }
+                slot = (slot + 1) & (ts - 1);
+            }
+        }
+    }
+    (void)slots;
+}
+
+void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, cudaStream_t st) {
+    if (nb == 0) return;
+    u32 ts = 64;
+    while (ts < 2 * smax) ts <<= 1;
+    const size_t smem = (size_t)ts * 8;
+    cudaFuncSetAttribute(k_dedupe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const u32 threads = smax <= 128 ? 128 : 256;
+    unsigned grid = nb < 148ull * 64 ? (unsigned)nb : 148u * 64;
+    k_dedupe<<<grid, threads, smem, st>>>(lo, C, nb, ts, dup);
     g_launches++;
 }
 

@@ -287,7 +287,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     Timer tm(st);
     const int e0 = tm.mark();
 
-    // ---- A1/A2: hash + duplicate set, histogram, counting sort by bucket -----------
+    // ---- A1/A2: hash, histogram, counting sort by bucket, duplicate check ---------
     u64* lo_t = A.alloc<u64>(n);
     u8* ab_t = A.alloc<u8>(n);
     u32* bkt = A.alloc<u32>(n);
@@ -295,15 +295,11 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     u64* C = A.alloc<u64>(Bl + 2);
     I.C = C;
     u64* cursor = A.alloc<u64>(Bl + 1);
-    // [0] max, [1] min bucket size, [2] duplicate flag, [3] keys with MHC.hi == 0, [4] seed cap
+    // [0] max, [1] min bucket size, [2] duplicate flag, [3] keys with lo == 0, [4] seed cap
     u32* small = A.alloc<u32>(8);
     const uint32_t cap = kMaxBucketKeys;
     u32* size_hist_d = A.alloc<u32>(cap + 1);
     void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(Bl + 1, 1)) + 64);
-    uint64_t set_slots = 1024;
-    while (set_slots < 2 * ((n + world - 1) / world + 1024)) set_slots <<= 1;
-    unsigned long long* dupset = A.alloc<unsigned long long>(set_slots);
-    CK(cudaMemsetAsync(dupset, 0, set_slots * 8, st));
     CK(cudaMemsetAsync(hist, 0, (Bl + 1) * 4, st));
     CK(cudaMemsetAsync(size_hist_d, 0, (cap + 1) * 4, st));
     const uint32_t small_init[8] = {0, 0xffffffffu, 0, 0, 0, 0, 0, 0};
@@ -317,7 +313,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
         S.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
         return;
     }
-    launch_hash(d_keys, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt, hist, dupset, set_slots - 1, small + 2, st);
+    launch_hash(d_keys, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt, hist, st);
     CKL();
     launch_bucket_stats(hist, Bl, small, size_hist_d, cap, st);
     CKL();
@@ -348,6 +344,8 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     u64* lo_b = A.alloc<u64>(nl);
     u8* ab_b = A.alloc<u8>(nl);
     launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
+    CKL();
+    launch_dedupe(lo_a, C, Bl, smax, small + 2, st);
     CKL();
     const int e1 = tm.mark();
 
