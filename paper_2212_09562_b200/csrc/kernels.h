@@ -67,10 +67,9 @@ struct PhaseLaunch {
 void launch_search(const PhaseLaunch& P, cudaStream_t st);
 u32 search_active_slots(int sm_count);
 
-// key redistribution after a split phase (A7): in -> out for the phase's nodes
-void launch_reorder(const rsd::NodeRec* nodes, u32 n_nodes, const u64* values, const u64* lo_in,
-                    const u8* ab_in, u64* lo_out, u8* ab_out, u32 leaf, u32 u1, u32 u2,
-                    cudaStream_t st);
+// key redistribution after a split phase (A7), in place for the phase's nodes
+void launch_reorder(const rsd::NodeRec* nodes, u32 n_nodes, const u64* values, u64* lo, u8* ab, u32 leaf,
+                    u32 u1, u32 u2, u32 max_size, int sm_count, cudaStream_t st);
 
 // ---- encode (encode.cu), steps A10-A11.
 // bucket bit lengths: F(s) + N(s) + sum (x >> tau); also algorithmic-evals statistics

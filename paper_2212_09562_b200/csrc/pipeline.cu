@@ -341,8 +341,6 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     for (uint32_t x = 0; x <= smax; ++x) present[x] = size_hist[x] != 0;
     u64* lo_a = A.alloc<u64>(nl);
     u8* ab_a = A.alloc<u8>(nl);
-    u64* lo_b = A.alloc<u64>(nl);
-    u8* ab_b = A.alloc<u8>(nl);
     launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
     CKL();
     launch_dedupe(lo_a, C, Bl, smax, small + 2, st);
@@ -450,12 +448,8 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
         CKL();
         const int b = tm.mark();
         if (kind == SK_UPPER || kind == SK_LOWER) {
-            CK(cudaMemcpyAsync(lo_b, lo_a, nl * 8, cudaMemcpyDeviceToDevice, st));
-            CK(cudaMemcpyAsync(ab_b, ab_a, nl, cudaMemcpyDeviceToDevice, st));
-            launch_reorder(nodes + poff[q], (u32)pcount[q], values_d, lo_a, ab_a, lo_b, ab_b, leaf, sh.u1, sh.u2, st);
+            launch_reorder(nodes + poff[q], (u32)pcount[q], values_d, lo_a, ab_a, leaf, sh.u1, sh.u2, maxs, sms, st);
             CKL();
-            std::swap(lo_a, lo_b);
-            std::swap(ab_a, ab_b);
         }
         const int c = tm.mark();
         pev.push_back({cls, a, b, c});

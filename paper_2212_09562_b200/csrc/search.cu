@@ -578,17 +578,25 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
 // ------------------------------------------------------------------ reorder --
 
 // A7: stable partition of each split node's keys by child index with its found seed
-// (P:311-313).  One warp per node; children occupy consecutive sub-ranges in
-// part order, so every child's keys are contiguous for the next phase.
+// (P:311-313), in place: one warp per node stages the node's (lo, A/B) in shared
+// memory, then writes every key to its child's sub-range (children occupy consecutive
+// sub-ranges in part order, so every child's keys are contiguous for the next phase).
 __global__ void k_reorder(const NodeRec* __restrict__ nodes, u32 n_nodes, const u64* __restrict__ values,
-                          const u64* __restrict__ lo_in, const u8* __restrict__ ab_in, u64* __restrict__ lo_out,
-                          u8* __restrict__ ab_out, u32 leaf, u32 u1, u32 u2) {
-    const u32 lane = threadIdx.x & 31;
+                          u64* __restrict__ lo, u8* __restrict__ ab, u32 leaf, u32 u1, u32 u2, u32 cap) {
+    extern __shared__ __align__(16) unsigned char rsm[];
+    const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    u64* slo = reinterpret_cast<u64*>(rsm + (size_t)wib * cap * 9);
+    u8* sab = reinterpret_cast<u8*>(slo + cap);
     const u32 nwarps = gridDim.x * (blockDim.x >> 5);
-    for (u32 n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < n_nodes; n += nwarps) {
+    for (u32 n = blockIdx.x * (blockDim.x >> 5) + wib; n < n_nodes; n += nwarps) {
         const NodeRec r = nodes[n];
         const u32 s = r.size;
         const u64 sigma = values[r.slot];
+        for (u32 j = lane; j < s; j += 32) {
+            slo[j] = lo[r.key_off + j];
+            sab[j] = ab[r.key_off + j];
+        }
+        __syncwarp();
         u32 unit, f, c0 = 0;
         const bool upper = s > u2;
         if (upper) {
@@ -610,8 +618,8 @@ __global__ void k_reorder(const NodeRec* __restrict__ nodes, u32 n_nodes, const 
             u8 b = 0;
             u32 part = 0xff;
             if (valid) {
-                k = lo_in[r.key_off + j];
-                b = ab_in[r.key_off + j];
+                k = slo[j];
+                b = sab[j];
                 const u32 v = __umulhi(remix_hi(k + sigma), s);
                 part = upper ? (v >= c0) : v / unit;
             }
@@ -626,19 +634,28 @@ __global__ void k_reorder(const NodeRec* __restrict__ nodes, u32 n_nodes, const 
                 }
             }
             if (valid) {
-                lo_out[r.key_off + dst] = k;
-                ab_out[r.key_off + dst] = b;
+                lo[r.key_off + dst] = k;
+                ab[r.key_off + dst] = b;
             }
         }
+        __syncwarp();
     }
 }
 
-void launch_reorder(const NodeRec* nodes, u32 n_nodes, const u64* values, const u64* lo_in, const u8* ab_in,
-                    u64* lo_out, u8* ab_out, u32 leaf, u32 u1, u32 u2, cudaStream_t st) {
+void launch_reorder(const NodeRec* nodes, u32 n_nodes, const u64* values, u64* lo, u8* ab, u32 leaf, u32 u1, u32 u2,
+                    u32 max_size, int sm_count, cudaStream_t st) {
     if (n_nodes == 0) return;
-    u32 blocks = (n_nodes + 7) / 8;
-    if (blocks > 148u * 32u) blocks = 148u * 32u;
-    k_reorder<<<blocks, 256, 0, st>>>(nodes, n_nodes, values, lo_in, ab_in, lo_out, ab_out, leaf, u1, u2);
+    const u32 cap = (max_size + 15) & ~15u;
+    const size_t per_warp = (size_t)cap * 9;
+    u32 wpb = 8;
+    while (wpb > 1 && per_warp * wpb > 96 * 1024) --wpb;
+    cudaFuncSetAttribute(k_reorder, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reorder, (int)(wpb * 32), per_warp * wpb);
+    if (occ < 1) occ = 1;
+    u32 blocks = (n_nodes + wpb - 1) / wpb;
+    blocks = std::min<u32>(blocks, (u32)(occ * sm_count));
+    k_reorder<<<blocks, wpb * 32, per_warp * wpb, st>>>(nodes, n_nodes, values, lo, ab, leaf, u1, u2, cap);
     g_launches++;
 }
 
