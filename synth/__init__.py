@@ -25,6 +25,24 @@ def keys(n: int, seed: int) -> np.ndarray:
         out = np.concatenate([out, extra])
 
 
+def keys_device(n: int, seed: int):
+    """n distinct uniform 64-bit keys generated on the current CUDA device (torch's Philox
+    generator + unique), for scale runs whose key sets are too large to build on the host.
+    Returns an int64 CUDA tensor (bit patterns).  Deterministic in (n, seed, torch build)."""
+    import torch
+
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    lo, hi = -(2 ** 63), 2 ** 63 - 1
+    out = torch.randint(lo, hi, (n,), generator=gen, device="cuda", dtype=torch.int64)
+    while True:
+        u = torch.unique(out)
+        if u.numel() == n:
+            return out
+        extra = torch.randint(lo, hi, (n - u.numel(),), generator=gen, device="cuda", dtype=torch.int64)
+        out = torch.cat([u, extra])
+
+
 # Workload recipes (BASELINE.json configs); key seeds follow BASELINE.md section 4.
 CONFIGS = {
     "C1": dict(n=10_000, leaf=8, bucket=100, seed=1),

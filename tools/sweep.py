@@ -50,13 +50,26 @@ def point(kt, n, leaf, b, rf, reps):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["c4", "c5"])
+    ap.add_argument("which", choices=["c4", "c5", "n2"])
     ap.add_argument("--leaves", default="4,5,6,7,8,9,10,11,12,13,14,15,16")
     ap.add_argument("--buckets", default="100,500,1000,2000")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--max-s", type=float, default=60.0, help="skip BF points predicted slower than this")
     args = ap.parse_args()
     torch.cuda.set_device(0)
+    if args.which == "n2":
+        # billion-key build on one GPU, verified bijective with the GPU query
+        for n, leaf, b in [(1_000_000_000, 8, 100), (1_000_000_000, 5, 5)]:
+            kt = synth.keys_device(n, 7)
+            r = point(kt, n, leaf, b, True, args.reps)
+            blob = rs.build_device(kt, leaf, b)
+            q = rs.query_device(blob, kt)
+            r["bijective"] = bool(torch.equal(torch.sort(q).values, torch.arange(n, device="cuda")))
+            r["config"] = "N2"
+            print(json.dumps(r), flush=True)
+            del kt, q
+            torch.cuda.empty_cache()
+        return
     if args.which == "c5":
         cfg = synth.CONFIGS["C5"]
         keys = synth.keys(cfg["n"], cfg["seed"])
