@@ -250,6 +250,7 @@ struct Shard::Impl {
     uint64_t B = 0, b0 = 0, b1 = 0, Bl = 0, nl = 0, Dl = 0;
     u64* C = nullptr;      // local key offsets (Bl + 1)
     u64* Pbits = nullptr;  // local bit offsets (Bl + 1)
+    unsigned long long* d_data = nullptr;  // the shard's Golomb-Rice bits (local positions)
     Globals G{};
     explicit Impl(cudaStream_t s) : st(s), A(s) {}
 };
@@ -482,13 +483,12 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     I.Dl = D;
     for (int c = 0; c < 4; ++c) S.algo_evals[c] = ev_h[c];
     const uint64_t nwords = (D + 63) / 64;
-    data_words_.assign(nwords, 0);
     unsigned long long* data = A.alloc<unsigned long long>(nwords + 1);
+    I.d_data = data;
+    CK(cudaMemsetAsync(data, 0, (nwords + 1) * 8, st));
     if (!summary[SUM_DUP] && !summary[SUM_ERR]) {
-        CK(cudaMemsetAsync(data, 0, (nwords + 1) * 8, st));
         launch_write_data(C, Bl, nodebase, DT.tstart, DT.tnodes, DT.F, values_d, Pbits, data, st);
         CKL();
-        if (nwords) CK(cudaMemcpyAsync(data_words_.data(), data, nwords * 8, cudaMemcpyDeviceToHost, st));
     }
     if (want_values) {
         values.resize(total_nodes);
@@ -539,66 +539,125 @@ static void put_slice(std::vector<uint8_t>& out, uint64_t start, uint64_t nbits,
     if (nw) memcpy(out.data() + at, words, 8 * nw);
 }
 
-void Shard::finish(long long dR, std::vector<uint8_t>& part) {
-    Impl& I = *impl_;
-    auto t0 = std::chrono::steady_clock::now();
+// Phase 3 geometry + EF kernels: the five slices of this shard on the device.
+struct ShardSlices {
+    uint64_t start[5], nbits[5];             // data, C low, C up, P low, P up (global bits)
+    const unsigned long long* dev[5];
+    uint64_t k, c_up_total, p_up_total;
+};
+
+static ShardSlices make_slices(Shard::Impl& I, long long dR) {
     Globals& G = I.G;
     finalize_globals(G, I.B, dR);
     const uint64_t B = I.B, k = B + 1;
     const bool last = I.rank == I.world - 1;
     const uint64_t cnt = I.Bl + (last ? 1 : 0);  // index entries of this shard
-    const uint64_t e0 = I.b0, e1 = I.b0 + cnt;
-    // global bit ranges of the shard's slices (exact partitions of each bit vector)
     auto cprime = [&](uint64_t i, uint64_t Cg) { return Cg - i * G.dC; };
     auto rres = [&](uint64_t Pg, uint64_t Cg) {
         return (long long)Pg - (long long)(((unsigned __int128)G.beta * Cg) >> 20);
     };
     auto pprime = [&](uint64_t i, uint64_t Pg, uint64_t Cg) { return (uint64_t)(rres(Pg, Cg) - (long long)i * dR); };
-    const uint64_t c_up_total = (G.UC >> G.LC) + k, p_up_total = (G.UP >> G.LP) + k;
+    ShardSlices S{};
+    S.k = k;
+    S.c_up_total = (G.UC >> G.LC) + k;
+    S.p_up_total = (G.UP >> G.LP) + k;
     const uint64_t Kb = G.key_base, Ob = G.bit_base;
+    // global bit ranges of the shard's slices (exact partitions of each bit vector)
     const uint64_t cu_start = (cprime(I.b0, Kb) >> G.LC) + I.b0;
     const uint64_t pu_start = (pprime(I.b0, Ob, Kb) >> G.LP) + I.b0;
-    const uint64_t cu_end = last ? c_up_total : (cprime(I.b1, Kb + I.nl) >> G.LC) + I.b1;
-    const uint64_t pu_end = last ? p_up_total : (pprime(I.b1, Ob + I.Dl, Kb + I.nl) >> G.LP) + I.b1;
-    const uint64_t cl_start = e0 * G.LC, cl_bits = cnt * G.LC;
-    const uint64_t pl_start = e0 * G.LP, pl_bits = cnt * G.LP;
-    const uint64_t cu_bits = cnt ? cu_end - cu_start : 0, pu_bits = cnt ? pu_end - pu_start : 0;
-    (void)e1;
-    auto words = [](uint64_t bits) { return (bits + 63) / 64; };
-    std::vector<uint64_t> cl(words(cl_bits)), cu(words(cu_bits)), pl(words(pl_bits)), pu(words(pu_bits));
+    const uint64_t cu_end = last ? S.c_up_total : (cprime(I.b1, Kb + I.nl) >> G.LC) + I.b1;
+    const uint64_t pu_end = last ? S.p_up_total : (pprime(I.b1, Ob + I.Dl, Kb + I.nl) >> G.LP) + I.b1;
+    const uint64_t st_[5] = {Ob, I.b0 * G.LC, cu_start, I.b0 * G.LP, pu_start};
+    const uint64_t nb_[5] = {I.Dl, cnt * G.LC, cnt ? cu_end - cu_start : 0, cnt * G.LP, cnt ? pu_end - pu_start : 0};
+    for (int q = 0; q < 5; ++q) {
+        S.start[q] = st_[q];
+        S.nbits[q] = nb_[q];
+    }
+    S.dev[0] = I.d_data;
+    Arena& A = I.A;
+    unsigned long long* d[4];
+    for (int q = 0; q < 4; ++q) {
+        const uint64_t w = (S.nbits[q + 1] + 63) / 64 + 1;
+        d[q] = A.alloc<unsigned long long>(w);
+        CK(cudaMemsetAsync(d[q], 0, w * 8, I.st));
+        S.dev[q + 1] = d[q];
+    }
     if (cnt) {
-        Arena& A = I.A;
-        unsigned long long* d_cl = A.alloc<unsigned long long>(cl.size() + 1);
-        unsigned long long* d_cu = A.alloc<unsigned long long>(cu.size() + 1);
-        unsigned long long* d_pl = A.alloc<unsigned long long>(pl.size() + 1);
-        unsigned long long* d_pu = A.alloc<unsigned long long>(pu.size() + 1);
-        CK(cudaMemsetAsync(d_cl, 0, (cl.size() + 1) * 8, I.st));
-        CK(cudaMemsetAsync(d_cu, 0, (cu.size() + 1) * 8, I.st));
-        CK(cudaMemsetAsync(d_pl, 0, (pl.size() + 1) * 8, I.st));
-        CK(cudaMemsetAsync(d_pu, 0, (pu.size() + 1) * 8, I.st));
         IndexView v{I.b0, I.Bl, Kb, Ob, G.beta};
-        EfSlices e{G.LC, G.LP, G.dC, dR, cl_start, cu_start, pl_start, pu_start, d_cl, d_cu, d_pl, d_pu};
+        EfSlices e{G.LC, G.LP, G.dC, dR, S.start[1], S.start[2], S.start[3], S.start[4], d[0], d[1], d[2], d[3]};
         launch_ef_write(I.C, I.Pbits, v, cnt, e, I.st);
         CKL();
-        if (!cl.empty()) CK(cudaMemcpyAsync(cl.data(), d_cl, cl.size() * 8, cudaMemcpyDeviceToHost, I.st));
-        if (!cu.empty()) CK(cudaMemcpyAsync(cu.data(), d_cu, cu.size() * 8, cudaMemcpyDeviceToHost, I.st));
-        if (!pl.empty()) CK(cudaMemcpyAsync(pl.data(), d_pl, pl.size() * 8, cudaMemcpyDeviceToHost, I.st));
-        if (!pu.empty()) CK(cudaMemcpyAsync(pu.data(), d_pu, pu.size() * 8, cudaMemcpyDeviceToHost, I.st));
-        CK(cudaStreamSynchronize(I.st));
     }
-    // part = global header fields + five slices
+    return S;
+}
+
+void Shard::finish(long long dR, std::vector<uint8_t>& part) {
+    Impl& I = *impl_;
+    auto t0 = std::chrono::steady_clock::now();
+    const ShardSlices S = make_slices(I, dR);
+    const Globals& G = I.G;
+    // part = global header fields + five slices, copied straight from the device
     part.clear();
     part.insert(part.end(), {'R', 'S', 'P', 'T'});
     put_le(part, 1, 4);
-    const uint64_t hdr[16] = {I.p.leaf, I.p.rf ? 1u : 0u, I.p.bucket, I.p.g, G.n, B, G.D, G.dC, G.beta,
-                              (uint64_t)dR, G.LC, G.LP, k * G.LC, c_up_total, k * G.LP, p_up_total};
+    const uint64_t hdr[16] = {I.p.leaf, I.p.rf ? 1u : 0u, I.p.bucket, I.p.g, G.n, I.B, G.D, G.dC, G.beta,
+                              (uint64_t)dR, G.LC, G.LP, S.k * G.LC, S.c_up_total, S.k * G.LP, S.p_up_total};
     for (uint64_t x : hdr) put_le(part, x, 8);
-    put_slice(part, Ob, I.Dl, data_words_.data());
-    put_slice(part, cl_start, cl_bits, cl.data());
-    put_slice(part, cu_start, cu_bits, cu.data());
-    put_slice(part, pl_start, pl_bits, pl.data());
-    put_slice(part, pu_start, pu_bits, pu.data());
-    stats.index_bits = 0;
+    size_t total = part.size();
+    for (int q = 0; q < 5; ++q) total += 16 + 8 * ((S.nbits[q] + 63) / 64);
+    part.reserve(total);
+    for (int q = 0; q < 5; ++q) {
+        put_le(part, S.start[q], 8);
+        put_le(part, S.nbits[q], 8);
+        const size_t nb = 8 * ((S.nbits[q] + 63) / 64);
+        const size_t at = part.size();
+        part.resize(at + nb);
+        if (nb) CK(cudaMemcpyAsync(part.data() + at, S.dev[q], nb, cudaMemcpyDeviceToHost, I.st));
+    }
+    CK(cudaStreamSynchronize(I.st));
+    stats.t_d2h += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void Shard::finish_blob(long long dR, std::vector<uint8_t>& blob) {
+    Impl& I = *impl_;
+    if (I.world != 1) throw Error(RECSPLIT_E_INVALID, "finish_blob needs a single shard");
+    auto t0 = std::chrono::steady_clock::now();
+    const ShardSlices S = make_slices(I, dR);
+    const Globals& G = I.G;
+    // single shard: every slice starts at bit 0 of its section -> D2H into the final layout
+    auto nbytes = [](uint64_t bits) { return (size_t)(8 * ((bits + 63) / 64)); };
+    const size_t size = 72 + 2 * 24 + nbytes(S.nbits[1]) + nbytes(S.nbits[2]) + nbytes(S.nbits[3]) +
+                        nbytes(S.nbits[4]) + nbytes(S.nbits[0]);
+    blob.clear();
+    blob.reserve(size);
+    blob.push_back('R');
+    blob.push_back('S');
+    blob.push_back('R');
+    blob.push_back('F');
+    put_le(blob, 1, 2);
+    blob.push_back((uint8_t)I.p.leaf);
+    blob.push_back(I.p.rf ? 1 : 0);
+    put_le(blob, I.p.bucket, 4);
+    put_le(blob, 0, 4);
+    for (uint64_t x : {I.p.g, G.n, I.B, G.D, G.dC, G.beta, (uint64_t)dR}) put_le(blob, x, 8);
+    auto section = [&](int q) {
+        put_le(blob, S.nbits[q], 8);
+        const size_t nb = nbytes(S.nbits[q]), at = blob.size();
+        blob.resize(at + nb);
+        if (nb) CK(cudaMemcpyAsync(blob.data() + at, S.dev[q], nb, cudaMemcpyDeviceToHost, I.st));
+    };
+    blob.push_back((uint8_t)G.LC);
+    for (int z = 0; z < 7; ++z) blob.push_back(0);
+    section(1);
+    section(2);
+    blob.push_back((uint8_t)G.LP);
+    for (int z = 0; z < 7; ++z) blob.push_back(0);
+    section(3);
+    section(4);
+    const size_t nb = nbytes(S.nbits[0]), at = blob.size();
+    blob.resize(at + nb);
+    if (nb) CK(cudaMemcpyAsync(blob.data() + at, S.dev[0], nb, cudaMemcpyDeviceToHost, I.st));
+    CK(cudaStreamSynchronize(I.st));
     stats.t_d2h += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -693,13 +752,17 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
     long long dR = LLONG_MAX;  // allreduce-min (local exchange)
     for (auto& s : shards) dR = std::min(dR, s->min_step(all.data()));
     if (dR == LLONG_MAX) dR = 0;
-    std::vector<std::vector<uint8_t>> parts(world);
-    std::vector<std::pair<const uint8_t*, size_t>> views;
-    for (int r = 0; r < world; ++r) {
-        shards[r]->finish(dR, parts[r]);
-        views.emplace_back(parts[r].data(), parts[r].size());
+    if (world == 1) {
+        shards[0]->finish_blob(dR, out.bytes);
+    } else {
+        std::vector<std::vector<uint8_t>> parts(world);
+        std::vector<std::pair<const uint8_t*, size_t>> views;
+        for (int r = 0; r < world; ++r) {
+            shards[r]->finish(dR, parts[r]);
+            views.emplace_back(parts[r].data(), parts[r].size());
+        }
+        stitch(views, out.bytes);
     }
-    stitch(views, out.bytes);
     recsplit_stats& S = out.stats;
     memset(&S, 0, sizeof S);
     for (auto& s : shards) {

@@ -55,14 +55,15 @@ class Shard {
     long long min_step(const uint64_t* all_summaries);
     // phase 3: EF and data slices at their global bit positions -> serialized part
     void finish(long long dR, std::vector<uint8_t>& part);
+    // phase 3 for a single shard (world 1): the serialized MPHF directly
+    void finish_blob(long long dR, std::vector<uint8_t>& blob);
     const Globals& globals() const;
+    struct Impl;
     std::vector<uint64_t> values;  // node values of the shard (want_values)
     recsplit_stats stats{};
 
    private:
-    struct Impl;
     Impl* impl_;
-    std::vector<uint64_t> data_words_;
 };
 
 // OR all parts' slices into the serialized MPHF
