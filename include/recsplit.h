@@ -131,6 +131,21 @@ RECSPLIT_API int recsplit_build_values(const uint64_t *keys, size_t n, uint32_t 
                           uint32_t bucket_size, const recsplit_options *opt, recsplit_bytes *out,
                           uint64_t **values, size_t *n_values);
 
+/*
+ * String keys (the paper's competitor workload P:386-388).  Key i is the
+ * byte string data[offsets[i] .. offsets[i+1]) (HOST arrays; offsets has n+1 non-decreasing
+ * entries).  Its master hash code is reading R16; everything after step A1 is
+ * the same pipeline.  The header records the key type (flags bit 1).  Equal strings ->
+ * RECSPLIT_E_DUPLICATE.
+ */
+RECSPLIT_API int recsplit_build_strings(const uint8_t *data, const uint64_t *offsets, size_t n,
+                                        uint32_t leaf_size, uint32_t bucket_size,
+                                        const recsplit_options *opt, recsplit_bytes *out,
+                                        recsplit_stats *stats);
+/* Host evaluation of a string-key MPHF on n strings (same layout as recsplit_build_strings). */
+RECSPLIT_API int recsplit_query_strings(const uint8_t *mphf, size_t size, const uint8_t *data,
+                                        const uint64_t *offsets, size_t n, uint64_t *out);
+
 /* Evaluate the MPHF serialized at mphf[0..size) on one key (host).  For a key of
  * the build set the result is its unique index in [0, n); otherwise some value in
  * [0, n).  Corrupt blobs -> RECSPLIT_E_FORMAT. */

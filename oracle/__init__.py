@@ -62,6 +62,12 @@ def lib():
         L.oracle_query_many.restype = i32
         L.oracle_query_many.argtypes = [P8, u64, P64, u64, P64]
         L.oracle_free.restype, L.oracle_free.argtypes = None, [C.c_void_p]
+        L.oracle_mhc_string.restype = None
+        L.oracle_mhc_string.argtypes = [P8, u64, u64, P64, P64]
+        L.oracle_build_strings.restype = i32
+        L.oracle_build_strings.argtypes = [P8, P64, u64, u32, u32, i32, u64, i32, C.POINTER(P8), C.POINTER(u64)]
+        L.oracle_query_strings.restype = i32
+        L.oracle_query_strings.argtypes = [P8, u64, P8, P64, u64, P64]
         _lib = L
     return _lib
 
@@ -195,4 +201,47 @@ def query_many(blob: bytes, keys) -> np.ndarray:
                                  len(keys), _p64(out))
     if rc:
         raise OracleError(rc, "oracle_query_many")
+    return out
+
+
+# ---------------------------------------------------------------- string keys (N4) --
+
+def _p8(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def mhc_string(s: bytes, g: int = 0) -> tuple[int, int]:
+    buf = np.frombuffer(s, dtype=np.uint8) if len(s) else np.zeros(1, np.uint8)
+    hi, lo = C.c_uint64(), C.c_uint64()
+    lib().oracle_mhc_string(_p8(buf), len(s), g, C.byref(hi), C.byref(lo))
+    return hi.value, lo.value
+
+
+def build_strings(data, offsets, leaf: int, bucket: int, rf: bool = True, g: int = 0, threads: int = 1) -> bytes:
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    if data.size == 0:
+        data = np.zeros(1, np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    out = C.POINTER(C.c_uint8)()
+    size = C.c_uint64()
+    rc = lib().oracle_build_strings(_p8(data), _p64(offsets), len(offsets) - 1, leaf, bucket, int(rf), g, threads,
+                                    C.byref(out), C.byref(size))
+    if rc:
+        raise OracleError(rc, "oracle_build_strings")
+    blob = C.string_at(out, size.value)
+    lib().oracle_free(out)
+    return blob
+
+
+def query_strings(blob: bytes, data, offsets) -> np.ndarray:
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    if data.size == 0:
+        data = np.zeros(1, np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = len(offsets) - 1
+    out = np.zeros(n, dtype=np.uint64)
+    b = np.frombuffer(blob, dtype=np.uint8)
+    rc = lib().oracle_query_strings(_p8(b), len(blob), _p8(data), _p64(offsets), n, _p64(out))
+    if rc:
+        raise OracleError(rc, "oracle_query_strings")
     return out

@@ -59,6 +59,25 @@ void oracle_mhc(u64 key, u64 g, u64 *hi, u64 *lo) {
     *lo = oracle_remix(key ^ g ^ 0xC2B2AE3D27D4EB4FULL);
 }
 
+/* Reading R16 (string keys; the paper's competitor workload P:386-388):
+ * MHC of a byte string = two length-salted SplitMix64 chains over its 8-byte little-endian
+ * chunks (last chunk zero-padded): h = seed ^ len*0x9E3779B97F4A7C15; h = remix(h ^ chunk)
+ * per chunk; result remix(h).  hi uses seed g^C_HI, lo uses seed g^C_LO. */
+static u64 str_chain(const u8 *s, u64 len, u64 seed) {
+    u64 h = seed ^ (len * 0x9E3779B97F4A7C15ULL);
+    for (u64 i = 0; i < len; i += 8) {
+        u64 c = 0;
+        for (u64 t = 0; t < 8 && i + t < len; t++) c |= (u64)s[i + t] << (8 * t);
+        h = oracle_remix(h ^ c);
+    }
+    return oracle_remix(h);
+}
+
+void oracle_mhc_string(const u8 *s, u64 len, u64 g, u64 *hi, u64 *lo) {
+    *hi = str_chain(s, len, g ^ 0x9E3779B97F4A7C15ULL);
+    *lo = str_chain(s, len, g ^ 0xC2B2AE3D27D4EB4FULL);
+}
+
 /* Reading R3: "a hash function modulo l" as the fixed-point reduction
  * floor(high32(h) * r / 2^32). */
 u32 oracle_remap(u64 h, u64 r) { return (u32)(((h >> 32) * r) >> 32); }
@@ -484,23 +503,54 @@ static void put_words(u8 **p, const u64 *w, u64 nbits) {
  * If values_out is non-NULL it receives all node values (bucket order, each
  * bucket in preorder) for diagnostics.
  */
+static int cmp_mhc_full(const void *a, const void *b) {
+    const mhc_t *x = (const mhc_t *)a, *y = (const mhc_t *)b;
+    if (x->hi != y->hi) return (x->hi > y->hi) - (x->hi < y->hi);
+    return (x->lo > y->lo) - (x->lo < y->lo);
+}
+
+/* core construction over precomputed master hash codes (mk, n entries, consumed);
+ * flags bit0 = rotation fitting, bit1 = string keys (recorded in the header) */
+static int build_core(mhc_t *mk, u64 n, u32 leaf, u32 bsize, int flags, u64 g, int threads, u8 **out,
+                      u64 *out_size, u64 **values_out, u64 *n_values);
+
 int oracle_build_ex(const u64 *keys, u64 n, u32 leaf, u32 bsize, int rf, u64 g, int threads,
                     u8 **out, u64 *out_size, u64 **values_out, u64 *n_values) {
     *out = NULL;
     *out_size = 0;
-    if (values_out) *values_out = NULL;
-    if (n_values) *n_values = 0;
     if (n == 0 || leaf < 2 || leaf > 24 || bsize < 1 || n >= (1ULL << 32)) return ORC_E_INVALID;
-    if (threads < 1) threads = 1;
-    u64 B = (n + bsize - 1) / bsize; /* reading R12 */
-
-    /* 1. MHC, sort by hi (bucket is monotone in hi), duplicate check */
     mhc_t *mk = (mhc_t *)malloc((size_t)n * sizeof(mhc_t));
     if (!mk) return ORC_E_NOMEM;
     for (u64 i = 0; i < n; i++) oracle_mhc(keys[i], g, &mk[i].hi, &mk[i].lo);
-    qsort(mk, (size_t)n, sizeof(mhc_t), cmp_mhc);
+    return build_core(mk, n, leaf, bsize, rf ? 1 : 0, g, threads, out, out_size, values_out, n_values);
+}
+
+/* String keys (N4): key i is bytes[offsets[i] .. offsets[i+1]). */
+int oracle_build_strings(const u8 *bytes, const u64 *offsets, u64 n, u32 leaf, u32 bsize, int rf, u64 g,
+                         int threads, u8 **out, u64 *out_size) {
+    *out = NULL;
+    *out_size = 0;
+    if (n == 0 || leaf < 2 || leaf > 24 || bsize < 1 || n >= (1ULL << 32)) return ORC_E_INVALID;
+    mhc_t *mk = (mhc_t *)malloc((size_t)n * sizeof(mhc_t));
+    if (!mk) return ORC_E_NOMEM;
+    for (u64 i = 0; i < n; i++)
+        oracle_mhc_string(bytes + offsets[i], offsets[i + 1] - offsets[i], g, &mk[i].hi, &mk[i].lo);
+    return build_core(mk, n, leaf, bsize, (rf ? 1 : 0) | 2, g, threads, out, out_size, NULL, NULL);
+}
+
+static int build_core(mhc_t *mk, u64 n, u32 leaf, u32 bsize, int flags, u64 g, int threads, u8 **out,
+                      u64 *out_size, u64 **values_out, u64 *n_values) {
+    const int rf = flags & 1;
+    if (values_out) *values_out = NULL;
+    if (n_values) *n_values = 0;
+    if (threads < 1) threads = 1;
+    u64 B = (n + bsize - 1) / bsize; /* reading R12 */
+
+    /* 1. sort by MHC (bucket is monotone in hi), duplicate check: equal master hash codes
+     *    (for u64 keys equal hi <=> equal key, R2; for strings equal (hi, lo)) */
+    qsort(mk, (size_t)n, sizeof(mhc_t), cmp_mhc_full);
     for (u64 i = 1; i < n; i++)
-        if (mk[i].hi == mk[i - 1].hi) {
+        if (mk[i].hi == mk[i - 1].hi && mk[i].lo == mk[i - 1].lo) {
             free(mk);
             return ORC_E_DUPLICATE;
         }
@@ -634,7 +684,7 @@ int oracle_build_ex(const u64 *keys, u64 n, u32 leaf, u32 bsize, int rf, u64 g, 
         put_u8(&p, 'F');
         put_u16(&p, 1);
         put_u8(&p, (u8)leaf);
-        put_u8(&p, (u8)(rf ? 1 : 0));
+        put_u8(&p, (u8)(flags & 3));
         put_u32(&p, bsize);
         put_u32(&p, 0);
         put_u64(&p, g);
@@ -752,7 +802,19 @@ static const u8 *parse_ef(const u8 *p, const u8 *end, ef_view *e) {
 /* Query: bucket -> index -> descend splits summing left sibling
  * sizes -> leaf value (+ r mod m for B keys under rotation fitting).
  * Decodes the index once, then evaluates every key. */
+static int query_impl(const u8 *blob, u64 size, const u64 *keys, const u8 *sbytes, const u64 *soff, u64 nk,
+                      u64 *out);
+
 int oracle_query_many(const u8 *blob, u64 size, const u64 *keys, u64 nk, u64 *out) {
+    return query_impl(blob, size, keys, NULL, NULL, nk, out);
+}
+
+int oracle_query_strings(const u8 *blob, u64 size, const u8 *bytes, const u64 *offsets, u64 nk, u64 *out) {
+    return query_impl(blob, size, NULL, bytes, offsets, nk, out);
+}
+
+static int query_impl(const u8 *blob, u64 size, const u64 *keys, const u8 *sbytes, const u64 *soff, u64 nk,
+                      u64 *out) {
     if (size < 72 || memcmp(blob, "RSRF", 4) != 0) return ORC_E_FORMAT;
     const u8 *end = blob + size;
     u32 leaf = blob[6];
@@ -781,9 +843,18 @@ int oracle_query_many(const u8 *blob, u64 size, const u64 *keys, u64 nk, u64 *ou
     tables T;
     tables_init(&T, leaf, rf, (u32)smax);
 
+    if (((blob[7] >> 1) & 1) != (keys == NULL)) {  /* key type must match the MPHF's */
+        tables_free(&T);
+        free(C);
+        free(P);
+        return ORC_E_FORMAT;
+    }
     for (u64 kk = 0; kk < nk; kk++) {
         u64 hi, lo;
-        oracle_mhc(keys[kk], g, &hi, &lo);
+        if (keys)
+            oracle_mhc(keys[kk], g, &hi, &lo);
+        else
+            oracle_mhc_string(sbytes + soff[kk], soff[kk + 1] - soff[kk], g, &hi, &lo);
         u64 i = oracle_remap(hi, B);
         u64 s = C[i + 1] - C[i];
         if (s == 0) {
@@ -834,7 +905,7 @@ int oracle_query_many(const u8 *blob, u64 size, const u64 *keys, u64 nk, u64 *ou
 }
 
 int oracle_query(const u8 *blob, u64 size, u64 key, u64 *out) {
-    return oracle_query_many(blob, size, &key, 1, out);
+    return query_impl(blob, size, &key, NULL, NULL, 1, out);
 }
 
 void oracle_free(void *p) { free(p); }

@@ -24,7 +24,7 @@ SYMBOLS = [
     "recsplit_bits_per_key", "recsplit_search_leaves", "recsplit_search_splits", "recsplit_tau",
     "recsplit_free", "recsplit_free_ptr", "recsplit_last_error", "recsplit_shard_begin",
     "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch", "recsplit_shard_free",
-    "recsplit_shard_globals", "recsplit_query_device",
+    "recsplit_shard_globals", "recsplit_query_device", "recsplit_build_strings", "recsplit_query_strings",
 ]
 
 
@@ -86,6 +86,11 @@ def lib():
         L.recsplit_bits_per_key.argtypes = [P8, sz, C.POINTER(C.c_double)]
         L.recsplit_query_device.argtypes = [P8, sz, C.c_void_p, sz, C.c_void_p, C.c_void_p]
         L.recsplit_query_device.restype = i32
+        L.recsplit_build_strings.argtypes = [P8, P64, sz, u32, u32, C.POINTER(Options), C.POINTER(Bytes),
+                                             C.POINTER(Stats)]
+        L.recsplit_build_strings.restype = i32
+        L.recsplit_query_strings.argtypes = [P8, sz, P8, P64, sz, P64]
+        L.recsplit_query_strings.restype = i32
         L.recsplit_search_leaves.argtypes = [P64, P8, P32, u32, u32, P64]
         L.recsplit_search_splits.argtypes = [P64, P32, u32, u32, P64]
         L.recsplit_tau.argtypes = [u32, u32, u32]
@@ -178,6 +183,35 @@ def build_values(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool 
     vals = np.ctypeslib.as_array(vp, shape=(nv.value,)).copy() if nv.value else np.zeros(0, np.uint64)
     lib().recsplit_free_ptr(vp)
     return _take(b), vals
+
+
+def build_strings(data, offsets, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
+                  global_seed: int = 0, stats: bool = False):
+    """Build from string keys: data (uint8) holds key i at data[offsets[i]:offsets[i+1]]."""
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    if data.size == 0:
+        data = np.zeros(1, np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    b = Bytes()
+    st = Stats()
+    o = _opts(rotation_fitting, global_seed, -1, 0)
+    _check(lib().recsplit_build_strings(data.ctypes.data_as(C.POINTER(C.c_uint8)), _p64(offsets), len(offsets) - 1,
+                                        leaf_size, bucket_size, C.byref(o), C.byref(b), C.byref(st)))
+    blob = _take(b)
+    return (blob, st.as_dict()) if stats else blob
+
+
+def query_strings(blob: bytes, data, offsets) -> np.ndarray:
+    data = np.ascontiguousarray(data, dtype=np.uint8)
+    if data.size == 0:
+        data = np.zeros(1, np.uint8)
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    out = np.zeros(len(offsets) - 1, dtype=np.uint64)
+    buf = np.frombuffer(blob, dtype=np.uint8)
+    _check(lib().recsplit_query_strings(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob),
+                                        data.ctypes.data_as(C.POINTER(C.c_uint8)), _p64(offsets), len(out),
+                                        _p64(out)))
+    return out
 
 
 def query(blob: bytes, key: int) -> int:

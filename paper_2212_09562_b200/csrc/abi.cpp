@@ -184,10 +184,25 @@ bool skip_ones(const uint8_t* d, uint64_t D, uint64_t& pos, uint64_t cnt) {
     return true;
 }
 
+// master hash code of a string key (R16): two length-salted chains over 8-byte chunks
+uint64_t str_chain(const uint8_t* s, uint64_t len, uint64_t seed) {
+    uint64_t h = seed ^ (len * 0x9E3779B97F4A7C15ULL);
+    for (uint64_t i = 0; i < len; i += 8) {
+        uint64_t c = 0;
+        for (uint64_t t = 0; t < 8 && i + t < len; ++t) c |= (uint64_t)s[i + t] << (8 * t);
+        h = remix(h ^ c);
+    }
+    return remix(h);
+}
+
+int query_mhc(const Parsed& M, uint64_t hi, uint64_t lo, uint64_t* out);
+
 int query_one(const Parsed& M, uint64_t key, uint64_t* out) {
+    return query_mhc(M, remix(key ^ M.g ^ 0x9E3779B97F4A7C15ULL), remix(key ^ M.g ^ 0xC2B2AE3D27D4EB4FULL), out);
+}
+
+int query_mhc(const Parsed& M, uint64_t hi, uint64_t lo, uint64_t* out) {
     const rs::Tables& T = *M.T;
-    const uint64_t hi = remix(key ^ M.g ^ 0x9E3779B97F4A7C15ULL);
-    const uint64_t lo = remix(key ^ M.g ^ 0xC2B2AE3D27D4EB4FULL);
     const uint64_t i = remap(hi, M.B);
     uint64_t s = M.C[i + 1] - M.C[i];
     uint64_t offset = M.C[i];
@@ -290,6 +305,7 @@ int recsplit_query(const uint8_t* mphf, size_t size, uint64_t key, uint64_t* out
         Parsed M;
         int rc = parse(mphf, size, M);
         if (rc) return rc;
+        if (M.strings) return fail(RECSPLIT_E_FORMAT, "MPHF was built from string keys");
         return query_one(M, key, out_index);
     });
 }
@@ -300,6 +316,7 @@ int recsplit_query_many(const uint8_t* mphf, size_t size, const uint64_t* keys, 
         Parsed M;
         int rc = parse(mphf, size, M);
         if (rc) return rc;
+        if (M.strings) return fail(RECSPLIT_E_FORMAT, "MPHF was built from string keys");
         unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 64));
         if (n < 100000) nt = 1;
         std::vector<int> rcs(nt, 0);
@@ -335,8 +352,84 @@ int recsplit_query_device(const uint8_t* mphf, size_t size, const uint64_t* d_ke
         Parsed M;
         int rc = parse(mphf, size, M);
         if (rc) return rc;
+        if (M.strings) return fail(RECSPLIT_E_FORMAT, "device query of string-key MPHFs is not supported");
         select_device(-1);
         rs::query_on_device(M, d_keys, n, d_out, (cudaStream_t)stream);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_build_strings(const uint8_t* data, const uint64_t* offsets, size_t n, uint32_t leaf_size,
+                           uint32_t bucket_size, const recsplit_options* opt, recsplit_bytes* out,
+                           recsplit_stats* stats) {
+    if (!out) return fail(RECSPLIT_E_INVALID, "out is NULL");
+    out->data = nullptr;
+    out->size = 0;
+    if (!offsets || (!data && n && offsets[n])) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    int rc = check_args(n, leaf_size, bucket_size);
+    if (rc) return rc;
+    for (size_t i = 0; i < n; ++i)
+        if (offsets[i + 1] < offsets[i]) return fail(RECSPLIT_E_INVALID, "offsets must be non-decreasing");
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        auto t0 = std::chrono::steady_clock::now();
+        rs::BuildParams p = params_of(n, leaf_size, bucket_size, opt);
+        p.strings = true;
+        select_device(p.device);
+        cudaStream_t st;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+            throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{st};
+        const uint64_t nbytes = offsets[n] - offsets[0];
+        uint8_t* d_data = nullptr;
+        uint64_t *d_off = nullptr, *d_mhc = nullptr;
+        if (cudaMallocAsync(&d_data, std::max<uint64_t>(nbytes, 16), st) != cudaSuccess ||
+            cudaMallocAsync(&d_off, (n + 1) * 8, st) != cudaSuccess ||
+            cudaMallocAsync(&d_mhc, 2 * n * 8, st) != cudaSuccess)
+            throw rs::Error(RECSPLIT_E_NOMEM, "device allocation failed");
+        struct Guard {
+            void *a, *b, *c;
+            cudaStream_t s;
+            ~Guard() {
+                cudaFreeAsync(a, s);
+                cudaFreeAsync(b, s);
+                cudaFreeAsync(c, s);
+            }
+        } gd{d_data, d_off, d_mhc, st};
+        std::vector<uint64_t> off0(offsets, offsets + n + 1);
+        for (auto& x : off0) x -= offsets[0];
+        if (nbytes && cudaMemcpyAsync(d_data, data + offsets[0], nbytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+            throw rs::Error(RECSPLIT_E_CUDA, "H2D failed");
+        if (cudaMemcpyAsync(d_off, off0.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+            throw rs::Error(RECSPLIT_E_CUDA, "H2D failed");
+        rs::launch_mhc_strings(d_data, d_off, n, p.g, d_mhc, st);
+        if (cudaGetLastError() != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, "string hash launch failed");
+        rs::BuildOutput o;
+        rs::build_on_device(d_mhc, p, st, false, o);
+        o.stats.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (stats) *stats = o.stats;
+        return emit(o, out);
+    });
+}
+
+int recsplit_query_strings(const uint8_t* mphf, size_t size, const uint8_t* data, const uint64_t* offsets, size_t n,
+                           uint64_t* out) {
+    if ((!offsets || !out) && n) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    return guarded([&]() -> int {
+        Parsed M;
+        int rc = parse(mphf, size, M);
+        if (rc) return rc;
+        if (!M.strings) return fail(RECSPLIT_E_FORMAT, "MPHF was built from 64-bit keys");
+        for (size_t i = 0; i < n; ++i) {
+            const uint8_t* s = data + offsets[i];
+            const uint64_t len = offsets[i + 1] - offsets[i];
+            rc = query_mhc(M, str_chain(s, len, M.g ^ 0x9E3779B97F4A7C15ULL),
+                           str_chain(s, len, M.g ^ 0xC2B2AE3D27D4EB4FULL), out + i);
+            if (rc) return rc;
+        }
         return RECSPLIT_OK;
     });
 }

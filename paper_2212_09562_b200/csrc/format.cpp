@@ -75,6 +75,7 @@ int parse_mphf(const uint8_t* blob, size_t size, Parsed& M, std::string* err) {
     if (ver != 1) return fail(RECSPLIT_E_FORMAT, "unsupported format version");
     M.leaf = blob[6];
     M.rf = blob[7] & 1;
+    M.strings = (blob[7] >> 1) & 1;
     if (M.leaf < 2 || M.leaf > 24) return fail(RECSPLIT_E_FORMAT, "bad leaf size");
     M.g = rd64(blob + 16);
     M.n = rd64(blob + 24);

@@ -19,6 +19,7 @@ struct EFView {
 struct Parsed {
     uint32_t leaf;
     bool rf;
+    bool strings;  // built from string keys (header flags bit 1, R16)
     uint64_t g, n, B, D, dC, beta;
     int64_t dR;
     EFView ec, ep;

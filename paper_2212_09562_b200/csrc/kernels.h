@@ -24,8 +24,11 @@ void exscan_u64(const u64* in, u64* out, size_t n, void* temp, cudaStream_t st);
 // ---- partition (partition.cu), steps A1-A2 of SURVEY section 8(a).
 // master hash code -> lo, A/B bit, bucket id; bucket histogram (zeroed); keys of buckets
 // [b0, b1) only (local bucket ids; others get bkt = NONE)
-void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt, u32* hist,
-                 cudaStream_t st);
+// (keys == nullptr: precomputed master hash codes in mhc, 2 u64 per key)
+void launch_hash(const u64* keys, const u64* mhc, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt,
+                 u32* hist, cudaStream_t st);
+// string keys: master hash codes (R16) of data[off[i] .. off[i+1]) into mhc (2 u64 per key)
+void launch_mhc_strings(const u8* data, const u64* off, u64 n, u64 g, u64* mhc, cudaStream_t st);
 // exact duplicate check per bucket after the scatter (dup[0..1] zeroed)
 void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, cudaStream_t st);
 // max/min bucket size and the histogram of bucket sizes (size_hist zeroed, cap+1 entries)

@@ -13,9 +13,11 @@ using namespace rsd;
 // buckets (one global atomic per bucket per block), else global.
 // Only buckets in [b0, b1) (this shard, P:320 contiguous bucket ranges) are kept; their
 // local index b - b0 goes to bkt, other keys get bkt = NONE.
-__global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u64 b0,
-                                               u64 b1, u64* __restrict__ lo, u8* __restrict__ ab,
-                                               u32* __restrict__ bkt, u32* __restrict__ hist, int smem_hist) {
+// keys == nullptr: the master hash codes are given (mhc[2i] = hi, mhc[2i+1] = lo; string keys).
+__global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, const u64* __restrict__ mhc, u64 n,
+                                               u64 g, u64 B, u64 b0, u64 b1, u64* __restrict__ lo,
+                                               u8* __restrict__ ab, u32* __restrict__ bkt, u32* __restrict__ hist,
+                                               int smem_hist) {
     extern __shared__ u32 sh[];
     const u64 Bl = b1 - b0;
     if (smem_hist) {
@@ -23,15 +25,15 @@ __global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64
         __syncthreads();
     }
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        const u64 k = keys[i] ^ g;
-        const u64 h = remix64(k ^ MHC_SALT_HI);
+        const u64 k = keys ? keys[i] ^ g : 0;
+        const u64 h = keys ? remix64(k ^ MHC_SALT_HI) : mhc[2 * i];
         const u64 bg = ((h >> 32) * B) >> 32;
         if (bg < b0 || bg >= b1) {
             bkt[i] = NONE;
             continue;
         }
         const u32 b = (u32)(bg - b0);
-        const u64 l = remix64(k ^ MHC_SALT_LO);
+        const u64 l = keys ? remix64(k ^ MHC_SALT_LO) : mhc[2 * i + 1];
         lo[i] = l;
         ab[i] = (u8)(h & 1);
         bkt[i] = b;
@@ -47,8 +49,8 @@ __global__ void __launch_bounds__(1024) k_hash(const u64* __restrict__ keys, u64
     }
 }
 
-void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt, u32* hist,
-                 cudaStream_t st) {
+void launch_hash(const u64* keys, const u64* mhc, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, u8* ab, u32* bkt,
+                 u32* hist, cudaStream_t st) {
     const u64 Bl = b1 - b0;
     const int smem_hist = Bl <= 12288;
     const size_t smem = smem_hist ? Bl * 4 : 0;
@@ -57,7 +59,7 @@ void launch_hash(const u64* keys, u64 n, u64 g, u64 B, u64 b0, u64 b1, u64* lo, 
     if (grid > cap) grid = cap;
     if (grid == 0) grid = 1;
     cudaFuncSetAttribute(k_hash, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    k_hash<<<grid, 1024, smem, st>>>(keys, n, g, B, b0, b1, lo, ab, bkt, hist, smem_hist);
+    k_hash<<<grid, 1024, smem, st>>>(keys, mhc, n, g, B, b0, b1, lo, ab, bkt, hist, smem_hist);
     g_launches++;
 }
 
@@ -172,6 +174,36 @@ void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, cuda
     const u32 threads = smax <= 128 ? 128 : 256;
     unsigned grid = nb < 148ull * 64 ? (unsigned)nb : 148u * 64;
     k_dedupe<<<grid, threads, smem, st>>>(lo, C, nb, ts, dup);
+    g_launches++;
+}
+
+// String keys (reading R16): master hash code of bytes[off[i] .. off[i+1])
+// = two length-salted SplitMix64 chains over 8-byte little-endian chunks.  One thread per key.
+__device__ __forceinline__ u64 str_chain(const u8* __restrict__ s, u64 len, u64 seed) {
+    u64 h = seed ^ (len * 0x9E3779B97F4A7C15ULL);
+    for (u64 i = 0; i < len; i += 8) {
+        u64 c = 0;
+        const u64 m = len - i < 8 ? len - i : 8;
+        for (u64 t = 0; t < m; ++t) c |= (u64)s[i + t] << (8 * t);
+        h = remix64(h ^ c);
+    }
+    return remix64(h);
+}
+
+__global__ void k_mhc_strings(const u8* __restrict__ data, const u64* __restrict__ off, u64 n, u64 g,
+                              u64* __restrict__ mhc) {
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 a = off[i], len = off[i + 1] - a;
+        mhc[2 * i] = str_chain(data + a, len, g ^ MHC_SALT_HI);
+        mhc[2 * i + 1] = str_chain(data + a, len, g ^ MHC_SALT_LO);
+    }
+}
+
+void launch_mhc_strings(const u8* data, const u64* off, u64 n, u64 g, u64* mhc, cudaStream_t st) {
+    unsigned grid = (unsigned)((n + 255) / 256);
+    if (grid > 148u * 16u) grid = 148u * 16u;
+    if (grid == 0) grid = 1;
+    k_mhc_strings<<<grid, 256, 0, st>>>(data, off, n, g, mhc);
     g_launches++;
 }
 

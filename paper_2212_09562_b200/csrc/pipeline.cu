@@ -314,7 +314,8 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
         S.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
         return;
     }
-    launch_hash(d_keys, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt, hist, st);
+    launch_hash(p.strings ? nullptr : d_keys, p.strings ? d_keys : nullptr, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt,
+                hist, st);
     CKL();
     launch_bucket_stats(hist, Bl, small, size_hist_d, cap, st);
     CKL();
@@ -600,7 +601,7 @@ void Shard::finish(long long dR, std::vector<uint8_t>& part) {
     part.clear();
     part.insert(part.end(), {'R', 'S', 'P', 'T'});
     put_le(part, 1, 4);
-    const uint64_t hdr[16] = {I.p.leaf, I.p.rf ? 1u : 0u, I.p.bucket, I.p.g, G.n, I.B, G.D, G.dC, G.beta,
+    const uint64_t hdr[16] = {I.p.leaf, (I.p.rf ? 1u : 0u) | (I.p.strings ? 2u : 0u), I.p.bucket, I.p.g, G.n, I.B, G.D, G.dC, G.beta,
                               (uint64_t)dR, G.LC, G.LP, S.k * G.LC, S.c_up_total, S.k * G.LP, S.p_up_total};
     for (uint64_t x : hdr) put_le(part, x, 8);
     size_t total = part.size();
@@ -636,7 +637,7 @@ void Shard::finish_blob(long long dR, std::vector<uint8_t>& blob) {
     blob.push_back('F');
     put_le(blob, 1, 2);
     blob.push_back((uint8_t)I.p.leaf);
-    blob.push_back(I.p.rf ? 1 : 0);
+    blob.push_back((uint8_t)((I.p.rf ? 1 : 0) | (I.p.strings ? 2 : 0)));
     put_le(blob, I.p.bucket, 4);
     put_le(blob, 0, 4);
     for (uint64_t x : {I.p.g, G.n, I.B, G.D, G.dC, G.beta, (uint64_t)dR}) put_le(blob, x, 8);

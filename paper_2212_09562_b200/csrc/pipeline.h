@@ -23,6 +23,7 @@ struct BuildParams {
     uint64_t g;
     int device;
     uint32_t shards;  // virtual shards (>= 1)
+    bool strings = false;  // keys are precomputed master hash codes of strings (2 u64 each, R16)
 };
 
 struct BuildOutput {
@@ -69,7 +70,12 @@ class Shard {
 // OR all parts' slices into the serialized MPHF
 void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::vector<uint8_t>& blob);
 
-// d_keys: device pointer (n keys) on params.device; work ordered on st.
+// string keys (R16): master hash codes of data[off[i] .. off[i+1]) into mhc (2 u64 per key)
+void launch_mhc_strings(const uint8_t* data, const uint64_t* off, uint64_t n, uint64_t g, uint64_t* mhc,
+                        cudaStream_t st);
+
+// d_keys: device pointer (n keys; params.strings: 2n master-hash words) on params.device;
+// work ordered on st.
 void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, bool want_values,
                      BuildOutput& out);
 

@@ -43,6 +43,24 @@ def keys_device(n: int, seed: int):
         out = torch.cat([u, extra])
 
 
+def strings(n: int, seed: int, min_len: int = 10, max_len: int = 50):
+    """n distinct random byte strings, lengths uniform in [min_len, max_len], bytes in
+    1..255 (the paper's competitor workload: "strings of uniform random length in [10, 50]
+    containing random characters except for the zero byte").  Returns (data uint8,
+    offsets uint64 of n+1 entries).  Distinctness is checked for n <= 2e6 (collisions are
+    astronomically unlikely: >= 255^10 strings per length)."""
+    gen = np.random.Generator(np.random.PCG64(seed))
+    lens = gen.integers(min_len, max_len + 1, size=n, dtype=np.int64)
+    offsets = np.zeros(n + 1, dtype=np.uint64)
+    offsets[1:] = np.cumsum(lens)
+    data = gen.integers(1, 256, size=int(offsets[-1]), dtype=np.uint8)
+    if n <= 2_000_000:
+        seen = {data[offsets[i]:offsets[i + 1]].tobytes() for i in range(n)}
+        if len(seen) != n:
+            raise RuntimeError("duplicate strings; choose another seed")
+    return data, offsets
+
+
 # Workload recipes (BASELINE.json configs); key seeds follow BASELINE.md section 4.
 CONFIGS = {
     "C1": dict(n=10_000, leaf=8, bucket=100, seed=1),

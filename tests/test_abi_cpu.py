@@ -89,3 +89,16 @@ def test_argument_validation():
     with pytest.raises(rs.RecSplitError) as e:
         rs.build(np.zeros(0, np.uint64), 8, 100)
     assert e.value.code == rs.E_INVALID
+
+
+def test_library_string_query_reads_oracle_format():
+    """String keys (N4, R16): the library's host string query reads the oracle's string-key
+    MPHFs (independent implementations of the string hash) and rejects u64 queries."""
+    data, off = synth.strings(4000, 21)
+    blob = oracle.build_strings(data, off, 8, 100, threads=2)
+    q = rs.query_strings(blob, data, off)
+    assert np.array_equal(q, oracle.query_strings(blob, data, off))
+    assert np.array_equal(np.sort(q), np.arange(4000, dtype=np.uint64))
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.query_many(blob, np.array([1], dtype=np.uint64))
+    assert e.value.code == rs.E_FORMAT

@@ -300,3 +300,25 @@ def test_query_device_matches_host_and_oracle(leaf, b, rf, n):
     assert np.array_equal(np.sort(got), np.arange(n, dtype=np.uint64))
     other = torch.from_numpy(synth.keys(5000, 991).view(np.int64)).cuda()
     assert (rs.query_device(blob, other).cpu().numpy().view(np.uint64) < n).all()
+
+
+# --------------------------------------------------------------- string keys --
+
+@pytest.mark.parametrize("leaf,b,n", [(8, 100, 20_000), (16, 2000, 8_000), (5, 5, 10_000), (12, 1000, 30_000)])
+def test_string_keys_full_parity(leaf, b, n):
+    """strings of length 10..50: GPU bytes == oracle bytes, bijective."""
+    data, off = synth.strings(n, leaf * 13 + b)
+    want = oracle.build_strings(data, off, leaf, b, threads=os.cpu_count())
+    got = rs.build_strings(data, off, leaf, b)
+    assert got == want
+    q = rs.query_strings(got, data, off)
+    assert np.array_equal(np.sort(q), np.arange(n, dtype=np.uint64))
+
+
+def test_string_keys_duplicate_rejected():
+    data, off = synth.strings(3000, 5)
+    d2 = np.concatenate([data, data[off[10]:off[11]]])
+    o2 = np.concatenate([off, [off[-1] + (off[11] - off[10])]]).astype(np.uint64)
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.build_strings(d2, o2, 8, 100)
+    assert e.value.code == rs.E_DUPLICATE

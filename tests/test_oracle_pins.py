@@ -564,3 +564,46 @@ def test_bits_per_object_vs_paper_l8_b100():
     keys = synth.keys(500_000, 77)
     bpo = bits_per_object(oracle.build(keys, 8, 100, threads=os.cpu_count() or 1))
     assert abs(bpo - 1.806) < 0.012, bpo
+
+
+# ----------------------------------------------------------- string keys (N4) --
+
+def _np_str_chain(s: bytes, seed: int) -> int:
+    """R16 written out directly (the remix itself is pinned above): length-salted chain."""
+    h = (seed ^ (len(s) * 0x9E3779B97F4A7C15)) & M64
+    for i in range(0, len(s), 8):
+        h = oracle.remix(h ^ int.from_bytes(s[i:i + 8], "little"))
+    return oracle.remix(h)
+
+
+def test_string_mhc_chain_and_properties():
+    """R16: the string MHC equals its definition on assorted lengths (incl. 0, 8, 9), is
+    deterministic, length-sensitive (a zero byte appended changes it) and, on 2e4 random
+    strings, free of collisions with about half the strings in B (R7)."""
+    for s in [b"", b"a", b"abcdefgh", b"abcdefghi", bytes(range(1, 51)), b"\x00" * 8]:
+        hi, lo = oracle.mhc_string(s)
+        assert hi == _np_str_chain(s, 0x9E3779B97F4A7C15) and lo == _np_str_chain(s, 0xC2B2AE3D27D4EB4F)
+    assert oracle.mhc_string(b"abc") != oracle.mhc_string(b"abc\x00")
+    assert oracle.mhc_string(b"abc", 1) != oracle.mhc_string(b"abc", 0)
+    data, off = synth.strings(20000, 3)
+    codes = {oracle.mhc_string(data[off[i]:off[i + 1]].tobytes()) for i in range(20000)}
+    assert len(codes) == 20000
+    nb = sum(h & 1 for h, _ in codes)
+    assert abs(nb - 10000) < 4 * math.sqrt(5000)
+
+
+def test_string_build_bijective_and_typed():
+    """Strings of length 10..50: the MPHF is a bijection on S; a u64-key query on a
+    string-key MPHF is rejected (header flag bit 1)."""
+    data, off = synth.strings(5000, 9)
+    blob = oracle.build_strings(data, off, 8, 100, threads=2)
+    assert blob[7] == 3
+    q = oracle.query_strings(blob, data, off)
+    assert sorted(q.tolist()) == list(range(5000))
+    with pytest.raises(oracle.OracleError):
+        oracle.query_many(blob, np.array([1, 2], dtype=np.uint64))
+    dup_off = np.concatenate([off, [off[-1] + (off[1] - off[0])]]).astype(np.uint64)
+    dup_data = np.concatenate([data, data[off[0]:off[1]]])
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.build_strings(dup_data, dup_off, 8, 100)
+    assert e.value.rc == oracle.E_DUPLICATE
