@@ -20,6 +20,7 @@
 //    result equals the sequential search.
 //  * phases of small nodes ("batch" mode): a warp takes `batch` nodes per cursor atomic
 //    and searches each alone, windows in increasing order, first hit wins.
+#include <cstdlib>
 #include <algorithm>
 
 #include "kernels.h"
@@ -49,7 +50,9 @@ struct Args {
     u32 iters;
     u32 warp_cap;
     int help;
-    u32 batch;  // nodes per cursor atomic in batch mode
+    u32 batch;     // nodes per cursor atomic in batch mode
+    u32 cp_l1;     // early-rejection checkpoint (key groups of 4) for full lower-level-1 nodes, 0 = off
+    u32 cp_l2;     // same for full lower-level-2 nodes
 };
 
 // ------------------------------------------------------------------ trials --
@@ -134,14 +137,16 @@ __device__ __forceinline__ u32 inc_of(u32 h, u32 r, u32 tbase) {
 
 // Lower split: packed counter.  CL = 0/1: full node of lower level 1/2,
 // part = remap(h, f) looked up in the block-wide static table; CL = 2: node with a smaller
-// last part, warp table over v = remap(h, s) (r = s).
-template <int MODE, int CL>
-__device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, u32 r) {
-    u32 c0 = 0, c1 = 0;
-    const u32 ng = s >> 2;
-    const u32* __restrict__ g = K.G;
+// last part, warp table over v = remap(h, s) (r = s).  Keys of groups [g0, g1), plus the
+// s % 4 tail keys when TAIL.
+template <int MODE, int CL, bool TAIL = true>
+__device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, u32 r, u32 g0 = 0,
+                                           u32 g1 = 0xffffffffu, u32 init = 0) {
+    u32 c0 = init, c1 = 0;
+    const u32 ng = min(s >> 2, g1);
+    const u32* __restrict__ g = K.G + 12 * g0;
 #pragma unroll 1
-    for (u32 q = 0; q < ng; ++q, g += 12) {
+    for (u32 q = g0; q < ng; ++q, g += 12) {
         u32 h[4];
         hash4<MODE>(g, sigma, h);
         if (CL < 2) {
@@ -152,10 +157,11 @@ __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, 
             c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
         }
     }
-    for (u32 j = ng << 2; j < s; ++j) {
-        const u32 h = hash1<MODE, 12>(K, j, sigma);
-        c0 += CL < 2 ? inc_full<(CL < 2 ? CL : 0)>(h, r) : inc_of(h, r, K.tbase);
-    }
+    if (TAIL)
+        for (u32 j = (s >> 2) << 2; j < s; ++j) {
+            const u32 h = hash1<MODE, 12>(K, j, sigma);
+            c0 += CL < 2 ? inc_full<(CL < 2 ? CL : 0)>(h, r) : inc_of(h, r, K.tbase);
+        }
     return c0 + c1;
 }
 
@@ -226,6 +232,7 @@ struct NodeCtx {
     u32 f, w, unit, full, mu, r, wide, target, mask, margin;
     u32 l2;  // lower level 2 node (s > u1)
     u64 target64, mask64;
+    u32 cp;  // early rejection (full lower nodes): checkpoint in key groups, 0 = off
 };
 
 
@@ -334,6 +341,8 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
             c.wide = (f - 1) * w > 32;
             c.r = c.full ? f : s;
             c.l2 = s > A.u1;
+            const u32 cpg = c.l2 ? A.cp_l2 : A.cp_l1;
+            c.cp = c.full && cpg < (s >> 2) && (f - 1) * w <= 31 ? cpg : 0;
             if (!c.wide) {
                 u32 t = 0;
                 for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
@@ -360,14 +369,93 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
 
 // Search the window [wstart, wstart + 32*iters) of base values (seeds, or base seeds k for
 // RF) in order; on a hit returns true with the stored value in *val (warp-uniform).
-template <int KIND>
+// Early rejection with warp compaction (full lower-level nodes, no-carry path).  Stage 1
+// counts the first c.cp key groups of 32 seeds; a seed whose packed counter already shows
+// a part above its target cannot succeed (a carry only happens when some count exceeds
+// 2^w - 1 > unit, so the test never rejects a valid seed).  Survivors go to a per-warp FIFO
+// queue in increasing seed order; whenever 32 are queued (and at the end of the window)
+// stage 2 finishes their counts over the remaining keys.  Survivors are completed in
+// increasing seed order and every other seed of the window was rejected, so the first
+// hit is the smallest successful seed of the window.
+template <int CL>
+__device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart, u32 lane,
+                                           u32* qs, u32* qc, u64* val) {
+    // packed "some field > unit" test: ((cnt & me) + ke) & ce | ((cnt & mo) + ko) & co, fields
+    // 0..f-2 split into even and odd ones so that the added carries stay inside a field gap
+    u32 me = 0, mo = 0, ke = 0, ko = 0, ce = 0, co = 0;
+    {
+        const u32 fm = (1u << c.w) - 1, kadd = fm - c.unit;  // field + kadd >= 2^w <=> field > unit
+        for (u32 j = 0; j + 1 < c.f; ++j) {
+            const u32 sh = j * c.w;
+            if (j & 1) {
+                mo |= fm << sh;
+                ko |= kadd << sh;
+                co |= 1u << (sh + c.w);
+            } else {
+                me |= fm << sh;
+                ke |= kadd << sh;
+                ce |= 1u << (sh + c.w);
+            }
+        }
+    }
+    const u32 lt = lanemask_lt();
+    u32 qn = 0;
+    for (u32 it = 0; it <= A.iters; ++it) {
+        if (it < A.iters) {
+            const u32 sig = (u32)(wstart + (u64)it * 32 + lane);
+            const u32 cnt = count_lower<0, CL, false>(K, c.s, sig, c.r, 0, c.cp);
+            const bool rej = ((((cnt & me) + ke) & ce) | (((cnt & mo) + ko) & co)) != 0;
+            const u32 bal = __ballot_sync(FULL, !rej);
+            if (!rej) {
+                const u32 pos = qn + __popc(bal & lt);
+                qs[pos] = sig;
+                qc[pos] = cnt;
+            }
+            qn += __popc(bal);
+            __syncwarp();
+            if (qn < 32) continue;
+        } else if (qn == 0) {
+            break;
+        }
+        // stage 2 on queue entries [0, min(qn, 32))
+        const bool have = lane < qn;
+        const u32 sig = have ? qs[lane] : 0;
+        u32 cnt = have ? qc[lane] : 0;
+        cnt = count_lower<0, CL, true>(K, c.s, sig, c.r, c.cp, 0xffffffffu, cnt);
+        const u32 bal = __ballot_sync(FULL, have && (cnt & c.mask) == c.target);
+        if (bal) {
+            *val = __shfl_sync(FULL, sig, __ffs(bal) - 1);
+            return true;
+        }
+        __syncwarp();
+        const u32 rest = qn > 32 ? qn - 32 : 0;
+        u32 a = 0, b = 0;
+        if (lane < rest) {
+            a = qs[32 + lane];
+            b = qc[32 + lane];
+        }
+        __syncwarp();
+        if (lane < rest) {
+            qs[lane] = a;
+            qc[lane] = b;
+        }
+        __syncwarp();
+        qn = rest;
+    }
+    return false;
+}
+
+template <int KIND, bool CP>
 __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
-                                           u32 lane, u64* val) {
+                                           u32 lane, u64* val, u32* qs, u32* qc) {
     const u64 ws = 32ull * A.iters;
     // largest value (seed, or base seed k*m) any lane tries in this window
     const u64 last = KIND == SK_LEAF_RF ? (wstart + ws - 1) * c.s : wstart + ws - 1;
     const bool fast = last < (1ull << 32) && !(KIND == SK_LOWER && c.wide);
     const bool nocarry = fast && last <= c.margin;
+    if (CP && KIND == SK_LOWER && nocarry && c.cp)
+        return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, qc, val)
+                    : run_window_cp<0>(A, K, c, wstart, lane, qs, qc, val);
     for (u32 it = 0; it < A.iters; ++it) {
         const u64 idx = wstart + (u64)it * 32 + lane;
         int r = 0;
@@ -413,7 +501,7 @@ __device__ u32 find_help(const Args& A, u32 gw, u32 lane, u32 nn) {
 #ifndef RS_MIN_BLOCKS
 #define RS_MIN_BLOCKS 1
 #endif
-template <int KIND>
+template <int KIND, bool CP = false>
 __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 : RS_MIN_BLOCKS) k_search(const Args A) {
     constexpr u32 GW = Layout<KIND>::GW;
     extern __shared__ __align__(16) u32 smem32[];
@@ -422,8 +510,10 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     const u32 cap = A.warp_cap;                    // keys (multiple of 4)
     const u32 gwords = GW * (cap / 4 + 1);         // key groups
     const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
-    u32* G = smem32 + (size_t)wib * (gwords + twords);
+    u32* G = smem32 + (size_t)wib * (gwords + twords + 128);
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
+    u32* QS = G + gwords + twords;  // early-rejection queue: seeds, partial counters (64 each)
+    u32* QC = QS + 64;
     const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
     if (KIND == SK_LOWER) {  // shift tables of full nodes: part p -> p*w (p < f-1), 32 for the last
         for (u32 t = threadIdx.x; t < 64; t += blockDim.x) {
@@ -456,7 +546,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                         val = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
                         break;
                     }
-                    if (run_window<KIND>(A, K, c, wstart, lane, &val)) break;
+                    if (run_window<KIND, CP>(A, K, c, wstart, lane, &val, QS, QC)) break;
                 }
                 if (lane == 0) A.values[c.slot] = val;
                 __syncwarp();
@@ -503,15 +593,15 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             continue;
         }
         u64 val;
-        if (run_window<KIND>(A, K, c, wstart, lane, &val) && lane == 0)
+        if (run_window<KIND, CP>(A, K, c, wstart, lane, &val, QS, QC) && lane == 0)
             atomicMin((unsigned long long*)(A.values + c.slot), (unsigned long long)val);
     }
 }
 
-template <int KIND>
+template <int KIND, bool CP = false>
 void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 grid, cudaStream_t st) {
-    cudaFuncSetAttribute(k_search<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    k_search<KIND><<<grid, wpb * 32, smem, st>>>(A);
+    cudaFuncSetAttribute(k_search<KIND, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    k_search<KIND, CP><<<grid, wpb * 32, smem, st>>>(A);
 }
 
 }  // namespace
@@ -536,12 +626,19 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.u2 = P.u2;
     A.iters = P.iters ? P.iters : 1;
     A.help = P.help;
+    // early-rejection checkpoints (per mille of the node size; RS_CP1 / RS_CP2 override, 0 = off)
+    {
+        static const int cp1 = getenv("RS_CP1") ? atoi(getenv("RS_CP1")) : 850;
+        static const int cp2 = getenv("RS_CP2") ? atoi(getenv("RS_CP2")) : 940;
+        A.cp_l1 = (u32)((u64)P.u1 * cp1 / 4000);
+        A.cp_l2 = (u32)((u64)P.u2 * cp2 / 4000);
+    }
     // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
     const u32 GW = (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) ? 20 : 12;
-    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4) * sizeof(u32);
+    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + 128) * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;
@@ -568,7 +665,12 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.n_warps = grid * wpb;
     switch (P.kind) {
         case SK_UPPER: launch_kind<SK_UPPER>(P, A, wpb, smem, grid, st); break;
-        case SK_LOWER: launch_kind<SK_LOWER>(P, A, wpb, smem, grid, st); break;
+        case SK_LOWER:
+            if (A.cp_l1 | A.cp_l2)
+                launch_kind<SK_LOWER, true>(P, A, wpb, smem, grid, st);
+            else
+                launch_kind<SK_LOWER>(P, A, wpb, smem, grid, st);
+            break;
         case SK_LEAF_RF: launch_kind<SK_LEAF_RF>(P, A, wpb, smem, grid, st); break;
         case SK_LEAF_BF: launch_kind<SK_LEAF_BF>(P, A, wpb, smem, grid, st); break;
     }
