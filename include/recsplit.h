@@ -161,6 +161,33 @@ RECSPLIT_API int recsplit_query_many(const uint8_t *mphf, size_t size, const uin
 RECSPLIT_API int recsplit_query_device(const uint8_t *mphf, size_t size, const uint64_t *d_keys,
                                        size_t n, uint64_t *d_out, void *stream);
 
+/* Opened MPHF (SURVEY 8(b) recsplit_open): the blob is copied and parsed once (its
+ * Elias-Fano index decoded), so repeated queries skip the per-call parse.  device >= 0
+ * also places a resident copy in that GPU's HBM (decoded index + data words + per-size
+ * tables, about 16 B per bucket + the blob's data) for recsplit_handle_query_device;
+ * device < 0 makes a host-only handle (no GPU needed).  Errors: RECSPLIT_E_FORMAT for a
+ * corrupt blob (or a device handle of a string-key MPHF), RECSPLIT_E_CUDA / _NOMEM for
+ * device failures; *h is NULL on any error.  Close with recsplit_close (NULL-safe). */
+typedef struct recsplit_handle recsplit_handle;
+RECSPLIT_API int recsplit_open(const uint8_t *mphf, size_t size, int32_t device, recsplit_handle **h);
+/* Host evaluation on n u64 keys (multi-threaded for large n); reentrant. */
+RECSPLIT_API int recsplit_handle_query_many(const recsplit_handle *h, const uint64_t *keys, size_t n,
+                                            uint64_t *out);
+/* GPU evaluation on n keys with the resident copy: d_keys / d_out are DEVICE arrays of n
+ * u64 on the handle's device (which must be current).  ENQUEUED on `stream` only -- the
+ * call does not synchronise; d_out is valid once the stream reaches this point. */
+RECSPLIT_API int recsplit_handle_query_device(const recsplit_handle *h, const uint64_t *d_keys, size_t n,
+                                              uint64_t *d_out, void *stream);
+RECSPLIT_API void recsplit_close(recsplit_handle *h);
+
+/* Bijectivity check on the GPU (the property P:11 defines): d_values is a
+ * DEVICE array of n u64 on the current device (e.g. the query results of the n build
+ * keys); *bad receives the number of entries outside [0, n) plus the number of repeats,
+ * so *bad == 0 iff d_values is a permutation of [0, n).  Uses an n-bit device bitmap;
+ * ordered on `stream`, returns after completion. */
+RECSPLIT_API int recsplit_check_bijective_device(const uint64_t *d_values, size_t n, uint64_t *bad,
+                                                 void *stream);
+
 /* bits/object of a serialized MPHF: (Golomb-Rice bits + Elias-Fano bits) / n,
  * excluding the fixed header and word padding (reading R14). */
 RECSPLIT_API int recsplit_bits_per_key(const uint8_t *mphf, size_t size, double *out);

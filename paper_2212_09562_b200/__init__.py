@@ -25,6 +25,8 @@ SYMBOLS = [
     "recsplit_free", "recsplit_free_ptr", "recsplit_last_error", "recsplit_shard_begin",
     "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch", "recsplit_shard_free",
     "recsplit_shard_globals", "recsplit_query_device", "recsplit_build_strings", "recsplit_query_strings",
+    "recsplit_open", "recsplit_handle_query_many", "recsplit_handle_query_device", "recsplit_close",
+    "recsplit_check_bijective_device",
 ]
 
 
@@ -107,6 +109,16 @@ def lib():
         L.recsplit_shard_free.argtypes = [C.c_void_p]
         L.recsplit_shard_free.restype = None
         L.recsplit_shard_globals.argtypes = [P64, C.c_int32, C.c_int32, P64]
+        L.recsplit_open.argtypes = [P8, sz, C.c_int32, C.POINTER(C.c_void_p)]
+        L.recsplit_open.restype = i32
+        L.recsplit_handle_query_many.argtypes = [C.c_void_p, P64, sz, P64]
+        L.recsplit_handle_query_many.restype = i32
+        L.recsplit_handle_query_device.argtypes = [C.c_void_p, C.c_void_p, sz, C.c_void_p, C.c_void_p]
+        L.recsplit_handle_query_device.restype = i32
+        L.recsplit_check_bijective_device.argtypes = [C.c_void_p, sz, P64, C.c_void_p]
+        L.recsplit_check_bijective_device.restype = i32
+        L.recsplit_close.argtypes = [C.c_void_p]
+        L.recsplit_close.restype = None
         for name in ("recsplit_shard_begin", "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch",
                      "recsplit_shard_globals"):
             getattr(L, name).restype = i32
@@ -242,6 +254,65 @@ def query_device(blob: bytes, keys_tensor, stream=None):
                                        C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(),
                                        C.c_void_p(out.data_ptr()), C.c_void_p(stream.cuda_stream)))
     return out
+
+
+def check_bijective_device(values_tensor, stream=None) -> int:
+    """Number of entries of a CUDA tensor outside [0, n) or repeated (0 <=> permutation)."""
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream(values_tensor.device)
+    bad = np.zeros(1, dtype=np.uint64)
+    _check(lib().recsplit_check_bijective_device(C.c_void_p(values_tensor.data_ptr()), values_tensor.numel(),
+                                                 _p64(bad), C.c_void_p(stream.cuda_stream)))
+    return int(bad[0])
+
+
+class Handle:
+    """An opened MPHF (recsplit_open): parsed once; with device >= 0 also resident in that
+    GPU's HBM for query_device.  Use as a context manager or call close()."""
+
+    def __init__(self, blob: bytes, device: int = -1):
+        self._h = C.c_void_p()
+        buf = np.frombuffer(blob, dtype=np.uint8)
+        _check(lib().recsplit_open(buf.ctypes.data_as(C.POINTER(C.c_uint8)), len(blob), device, C.byref(self._h)))
+        self.device = device
+
+    def query_many(self, keys) -> np.ndarray:
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        out = np.zeros(len(keys), dtype=np.uint64)
+        _check(lib().recsplit_handle_query_many(self._h, _p64(keys), len(keys), _p64(out)))
+        return out
+
+    def query_device(self, keys_tensor, out=None, stream=None):
+        """Enqueue the GPU query of a CUDA tensor of keys on `stream` (default: the current
+        stream); returns the int64 output tensor without synchronising."""
+        import torch
+
+        if stream is None:
+            stream = torch.cuda.current_stream(keys_tensor.device)
+        if out is None:
+            out = torch.empty_like(keys_tensor)
+        _check(lib().recsplit_handle_query_device(self._h, C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(),
+                                                  C.c_void_p(out.data_ptr()), C.c_void_p(stream.cuda_stream)))
+        return out
+
+    def close(self):
+        if self._h:
+            lib().recsplit_close(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def bits_per_key(blob: bytes) -> float:

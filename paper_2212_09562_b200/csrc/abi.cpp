@@ -243,7 +243,42 @@ int query_mhc(const Parsed& M, uint64_t hi, uint64_t lo, uint64_t* out) {
     }
 }
 
+int query_many_parsed(const Parsed& M, const uint64_t* keys, size_t n, uint64_t* out) {
+    unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 64));
+    if (n < 100000) nt = 1;
+    std::vector<int> rcs(nt, 0);
+    std::vector<std::string> errs(nt);
+    auto work = [&](unsigned t) {
+        const size_t a = n * t / nt, b = n * (t + 1) / nt;
+        for (size_t i = a; i < b; ++i) {
+            int r = query_one(M, keys[i], out + i);
+            if (r) {
+                rcs[t] = r;
+                errs[t] = g_err;
+                return;
+            }
+        }
+    };
+    if (nt == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; ++t) th.emplace_back(work, t);
+        for (auto& x : th) x.join();
+    }
+    for (unsigned t = 0; t < nt; ++t)
+        if (rcs[t]) return fail(rcs[t], errs[t]);
+    return RECSPLIT_OK;
+}
+
 }  // namespace
+
+struct recsplit_handle {
+    std::vector<uint8_t> blob;  // owned copy; M points into it
+    rs::Parsed M;
+    rs::DeviceMphf* dev = nullptr;
+    int device = -1;
+};
 
 extern "C" {
 
@@ -317,32 +352,73 @@ int recsplit_query_many(const uint8_t* mphf, size_t size, const uint64_t* keys, 
         int rc = parse(mphf, size, M);
         if (rc) return rc;
         if (M.strings) return fail(RECSPLIT_E_FORMAT, "MPHF was built from string keys");
-        unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 64));
-        if (n < 100000) nt = 1;
-        std::vector<int> rcs(nt, 0);
-        std::vector<std::string> errs(nt);
-        auto work = [&](unsigned t) {
-            const size_t a = n * t / nt, b = n * (t + 1) / nt;
-            for (size_t i = a; i < b; ++i) {
-                int r = query_one(M, keys[i], out + i);
-                if (r) {
-                    rcs[t] = r;
-                    errs[t] = g_err;
-                    return;
-                }
-            }
-        };
-        if (nt == 1) {
-            work(0);
-        } else {
-            std::vector<std::thread> th;
-            for (unsigned t = 0; t < nt; ++t) th.emplace_back(work, t);
-            for (auto& x : th) x.join();
+        return query_many_parsed(M, keys, n, out);
+    });
+}
+
+// ------------------------------------------------------------------ handles --
+
+int recsplit_open(const uint8_t* mphf, size_t size, int32_t device, recsplit_handle** h) {
+    if (!h) return fail(RECSPLIT_E_INVALID, "h is NULL");
+    *h = nullptr;
+    if (!mphf && size) return fail(RECSPLIT_E_INVALID, "mphf is NULL");
+    return guarded([&]() -> int {
+        std::unique_ptr<recsplit_handle, void (*)(recsplit_handle*)> x(new recsplit_handle(), recsplit_close);
+        x->blob.assign(mphf, mphf + size);
+        int rc = parse(x->blob.data(), x->blob.size(), x->M);
+        if (rc) return rc;
+        if (device >= 0) {
+            if (x->M.strings) return fail(RECSPLIT_E_FORMAT, "device handles of string-key MPHFs are not supported");
+            select_device(device);
+            cudaStream_t st;
+            if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+                throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
+            struct StreamGuard {
+                cudaStream_t s;
+                ~StreamGuard() { cudaStreamDestroy(s); }
+            } sg{st};
+            x->dev = rs::upload_mphf(x->M, st);
+            x->device = device;
         }
-        for (unsigned t = 0; t < nt; ++t)
-            if (rcs[t]) return fail(rcs[t], errs[t]);
+        *h = x.release();
         return RECSPLIT_OK;
     });
+}
+
+int recsplit_handle_query_many(const recsplit_handle* h, const uint64_t* keys, size_t n, uint64_t* out) {
+    if (!h) return fail(RECSPLIT_E_INVALID, "h is NULL");
+    if ((!keys || !out) && n) return fail(RECSPLIT_E_INVALID, "NULL keys/out");
+    if (h->M.strings) return fail(RECSPLIT_E_FORMAT, "MPHF was built from string keys");
+    return guarded([&]() -> int { return query_many_parsed(h->M, keys, n, out); });
+}
+
+int recsplit_handle_query_device(const recsplit_handle* h, const uint64_t* d_keys, size_t n, uint64_t* d_out,
+                                 void* stream) {
+    if (!h) return fail(RECSPLIT_E_INVALID, "h is NULL");
+    if (!h->dev) return fail(RECSPLIT_E_INVALID, "handle has no device copy (opened with device < 0)");
+    if ((!d_keys || !d_out) && n) return fail(RECSPLIT_E_INVALID, "NULL keys/out");
+    return guarded([&]() -> int {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != h->device) return fail(RECSPLIT_E_INVALID, "current device differs from the handle's device");
+        rs::query_resident(*h->dev, d_keys, n, d_out, (cudaStream_t)stream);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_check_bijective_device(const uint64_t* d_values, size_t n, uint64_t* bad, void* stream) {
+    if (!bad || (!d_values && n)) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    return guarded([&]() -> int {
+        select_device(-1);
+        *bad = rs::count_non_bijective(d_values, n, (cudaStream_t)stream);
+        return RECSPLIT_OK;
+    });
+}
+
+void recsplit_close(recsplit_handle* h) {
+    if (!h) return;
+    rs::free_mphf(h->dev);
+    delete h;
 }
 
 int recsplit_query_device(const uint8_t* mphf, size_t size, const uint64_t* d_keys, size_t n, uint64_t* d_out,

@@ -82,6 +82,14 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
 // Batched query on the device; d_keys / d_out device arrays of n.
 struct Parsed;
 void query_on_device(const Parsed& M, const uint64_t* d_keys, uint64_t n, uint64_t* d_out, cudaStream_t st);
+// resident copy on the current device (recsplit_open): upload once, query many times
+struct DeviceMphf;
+DeviceMphf* upload_mphf(const Parsed& M, cudaStream_t st);
+void free_mphf(DeviceMphf* h);  // NULL-safe
+// number of values outside [0, n) or repeated (0 <=> d_vals is a permutation of [0, n))
+uint64_t count_non_bijective(const uint64_t* d_vals, uint64_t n, cudaStream_t st);
+// enqueue only (no synchronisation)
+void query_resident(const DeviceMphf& h, const uint64_t* d_keys, uint64_t n, uint64_t* d_out, cudaStream_t st);
 
 // Kernel-level entry points for parity tests (host arrays).
 void search_leaves_host(const uint64_t* lo, const uint8_t* isb, const uint32_t* off, uint32_t n_nodes, bool rf,

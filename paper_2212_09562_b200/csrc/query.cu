@@ -102,10 +102,27 @@ __global__ void k_query(QueryArgs q, const u64* __restrict__ keys, u64 n, u64* _
         out[t] = query_key(q, keys[t]);
 }
 
+// Bijectivity check: mark every value in a bitmap of n bits; a value
+// outside [0, n) or one whose bit was already set is a violation.
+__global__ void k_mark(const u64* __restrict__ v, u64 n, u32* __restrict__ bitmap, unsigned long long* bad) {
+    u32 local = 0;
+    for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (u64)gridDim.x * blockDim.x) {
+        const u64 x = v[t];
+        if (x >= n) {
+            ++local;
+            continue;
+        }
+        const u32 bit = 1u << (x & 31);
+        if (atomicOr(bitmap + (x >> 5), bit) & bit) ++local;
+    }
+    for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, (unsigned long long)local);
+}
+
 template <typename T>
 T* upload(const std::vector<T>& v, cudaStream_t st, std::vector<void*>& owned) {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, std::max<size_t>(v.size() * sizeof(T), 16), st) != cudaSuccess)
+    if (cudaMalloc(&p, std::max<size_t>(v.size() * sizeof(T), 16)) != cudaSuccess)
         throw Error(RECSPLIT_E_NOMEM, "device allocation failed");
     owned.push_back(p);
     if (!v.empty() && cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -115,41 +132,91 @@ T* upload(const std::vector<T>& v, cudaStream_t st, std::vector<void*>& owned) {
 
 }  // namespace
 
-void query_on_device(const Parsed& M, const uint64_t* d_keys, uint64_t n, uint64_t* d_out, cudaStream_t st) {
-    std::vector<void*> owned;
-    struct Free {
-        std::vector<void*>& o;
-        cudaStream_t s;
-        ~Free() {
-            for (void* p : o) cudaFreeAsync(p, s);
-        }
-    } fr{owned, st};
-    const Tables& T = *M.T;
-    const uint32_t smax = (uint32_t)M.smax;
-    std::vector<uint32_t> tau(T.tau.begin(), T.tau.begin() + smax + 1);
-    std::vector<uint64_t> F(T.F.begin(), T.F.begin() + smax + 1);
-    std::vector<uint32_t> N(T.N.begin(), T.N.begin() + smax + 1);
-    std::vector<uint64_t> data((M.D + 63) / 64 + 2, 0);
-    if (M.D) memcpy(data.data(), M.data, 8 * ((M.D + 63) / 64));
+// Resident device copy of a parsed MPHF: decoded index C/P, Golomb-Rice data words and the
+// per-size tau/F/N tables (the layout k_query reads).  Plain cudaMalloc so that the copy
+// outlives any stream.
+struct DeviceMphf {
     QueryArgs q;
-    q.C = upload(M.C, st, owned);
-    q.P = upload(M.P, st, owned);
-    q.data = upload(data, st, owned);
-    q.tau = upload(tau, st, owned);
-    q.F = upload(F, st, owned);
-    q.N = upload(N, st, owned);
-    q.B = M.B;
-    q.D = M.D;
-    q.g = M.g;
-    q.leaf = M.leaf;
-    q.u1 = T.sh.u1;
-    q.u2 = T.sh.u2;
-    q.rf = M.rf ? 1 : 0;
-    if (n) {
-        unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-        k_query<<<grid, 256, 0, st>>>(q, d_keys, n, d_out);
-        if (cudaGetLastError() != cudaSuccess) throw Error(RECSPLIT_E_CUDA, "query launch failed");
+    std::vector<void*> owned;
+    int device;
+};
+
+DeviceMphf* upload_mphf(const Parsed& M, cudaStream_t st) {
+    std::unique_ptr<DeviceMphf> h(new DeviceMphf());
+    try {
+        cudaGetDevice(&h->device);
+        const Tables& T = *M.T;
+        const uint32_t smax = (uint32_t)M.smax;
+        std::vector<uint32_t> tau(T.tau.begin(), T.tau.begin() + smax + 1);
+        std::vector<uint64_t> F(T.F.begin(), T.F.begin() + smax + 1);
+        std::vector<uint32_t> N(T.N.begin(), T.N.begin() + smax + 1);
+        std::vector<uint64_t> data((M.D + 63) / 64 + 2, 0);
+        if (M.D) memcpy(data.data(), M.data, 8 * ((M.D + 63) / 64));
+        QueryArgs& q = h->q;
+        q.C = upload(M.C, st, h->owned);
+        q.P = upload(M.P, st, h->owned);
+        q.data = upload(data, st, h->owned);
+        q.tau = upload(tau, st, h->owned);
+        q.F = upload(F, st, h->owned);
+        q.N = upload(N, st, h->owned);
+        q.B = M.B;
+        q.D = M.D;
+        q.g = M.g;
+        q.leaf = M.leaf;
+        q.u1 = T.sh.u1;
+        q.u2 = T.sh.u2;
+        q.rf = M.rf ? 1 : 0;
+        // the host vectors die here: finish the copies first
+        if (cudaStreamSynchronize(st) != cudaSuccess) throw Error(RECSPLIT_E_CUDA, "upload failed");
+    } catch (...) {
+        free_mphf(h.release());
+        throw;
     }
+    return h.release();
+}
+
+void free_mphf(DeviceMphf* h) {
+    if (!h) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(h->device);
+    for (void* p : h->owned) cudaFree(p);
+    cudaSetDevice(cur);
+    delete h;
+}
+
+void query_resident(const DeviceMphf& h, const uint64_t* d_keys, uint64_t n, uint64_t* d_out, cudaStream_t st) {
+    if (!n) return;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k_query<<<grid, 256, 0, st>>>(h.q, d_keys, n, d_out);
+    if (cudaGetLastError() != cudaSuccess) throw Error(RECSPLIT_E_CUDA, "query launch failed");
+}
+
+uint64_t count_non_bijective(const uint64_t* d_vals, uint64_t n, cudaStream_t st) {
+    if (!n) return 0;
+    const size_t words = (n + 31) / 32;
+    void* buf = nullptr;
+    if (cudaMallocAsync(&buf, words * 4 + 8, st) != cudaSuccess) throw Error(RECSPLIT_E_NOMEM, "bitmap allocation failed");
+    struct Free {
+        void* p;
+        cudaStream_t s;
+        ~Free() { cudaFreeAsync(p, s); }
+    } fr{buf, st};
+    unsigned long long* bad = (unsigned long long*)buf;  // 8 B counter, then the bitmap
+    u32* bitmap = (u32*)((char*)buf + 8);
+    cudaMemsetAsync(buf, 0, words * 4 + 8, st);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k_mark<<<grid, 256, 0, st>>>(d_vals, n, bitmap, bad);
+    if (cudaGetLastError() != cudaSuccess) throw Error(RECSPLIT_E_CUDA, "bijectivity check launch failed");
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, bad, 8, cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) throw Error(RECSPLIT_E_CUDA, "bijectivity check failed");
+    return h;
+}
+
+void query_on_device(const Parsed& M, const uint64_t* d_keys, uint64_t n, uint64_t* d_out, cudaStream_t st) {
+    std::unique_ptr<DeviceMphf, void (*)(DeviceMphf*)> h(upload_mphf(M, st), free_mphf);
+    query_resident(*h, d_keys, n, d_out, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) throw Error(RECSPLIT_E_CUDA, "query failed");
 }
 

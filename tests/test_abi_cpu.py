@@ -102,3 +102,18 @@ def test_library_string_query_reads_oracle_format():
     with pytest.raises(rs.RecSplitError) as e:
         rs.query_many(blob, np.array([1], dtype=np.uint64))
     assert e.value.code == rs.E_FORMAT
+
+
+def test_host_handle_matches_blob_query():
+    """recsplit_open with device < 0 (no GPU needed): the handle's query equals the
+    per-call query and the oracle's; bad blobs fail at open; close is NULL-safe."""
+    keys = synth.keys(20000, 5)
+    blob = oracle.build(keys, 12, 1000, threads=4)
+    with rs.Handle(blob) as h:
+        assert np.array_equal(h.query_many(keys), oracle.query_many(blob, keys))
+        # host-only handle: the device query is refused, not emulated
+        assert rs.lib().recsplit_handle_query_device(h._h, None, 0, None, None) == rs.E_INVALID
+    with pytest.raises(rs.RecSplitError) as e:
+        rs.Handle(blob[:-8])
+    assert e.value.code == rs.E_FORMAT
+    rs.lib().recsplit_close(None)

@@ -302,6 +302,33 @@ def test_query_device_matches_host_and_oracle(leaf, b, rf, n):
     assert (rs.query_device(blob, other).cpu().numpy().view(np.uint64) < n).all()
 
 
+def test_device_handle_and_bijectivity_check():
+    """recsplit_open(device 0): the resident copy answers like the per-call query on two
+    streams; recsplit_check_bijective_device finds 0 violations on S's results and counts
+    every injected repeat / out-of-range value."""
+    import torch
+    n = 200_000
+    keys = synth.keys(n, 4242)
+    blob = rs.build(keys, 12, 1000)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    want = rs.query_device(blob, kt)
+    with rs.Handle(blob, device=0) as h:
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        torch.cuda.synchronize()
+        a = h.query_device(kt, stream=s1)
+        b = h.query_device(kt[: n // 2], stream=s2)
+        torch.cuda.synchronize()
+        assert torch.equal(a, want) and torch.equal(b, want[: n // 2])
+        assert np.array_equal(h.query_many(keys[:1000]), want[:1000].cpu().numpy().view(np.uint64))
+    assert rs.check_bijective_device(want) == 0
+    bad = want.clone()
+    bad[5] = bad[6]        # one repeat
+    bad[7] = n             # out of range
+    bad[8] = -1            # 2^64 - 1: out of range
+    assert rs.check_bijective_device(bad) == 3
+    assert rs.check_bijective_device(torch.zeros(0, dtype=torch.int64, device="cuda")) == 0
+
+
 # --------------------------------------------------------------- string keys --
 
 @pytest.mark.parametrize("leaf,b,n", [(8, 100, 20_000), (16, 2000, 8_000), (5, 5, 10_000), (12, 1000, 30_000)])
