@@ -63,18 +63,20 @@ __device__ __forceinline__ u32 remix_hi(u64 x) {
     "xor.b32 %0, a, th;\n\t"                   \
     "}"
 
+// CARRY: x = (kh:kl) + (H:sigma) with the carry out of the low word (H = high word of the
+// 64-bit value, 0 below 2^32); otherwise x = (kh : kl + sigma).
 template <bool CARRY>
-__device__ __forceinline__ u32 remix_hi_fast(u32 kl, u32 kh, u32 sigma) {
+__device__ __forceinline__ u32 remix_hi_fast(u32 kl, u32 kh, u32 sigma, u32 H = 0) {
     u32 h;
     if (CARRY) {
         asm("{\n\t"
             ".reg .u32 tl, th, wl, wh, yl, yh, zl, zh, a;\n\t"
             ".reg .u64 p64;\n\t"
             "add.cc.u32 wl, %1, %3;\n\t"
-            "addc.u32 wh, %2, 0;\n\t"
+            "addc.u32 wh, %2, %4;\n\t"
             REMIX_HI_TAIL
             : "=r"(h)
-            : "r"(kl), "r"(kh), "r"(sigma));
+            : "r"(kl), "r"(kh), "r"(sigma), "r"(H));
     } else {
         asm("{\n\t"
             ".reg .u32 tl, th, wl, wh, yl, yh, zl, zh, a;\n\t"

@@ -808,12 +808,12 @@ static void search_nodes_host(const uint64_t* lo, const uint8_t* isb, const uint
     else
         CK(cudaMemset(d_ab, 0, nk));
     const Shape sh = make_shape(leaf ? leaf : 2);
-    // group nodes by kind so each launch is homogeneous
+    // group nodes by kind and level so each launch is homogeneous (as the pipeline's phases)
     std::vector<std::vector<rsd::NodeRec>> groups(4);
     std::vector<uint32_t> maxs(4, 0);
     for (uint32_t j = 0; j < n_nodes; ++j) {
         const uint32_t s = off[j + 1] - off[j];
-        int g = mode ? 3 : (s > sh.u2 ? 0 : 1);
+        int g = mode ? 3 : (s > sh.u2 ? 0 : s > sh.u1 ? 1 : 2);
         groups[g].push_back({off[j], s, j, 0});
         maxs[g] = std::max(maxs[g], s);
     }
@@ -836,6 +836,7 @@ static void search_nodes_host(const uint64_t* lo, const uint8_t* isb, const uint
         CK(cudaMemset(active, 0xff, nslots * 4));
         PhaseLaunch P{};
         P.kind = mode == 1 ? SK_LEAF_RF : mode == 2 ? SK_LEAF_BF : (g == 0 ? SK_UPPER : SK_LOWER);
+        // (groups 1 / 2 = lower level 2 / 1: launch_search picks the kernel variant by level)
         P.nodes = d_nodes;
         P.n_nodes = small + 6;
         P.n_nodes_host = cnt;

@@ -67,8 +67,10 @@ struct Args {
 //
 // Fast path (every value of the window < 2^32): when additionally k_lo + value < 2^32
 // for all keys of the node (checked once per window against the node's carry margin)
-// the no-carry evaluation remix_hi_nc is used; otherwise remix_hi_fast<true>.  Values
-// >= 2^32 (never at the measured configurations) take the generic 64-bit path.
+// the no-carry evaluation remix_hi_nc is used; otherwise remix_hi_fast<true>, which also
+// takes windows of values >= 2^32 whose values share one high word H (leaves at l >= 20
+// have stored values around 2^31..2^33).  A window straddling a multiple of 2^32 takes the
+// generic 64-bit path.
 
 template <int KIND>
 struct Layout {
@@ -78,6 +80,7 @@ struct Layout {
 struct KeysView {
     const u32* __restrict__ G;  // groups
     u32 tbase;                  // shared-space byte address of the shift table
+    u32 H;                      // carry path: high word of every value of the window
 };
 
 template <u32 GW>
@@ -92,8 +95,8 @@ __device__ __forceinline__ u32 hash_slow(const KeysView& K, u32 j, u64 sigma) {
 }
 
 // evaluate the four keys of group g
-template <int MODE>  // 0: no-carry, 1: carry
-__device__ __forceinline__ void hash4(const u32* __restrict__ g, u32 sigma, u32 h[4]) {
+template <int MODE>  // 0: no-carry, 1: carry (value = H * 2^32 + sigma)
+__device__ __forceinline__ void hash4(const u32* __restrict__ g, u32 sigma, u32 h[4], u32 H) {
     const uint4 kl = *reinterpret_cast<const uint4*>(g);
     const uint4 kh = *reinterpret_cast<const uint4*>(g + 4);
     if (MODE == 0) {
@@ -103,18 +106,22 @@ __device__ __forceinline__ void hash4(const u32* __restrict__ g, u32 sigma, u32 
         h[2] = remix_hi_nc(kl.z, kh.z, kc.z, sigma);
         h[3] = remix_hi_nc(kl.w, kh.w, kc.w, sigma);
     } else {
-        h[0] = remix_hi_fast<true>(kl.x, kh.x, sigma);
-        h[1] = remix_hi_fast<true>(kl.y, kh.y, sigma);
-        h[2] = remix_hi_fast<true>(kl.z, kh.z, sigma);
-        h[3] = remix_hi_fast<true>(kl.w, kh.w, sigma);
+        h[0] = remix_hi_fast<true>(kl.x, kh.x, sigma, H);
+        h[1] = remix_hi_fast<true>(kl.y, kh.y, sigma, H);
+        h[2] = remix_hi_fast<true>(kl.z, kh.z, sigma, H);
+        h[3] = remix_hi_fast<true>(kl.w, kh.w, sigma, H);
     }
 }
 
 template <int MODE, u32 GW>
 __device__ __forceinline__ u32 hash1(const KeysView& K, u32 j, u32 sigma) {
     return MODE == 0 ? remix_hi_nc(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), key_word<GW>(K, j, 2), sigma)
-                     : remix_hi_fast<true>(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), sigma);
+                     : remix_hi_fast<true>(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), sigma, K.H);
 }
+
+// kernel variants of the lower-level search: plain; with early rejection (full nodes with a
+// 32-bit packed counter); wide 64-bit packed counters (phases whose level has (f-1)*w > 32)
+enum { V_PLAIN = 0, V_CP = 1, V_WIDE = 2 };
 
 // Block-wide shift tables of the FULL lower-level nodes of a phase (all share f and w):
 // index 0 = lower level 1 (f1 parts of l), 1 = lower level 2 (f2 parts of u1).  Static
@@ -148,7 +155,7 @@ __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, 
 #pragma unroll 1
     for (u32 q = g0; q < ng; ++q, g += 12) {
         u32 h[4];
-        hash4<MODE>(g, sigma, h);
+        hash4<MODE>(g, sigma, h, K.H);
         if (CL < 2) {
             c0 += inc_full<CL>(h[0], r) + inc_full<CL>(h[1], r);
             c1 += inc_full<CL>(h[2], r) + inc_full<CL>(h[3], r);
@@ -165,6 +172,55 @@ __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, 
     return c0 + c1;
 }
 
+// Wide packed counter (l >= 19: (f-1)*w > 32): fields of parts 0..hs-1 in the low word,
+// parts hs..f-2 in the high word (hs = floor(32/w)); the table holds t = p*w (low word) or
+// 32 + (p-hs)*w (high word), 64 for the last part; increments 1 << t and 1 << (t-32), both
+// clamped to 0 out of range.  The exactness argument of DESIGN.md 5 holds per word.
+template <int MODE, int CL>
+__device__ __forceinline__ u64 count_lower_wide(const KeysView& K, u32 s, u32 sigma, u32 r) {
+    u32 lo = 0, hi = 0;
+    const u32 ng = s >> 2;
+    const u32* __restrict__ g = K.G;
+#pragma unroll 1
+    for (u32 q = 0; q < ng; ++q, g += 12) {
+        u32 h[4];
+        hash4<MODE>(g, sigma, h, K.H);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            u32 t;
+            if (CL < 2)
+                t = s_full_tab[CL < 2 ? CL : 0][__umulhi(h[k], r)];
+            else
+                asm volatile("{\n\t.reg .u32 ad;\n\tmad.hi.u32 ad, %1, %2, %3;\n\tld.shared.u8 %0, [ad];\n\t}"
+                             : "=r"(t)
+                             : "r"(h[k]), "r"(r), "r"(K.tbase));
+            lo += bit_clamp(t);
+            hi += bit_clamp(t - 32);
+        }
+    }
+    for (u32 j = ng << 2; j < s; ++j) {
+        const u32 h = hash1<MODE, 12>(K, j, sigma);
+        u32 t;
+        if (CL < 2)
+            t = s_full_tab[CL < 2 ? CL : 0][__umulhi(h, r)];
+        else
+            asm volatile("{\n\t.reg .u32 ad;\n\tmad.hi.u32 ad, %1, %2, %3;\n\tld.shared.u8 %0, [ad];\n\t}"
+                         : "=r"(t)
+                         : "r"(h), "r"(r), "r"(K.tbase));
+        lo += bit_clamp(t);
+        hi += bit_clamp(t - 32);
+    }
+    return ((u64)hi << 32) | lo;
+}
+
+// shift of part p in the packed counter: narrow p*w (32 = add nothing for the last part);
+// wide (split words, see count_lower_wide) p*w | 32+(p-hs)*w, 64 for the last part
+__host__ __device__ __forceinline__ u32 part_shift(u32 p, u32 f, u32 w) {
+    if ((f - 1) * w <= 32) return p + 1 < f ? p * w : 32;
+    const u32 hs = 32 / w;
+    return p + 1 >= f ? 64 : p < hs ? p * w : 32 + (p - hs) * w;
+}
+
 // Upper split: |{k : remap(h_k, s) < c0}| = |{k : h_k < T}|, T = ceil(c0 2^32 / s).
 template <int MODE>
 __device__ __forceinline__ u32 count_left(const KeysView& K, u32 s, u32 sigma, u32 T) {
@@ -174,7 +230,7 @@ __device__ __forceinline__ u32 count_left(const KeysView& K, u32 s, u32 sigma, u
 #pragma unroll 1
     for (u32 q = 0; q < ng; ++q, g += 12) {
         u32 h[4];
-        hash4<MODE>(g, sigma, h);
+        hash4<MODE>(g, sigma, h, K.H);
         c += (h[0] < T) + (h[1] < T) + (h[2] < T) + (h[3] < T);
     }
     for (u32 j = ng << 2; j < s; ++j) c += hash1<MODE, 12>(K, j, sigma) < T;
@@ -190,7 +246,7 @@ __device__ __forceinline__ void leaf_masks(const KeysView& K, u32 ng, u32 m, u32
 #pragma unroll 1
     for (u32 q = 0; q < ng; ++q, g += 20) {
         u32 h[4];
-        hash4<MODE>(g, base, h);
+        hash4<MODE>(g, base, h, K.H);
         const uint4 ma = *reinterpret_cast<const uint4*>(g + 12);
         const uint4 mb = *reinterpret_cast<const uint4*>(g + 16);
         const u32 t0 = 1u << __umulhi(h[0], m), t1 = 1u << __umulhi(h[1], m);
@@ -237,7 +293,7 @@ struct NodeCtx {
 
 
 // One trial of `sig` (32-bit fast path).  For rotation fitting r receives the rotation.
-template <int KIND, int MODE>
+template <int KIND, int MODE, bool WIDE = false>
 __device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, u32 sig, u32 lane, int& r) {
     if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
         const u32 base = KIND == SK_LEAF_RF ? sig * c.s : sig;
@@ -248,6 +304,12 @@ __device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, 
     } else if (KIND == SK_UPPER) {
         return count_left<MODE>(K, c.s, sig, c.mask) == c.target;
     } else {
+        if (WIDE) {
+            const u64 cnt = !c.full ? count_lower_wide<MODE, 2>(K, c.s, sig, c.r)
+                            : c.l2 ? count_lower_wide<MODE, 1>(K, c.s, sig, c.r)
+                                   : count_lower_wide<MODE, 0>(K, c.s, sig, c.r);
+            return (cnt & c.mask64) == c.target64;
+        }
         const u32 cnt = !c.full ? count_lower<MODE, 2>(K, c.s, sig, c.r)
                         : c.l2 ? count_lower<MODE, 1>(K, c.s, sig, c.r)
                                         : count_lower<MODE, 0>(K, c.s, sig, c.r);
@@ -256,7 +318,7 @@ __device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, 
 }
 
 // Generic 64-bit path (values >= 2^32; also the wide 64-bit packed counters, l >= 19).
-template <int KIND>
+template <int KIND, bool WIDE = false>
 __device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, u64 idx, u32 lane, int& r) {
     constexpr u32 GW = Layout<KIND>::GW;
     const u32 s = c.s;
@@ -275,9 +337,12 @@ __device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, 
         for (u32 j = 0; j < s; ++j) cnt += hash_slow<GW>(K, j, idx) < c.mask;
         return cnt == c.target;
     } else {
-        if (c.wide) {
+        if (WIDE) {
             u64 cnt = 0;
-            for (u32 j = 0; j < s; ++j) cnt += 1ull << (__umulhi(__umulhi(hash_slow<GW>(K, j, idx), s), c.mu) * c.w);
+            for (u32 j = 0; j < s; ++j) {
+                const u32 t = part_shift(__umulhi(__umulhi(hash_slow<GW>(K, j, idx), s), c.mu), c.f, c.w);
+                cnt += t < 64 ? 1ull << t : 0ull;
+            }
             return (cnt & c.mask64) == c.target64;
         }
         u32 cnt = 0;
@@ -290,7 +355,7 @@ __device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, 
 }
 
 // Load node n's keys into the warp's buffer and derive its constants.
-template <int KIND>
+template <int KIND, bool WIDE = false>
 __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G, u8* T8, NodeCtx& c) {
     constexpr u32 GW = Layout<KIND>::GW;
     const NodeRec rec = A.nodes[n];
@@ -338,7 +403,9 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
             c.unit = unit;
             c.full = (s == f * unit);
             c.mu = (u32)(((1ull << 32) + unit - 1) / unit);
-            c.wide = (f - 1) * w > 32;
+            // the wide kernel variant runs every node of its phase on the 64-bit counter (a
+            // partial node may itself fit 32 bits: part_shift then gives the narrow layout)
+            c.wide = WIDE;
             c.r = c.full ? f : s;
             c.l2 = s > A.u1;
             const u32 cpg = c.l2 ? A.cp_l2 : A.cp_l1;
@@ -355,10 +422,15 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
                     T8[v] = (u8)(p + 1 < f ? p * w : 32);
                 }
             } else {
-                u64 t = 0;
-                for (u32 j = 0; j + 1 < f; ++j) t += (u64)unit << (j * w);
+                u64 t = 0, m = 0;
+                for (u32 j = 0; j + 1 < f; ++j) {
+                    const u32 sh = part_shift(j, f, w);
+                    t += (u64)unit << sh;
+                    m |= (((u64)1 << w) - 1) << sh;
+                }
                 c.target64 = t;
-                c.mask64 = (1ull << ((f - 1) * w)) - 1ull;
+                c.mask64 = m;
+                for (u32 v = lane; v < c.r; v += 32) T8[v] = (u8)part_shift(c.full ? v : v / unit, f, w);
             }
         }
     }
@@ -445,15 +517,21 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
     return false;
 }
 
-template <int KIND, bool CP>
+template <int KIND, int VAR>
 __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
                                            u32 lane, u64* val, u32* qs, u32* qc) {
     const u64 ws = 32ull * A.iters;
-    // largest value (seed, or base seed k*m) any lane tries in this window
+    // smallest / largest value (seed, or base seed k*m) any lane tries in this window; the
+    // 32-bit paths need one high word H for all of them (values >= 2^32 run the carry path
+    // with x = k + H*2^32 + low word, same instruction count)
+    const u64 first = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
     const u64 last = KIND == SK_LEAF_RF ? (wstart + ws - 1) * c.s : wstart + ws - 1;
-    const bool fast = last < (1ull << 32) && !(KIND == SK_LOWER && c.wide);
-    const bool nocarry = fast && last <= c.margin;
-    if (CP && KIND == SK_LOWER && nocarry && c.cp)
+    const u32 H = (u32)(first >> 32);
+    const bool fast = (u32)(last >> 32) == H && (last >> 32) == (first >> 32);
+    const bool nocarry = H == 0 && last <= c.margin;
+    KeysView KH = K;
+    KH.H = H;
+    if (VAR == V_CP && KIND == SK_LOWER && nocarry && c.cp)
         return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, qc, val)
                     : run_window_cp<0>(A, K, c, wstart, lane, qs, qc, val);
     for (u32 it = 0; it < A.iters; ++it) {
@@ -461,11 +539,11 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, con
         int r = 0;
         bool ok;
         if (nocarry)
-            ok = trial_fast<KIND, 0>(K, c, (u32)idx, lane, r);
+            ok = trial_fast<KIND, 0, VAR == V_WIDE>(K, c, (u32)idx, lane, r);
         else if (fast)
-            ok = trial_fast<KIND, 1>(K, c, (u32)idx, lane, r);
+            ok = trial_fast<KIND, 1, VAR == V_WIDE>(KH, c, (u32)idx, lane, r);
         else
-            ok = trial_slow<KIND>(K, c, idx, lane, r);
+            ok = trial_slow<KIND, VAR == V_WIDE>(K, c, idx, lane, r);
         const u32 bal = __ballot_sync(FULL, ok);
         if (bal) {
             const int win = __ffs(bal) - 1;
@@ -501,7 +579,7 @@ __device__ u32 find_help(const Args& A, u32 gw, u32 lane, u32 nn) {
 #ifndef RS_MIN_BLOCKS
 #define RS_MIN_BLOCKS 1
 #endif
-template <int KIND, bool CP = false>
+template <int KIND, int VAR = V_PLAIN>
 __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 : RS_MIN_BLOCKS) k_search(const Args A) {
     constexpr u32 GW = Layout<KIND>::GW;
     extern __shared__ __align__(16) u32 smem32[];
@@ -520,7 +598,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             const u32 cl = t >> 5, p = t & 31;
             const u32 unit = cl ? A.u1 : A.leaf, f = cl ? A.u2 / A.u1 : A.u1 / A.leaf;
             const u32 w = 32 - __clz(unit + 1);
-            s_full_tab[cl][p] = (u8)(p + 1 < f ? p * w : 32);
+            s_full_tab[cl][p] = (u8)part_shift(p, f, w);
         }
         __syncthreads();
     }
@@ -538,7 +616,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             if (n0 >= nn) break;
             const u32 n1 = min(n0 + A.batch, nn);
             for (u32 n = n0; n < n1; ++n) {
-                load_node<KIND>(A, n, lane, G, T8, c);
+                load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c);
                 u64 val = 0;
                 for (u64 wstart = 0;; wstart += ws) {
                     if (wstart >= kSeedCap) {
@@ -546,7 +624,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                         val = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
                         break;
                     }
-                    if (run_window<KIND, CP>(A, K, c, wstart, lane, &val, QS, QC)) break;
+                    if (run_window<KIND, VAR>(A, K, c, wstart, lane, &val, QS, QC)) break;
                 }
                 if (lane == 0) A.values[c.slot] = val;
                 __syncwarp();
@@ -568,7 +646,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             }
             node = n;
             if (lane == 0) ((volatile int*)A.active)[gw] = (int)n;
-            load_node<KIND>(A, n, lane, G, T8, c);
+            load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c);
         }
         u32 w = 0;
         u64 f = 0;
@@ -593,15 +671,15 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             continue;
         }
         u64 val;
-        if (run_window<KIND, CP>(A, K, c, wstart, lane, &val, QS, QC) && lane == 0)
+        if (run_window<KIND, VAR>(A, K, c, wstart, lane, &val, QS, QC) && lane == 0)
             atomicMin((unsigned long long*)(A.values + c.slot), (unsigned long long)val);
     }
 }
 
-template <int KIND, bool CP = false>
+template <int KIND, int VAR = V_PLAIN>
 void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 grid, cudaStream_t st) {
-    cudaFuncSetAttribute(k_search<KIND, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    k_search<KIND, CP><<<grid, wpb * 32, smem, st>>>(A);
+    cudaFuncSetAttribute(k_search<KIND, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    k_search<KIND, VAR><<<grid, wpb * 32, smem, st>>>(A);
 }
 
 }  // namespace
@@ -665,12 +743,19 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.n_warps = grid * wpb;
     switch (P.kind) {
         case SK_UPPER: launch_kind<SK_UPPER>(P, A, wpb, smem, grid, st); break;
-        case SK_LOWER:
-            if (A.cp_l1 | A.cp_l2)
-                launch_kind<SK_LOWER, true>(P, A, wpb, smem, grid, st);
+        case SK_LOWER: {
+            // the phase holds one level: lower level 2 iff its largest node exceeds u1
+            const bool l2 = P.max_size > P.u1;
+            const u32 unit = l2 ? P.u1 : P.leaf, f = l2 ? P.u2 / P.u1 : P.u1 / P.leaf;
+            const u32 w = 32 - __builtin_clz(unit + 1);
+            if ((f - 1) * w > 32)
+                launch_kind<SK_LOWER, V_WIDE>(P, A, wpb, smem, grid, st);
+            else if (A.cp_l1 | A.cp_l2)
+                launch_kind<SK_LOWER, V_CP>(P, A, wpb, smem, grid, st);
             else
                 launch_kind<SK_LOWER>(P, A, wpb, smem, grid, st);
             break;
+        }
         case SK_LEAF_RF: launch_kind<SK_LEAF_RF>(P, A, wpb, smem, grid, st); break;
         case SK_LEAF_BF: launch_kind<SK_LEAF_BF>(P, A, wpb, smem, grid, st); break;
     }

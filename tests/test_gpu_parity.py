@@ -75,6 +75,24 @@ def test_leaf_search_large_m():
     assert got.tolist() == want
 
 
+def test_leaf_values_above_2_32():
+    """Rotation-fitting leaves of 24 keys have stored values around 2^31..2^33 (mean 2.1e9,
+    SURVEY 8(f) N3): values >= 2^32 run the carry path with a per-window high word.  Among
+    1500 random 24-key leaves, the ones the GPU stores above 2^32 (below 1.6 * 2^32, to bound
+    the oracle's time) are re-searched by the oracle from k = 0."""
+    rng = np.random.default_rng(2432)
+    m, nl = 24, 1500
+    off = np.arange(nl + 1, dtype=np.uint32) * m
+    lo = rng.integers(0, M64, size=nl * m, dtype=np.uint64, endpoint=True)
+    isb = rng.integers(0, 2, size=nl * m, dtype=np.uint8)
+    got = rs.search_leaves(lo, isb, off, rotation_fitting=True)
+    big = [j for j in range(nl) if (1 << 32) <= int(got[j]) < int(1.6 * (1 << 32))][:6]
+    assert len(big) >= 3
+    with ThreadPoolExecutor(len(big)) as ex:
+        want = list(ex.map(lambda j: oracle.leaf_rf(lo[j * m:(j + 1) * m], isb[j * m:(j + 1) * m]), big))
+    assert [int(got[j]) for j in big] == want
+
+
 @pytest.mark.parametrize("leaf", [2, 3, 5, 8, 12, 16, 19, 20, 24])
 def test_split_search_parity(leaf):
     """Every split class the oracle can finish in seconds: L1 full/partial, L2
