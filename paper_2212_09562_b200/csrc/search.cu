@@ -289,6 +289,7 @@ struct NodeCtx {
     u32 l2;  // lower level 2 node (s > u1)
     u64 target64, mask64;
     u32 cp;  // early rejection (full lower nodes): checkpoint in key groups, 0 = off
+    u64 kW;  // key rebase: the buffered keys are lo + kW (values are tried relative to kW)
 };
 
 
@@ -436,6 +437,29 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
     }
     for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
     c.margin = mg;
+    c.kW = 0;
+    __syncwarp();
+}
+
+// Rebase the buffered keys by delta (mod 2^64): lo' = lo + delta, kc' = key_const(hi'), and
+// the new carry margin min(2^32 - 1 - lo'_low).  Trying value v on key lo equals trying
+// v - kW on lo + kW, so a window of large values becomes a window of small ones and stays
+// on the no-carry path (a window of span <= margin never carries).
+template <u32 GW>
+__device__ __noinline__ void rebase_keys(u32* G, u32 s, u64 delta, u32 lane, u32& margin) {
+    __syncwarp();
+    u32 mg = FULL;
+    for (u32 j = lane; j < s; j += 32) {
+        u32* p = G + GW * (j >> 2) + (j & 3);
+        const u64 k = (((u64)p[4] << 32) | p[0]) + delta;
+        const u32 kh = (u32)(k >> 32);
+        p[0] = (u32)k;
+        p[4] = kh;
+        p[8] = key_const(kh);
+        mg = min(mg, ~(u32)k);
+    }
+    for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
+    margin = mg;
     __syncwarp();
 }
 
@@ -452,6 +476,7 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
 template <int CL>
 __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart, u32 lane,
                                            u32* qs, u32* qc, u64* val) {
+    const u32 wrel = (u32)(wstart - c.kW);  // window start relative to the key rebase
     // packed "some field > unit" test: ((cnt & me) + ke) & ce | ((cnt & mo) + ko) & co, fields
     // 0..f-2 split into even and odd ones so that the added carries stay inside a field gap
     u32 me = 0, mo = 0, ke = 0, ko = 0, ce = 0, co = 0;
@@ -474,7 +499,7 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
     u32 qn = 0;
     for (u32 it = 0; it <= A.iters; ++it) {
         if (it < A.iters) {
-            const u32 sig = (u32)(wstart + (u64)it * 32 + lane);
+            const u32 sig = wrel + it * 32 + lane;
             const u32 cnt = count_lower<0, CL, false>(K, c.s, sig, c.r, 0, c.cp);
             const bool rej = ((((cnt & me) + ke) & ce) | (((cnt & mo) + ko) & co)) != 0;
             const u32 bal = __ballot_sync(FULL, !rej);
@@ -496,7 +521,7 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
         cnt = count_lower<0, CL, true>(K, c.s, sig, c.r, c.cp, 0xffffffffu, cnt);
         const u32 bal = __ballot_sync(FULL, have && (cnt & c.mask) == c.target);
         if (bal) {
-            *val = __shfl_sync(FULL, sig, __ffs(bal) - 1);
+            *val = c.kW + __shfl_sync(FULL, sig, __ffs(bal) - 1);
             return true;
         }
         __syncwarp();
@@ -518,29 +543,53 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
 }
 
 template <int KIND, int VAR>
-__device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
+__device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, NodeCtx& c, u64 wstart,
                                            u32 lane, u64* val, u32* qs, u32* qc) {
+    constexpr u32 GW = Layout<KIND>::GW;
     const u64 ws = 32ull * A.iters;
-    // smallest / largest value (seed, or base seed k*m) any lane tries in this window; the
-    // 32-bit paths need one high word H for all of them (values >= 2^32 run the carry path
-    // with x = k + H*2^32 + low word, same instruction count)
-    const u64 first = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
-    const u64 last = KIND == SK_LEAF_RF ? (wstart + ws - 1) * c.s : wstart + ws - 1;
+    const u64 sc = KIND == SK_LEAF_RF ? c.s : 1;  // value units per seed index
+    // No-carry path relative to the key rebase c.kW (seed index units): values of the window
+    // minus the rebase must stay within the carry margin; otherwise rebase the buffered keys
+    // to the window start (cheap: s keys once per ~margin/span windows).
+    if (wstart < c.kW || (wstart - c.kW + ws) * sc - 1 > c.margin) {
+        rebase_keys<GW>(const_cast<u32*>(K.G), c.s, (wstart - c.kW) * sc, lane, c.margin);
+        c.kW = wstart;
+    }
+    if (ws * sc - 1 <= c.margin) {
+        const u32 wrel = (u32)(wstart - c.kW);
+        if (VAR == V_CP && KIND == SK_LOWER && c.cp)
+            return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, qc, val)
+                        : run_window_cp<0>(A, K, c, wstart, lane, qs, qc, val);
+        for (u32 it = 0; it < A.iters; ++it) {
+            int r = 0;
+            const bool ok = trial_fast<KIND, 0, VAR == V_WIDE>(K, c, wrel + it * 32 + lane, lane, r);
+            const u32 bal = __ballot_sync(FULL, ok);
+            if (bal) {
+                const int win = __ffs(bal) - 1;
+                u64 v = wstart + (u64)it * 32 + win;
+                if (KIND == SK_LEAF_RF) v = v * c.s + (u32)__shfl_sync(FULL, r, win);
+                *val = v;
+                return true;
+            }
+        }
+        return false;
+    }
+    // rare (a key within one window span of 2^32 after rebasing): absolute values on the
+    // original keys, carry path with one high word per window, else the generic 64-bit path
+    if (c.kW) {
+        rebase_keys<GW>(const_cast<u32*>(K.G), c.s, (0 - c.kW) * sc, lane, c.margin);
+        c.kW = 0;
+    }
+    const u64 first = wstart * sc, last = (wstart + ws - 1) * sc;
     const u32 H = (u32)(first >> 32);
-    const bool fast = (u32)(last >> 32) == H && (last >> 32) == (first >> 32);
-    const bool nocarry = H == 0 && last <= c.margin;
+    const bool fast = (last >> 32) == (first >> 32);
     KeysView KH = K;
     KH.H = H;
-    if (VAR == V_CP && KIND == SK_LOWER && nocarry && c.cp)
-        return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, qc, val)
-                    : run_window_cp<0>(A, K, c, wstart, lane, qs, qc, val);
     for (u32 it = 0; it < A.iters; ++it) {
         const u64 idx = wstart + (u64)it * 32 + lane;
         int r = 0;
         bool ok;
-        if (nocarry)
-            ok = trial_fast<KIND, 0, VAR == V_WIDE>(K, c, (u32)idx, lane, r);
-        else if (fast)
+        if (fast)
             ok = trial_fast<KIND, 1, VAR == V_WIDE>(KH, c, (u32)idx, lane, r);
         else
             ok = trial_slow<KIND, VAR == V_WIDE>(K, c, idx, lane, r);

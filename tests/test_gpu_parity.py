@@ -118,6 +118,52 @@ def test_split_search_parity(leaf):
     assert got.tolist() == want
 
 
+def _near_carry_keys(rng, n):
+    """Keys whose low 32 bits lie within 2^12 of 2^32: remix(lo + sigma) carries into the
+    high word for tiny seeds, so the searches start on the carry path and then rebase the
+    buffered keys once the window start passes the carry boundary."""
+    hi = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
+    low = np.uint64(0xFFFFFFFF) - rng.integers(0, 1 << 12, size=n, dtype=np.uint64)
+    return (hi << np.uint64(32)) | low
+
+
+@pytest.mark.parametrize("leaf", [5, 8, 16, 20])
+def test_carry_and_rebase_paths(leaf):
+    """Splits (lower and upper) and leaves (rotation fitting and brute force) over keys next
+    to the carry boundary equal the oracle's values."""
+    _, _, u1, u2 = oracle.shape(leaf)
+    rng = np.random.default_rng(77 + leaf)
+    sizes = [s for s in (leaf + 1, u1, u1 + 1, u2, 2 * u2 + 1)
+             if s / oracle.split_prob(leaf, s) <= 3e8]
+    sizes = sizes * 3
+    off = np.zeros(len(sizes) + 1, dtype=np.uint32)
+    off[1:] = np.cumsum(sizes)
+    lo = _near_carry_keys(rng, int(off[-1]))
+    got = rs.search_splits(lo, off, leaf)
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        want = list(ex.map(lambda j: oracle.find_split(leaf, lo[off[j]:off[j + 1]]), range(len(sizes))))
+    assert got.tolist() == want
+    m = min(leaf, 14)
+    lsz = [m, m - 1, 2, m] * 8
+    loff = np.zeros(len(lsz) + 1, dtype=np.uint32)
+    loff[1:] = np.cumsum(lsz)
+    llo = _near_carry_keys(rng, int(loff[-1]))
+    isb = rng.integers(0, 2, size=int(loff[-1]), dtype=np.uint8)
+    sl = [(int(loff[j]), int(loff[j + 1])) for j in range(len(lsz))]
+    got = rs.search_leaves(llo, isb, loff, rotation_fitting=True)
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        want = list(ex.map(lambda ab: oracle.leaf_rf(llo[ab[0]:ab[1]], isb[ab[0]:ab[1]]), sl))
+    assert got.tolist() == want
+    bsz = [min(m, 10), 7, 3] * 6
+    boff = np.zeros(len(bsz) + 1, dtype=np.uint32)
+    boff[1:] = np.cumsum(bsz)
+    blo = _near_carry_keys(rng, int(boff[-1]))
+    got = rs.search_leaves(blo, np.zeros(len(blo), np.uint8), boff, rotation_fitting=False)
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        want = list(ex.map(lambda j: oracle.leaf_bf(blo[boff[j]:boff[j + 1]]), range(len(bsz))))
+    assert got.tolist() == want
+
+
 # ------------------------------------------------------------------- end to end --
 
 def _check_full(keys, leaf, b, rf=True, threads=None):
