@@ -73,6 +73,10 @@ typedef struct {
     uint32_t virtual_shards;   /* >1: run the bucket-range sharded path with this many
                                   shards on one device and stitch them (tests the multi-GPU
                                   offset logic); 0/1 = unsharded */
+    uint32_t reserved;         /* 0 */
+    uint64_t total_keys;       /* recsplit_shard_begin only: keys of the WHOLE sharded build when
+                                  each rank passes just the keys it owns (routed with
+                                  recsplit_route_keys); 0 = n (every rank passes all keys) */
 } recsplit_options;
 
 /* Per-build statistics (optional output). Times are device (CUDA event) seconds. */
@@ -235,6 +239,18 @@ RECSPLIT_API int recsplit_shard_finish(recsplit_shard *sh, int64_t min_step, rec
 RECSPLIT_API int recsplit_stitch(const uint8_t *const *parts, const size_t *sizes, int32_t count,
                                  recsplit_bytes *out);
 RECSPLIT_API void recsplit_shard_free(recsplit_shard *sh); /* NULL-safe */
+
+/* Key routing for sharded builds: rank r of `world` owns the buckets
+ * [floor(rB/world), floor((r+1)B/world)), B = ceil(total_keys / bucket_size) (R12), bucket =
+ * remap(hi, B) of the master hash code (R2, R3, global_seed from opt).  Groups the n DEVICE
+ * keys d_keys (this rank's slice of the input) by owner: d_out (DEVICE, n u64) receives the
+ * keys for rank 0, then rank 1, ...; counts (HOST, world u64) the number per rank.  After an
+ * all-to-all exchange every rank holds exactly its keys and calls recsplit_shard_begin with
+ * opt->total_keys = total_keys.  Synchronises `stream`; the order inside a group is arbitrary
+ * (the output bytes do not depend on key order). */
+RECSPLIT_API int recsplit_route_keys(const uint64_t *d_keys, size_t n, uint64_t total_keys,
+                                     uint32_t bucket_size, const recsplit_options *opt, int32_t world,
+                                     void *stream, uint64_t *d_out, uint64_t *counts);
 /* Host arithmetic of step 3 (tests): out = {n, D, delta_C, beta, key_base, bit_base}. */
 RECSPLIT_API int recsplit_shard_globals(const uint64_t *summaries, int32_t world, int32_t rank,
                                         uint64_t out[6]);

@@ -26,7 +26,7 @@ SYMBOLS = [
     "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch", "recsplit_shard_free",
     "recsplit_shard_globals", "recsplit_query_device", "recsplit_build_strings", "recsplit_query_strings",
     "recsplit_open", "recsplit_handle_query_many", "recsplit_handle_query_device", "recsplit_close",
-    "recsplit_check_bijective_device",
+    "recsplit_check_bijective_device", "recsplit_route_keys",
 ]
 
 
@@ -42,7 +42,8 @@ class Bytes(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("rotation_fitting", C.c_uint32),
-                ("global_seed", C.c_uint64), ("device", C.c_int32), ("virtual_shards", C.c_uint32)]
+                ("global_seed", C.c_uint64), ("device", C.c_int32), ("virtual_shards", C.c_uint32),
+                ("reserved", C.c_uint32), ("total_keys", C.c_uint64)]
 
 
 class Stats(C.Structure):
@@ -117,6 +118,9 @@ def lib():
         L.recsplit_handle_query_device.restype = i32
         L.recsplit_check_bijective_device.argtypes = [C.c_void_p, sz, P64, C.c_void_p]
         L.recsplit_check_bijective_device.restype = i32
+        L.recsplit_route_keys.argtypes = [C.c_void_p, sz, u64, u32, C.POINTER(Options), C.c_int32, C.c_void_p,
+                                          C.c_void_p, P64]
+        L.recsplit_route_keys.restype = i32
         L.recsplit_close.argtypes = [C.c_void_p]
         L.recsplit_close.restype = None
         for name in ("recsplit_shard_begin", "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch",
@@ -140,8 +144,9 @@ def _p64(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_uint64))
 
 
-def _opts(rotation_fitting: bool, global_seed: int, device: int, virtual_shards: int):
-    return Options(C.sizeof(Options), int(bool(rotation_fitting)), global_seed, device, virtual_shards)
+def _opts(rotation_fitting: bool, global_seed: int, device: int, virtual_shards: int, total_keys: int = 0):
+    return Options(C.sizeof(Options), int(bool(rotation_fitting)), global_seed, device, virtual_shards, 0,
+                   total_keys)
 
 
 def _take(b: Bytes) -> bytes:
@@ -352,7 +357,9 @@ class Shard:
     """One rank's share of a sharded build (include/recsplit.h, recsplit_shard_*)."""
 
     def __init__(self, keys_tensor, leaf_size: int, bucket_size: int, rank: int, world: int,
-                 rotation_fitting: bool = True, global_seed: int = 0, stream=None):
+                 rotation_fitting: bool = True, global_seed: int = 0, stream=None, total_keys: int = 0):
+        """keys_tensor: all keys (total_keys = 0), or exactly the keys this rank owns after
+        route_keys + all-to-all (total_keys = the whole build's key count)."""
         import torch
 
         if not keys_tensor.is_cuda or not keys_tensor.is_contiguous() or keys_tensor.element_size() != 8:
@@ -361,7 +368,7 @@ class Shard:
             stream = torch.cuda.current_stream(keys_tensor.device)
         self._h = C.c_void_p()
         self.summary = np.zeros(8, dtype=np.uint64)
-        o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, 0)
+        o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, 0, total_keys)
         _check(lib().recsplit_shard_begin(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), leaf_size,
                                           bucket_size, C.byref(o), rank, world, C.c_void_p(stream.cuda_stream),
                                           C.byref(self._h), _p64(self.summary)))
@@ -452,15 +459,70 @@ def gather_parts(part: bytes, dst: int = 0, group=None):
     return [host[r * mx: r * mx + sizes[r]].tobytes() for r in range(world)]
 
 
+def route_keys(keys_tensor, total_keys: int, bucket_size: int, world: int, global_seed: int = 0, stream=None):
+    """Group this rank's CUDA keys by the rank that owns their bucket (recsplit_route_keys):
+    returns (keys grouped rank by rank, list of per-rank counts)."""
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream(keys_tensor.device)
+    out = torch.empty_like(keys_tensor)
+    counts = np.zeros(world, dtype=np.uint64)
+    o = _opts(True, global_seed, keys_tensor.device.index, 0)
+    _check(lib().recsplit_route_keys(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), total_keys,
+                                     bucket_size, C.byref(o), world, C.c_void_p(stream.cuda_stream),
+                                     C.c_void_p(out.data_ptr()), _p64(counts)))
+    return out, [int(c) for c in counts]
+
+
+def exchange_keys(routed, send_counts, group=None):
+    """all-to-all of routed keys (NCCL: device buffers; gloo: through host memory): returns
+    the keys this rank owns, on routed's device."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    nccl = dist.get_backend(group) == "nccl"
+    dev = routed.device if nccl else torch.device("cpu")
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+    rc = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_to_all_single(rc, sc, group=group)
+    recv_counts = rc.cpu().tolist()
+    src = routed if nccl else routed.cpu()
+    recv = torch.empty(sum(recv_counts), dtype=routed.dtype, device=dev)
+    dist.all_to_all_single(recv, src, output_split_sizes=recv_counts, input_split_sizes=list(send_counts),
+                           group=group)
+    return recv if nccl else recv.to(routed.device)
+
+
+def allreduce_sum(x: int, group=None) -> int:
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return int(t.item())
+
+
 def build_sharded(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
-                  global_seed: int = 0, group=None, stream=None):
+                  global_seed: int = 0, group=None, stream=None, distribute: bool = False):
     """Multi-GPU build of ONE MPHF over the torch.distributed group (one rank per GPU):
     bucket ranges per rank, allgather of summaries, allreduce-min of the residual step,
-    parts gathered to rank 0 and stitched.  Returns the bytes on rank 0, None elsewhere."""
+    parts gathered to rank 0 and stitched.  Returns the bytes on rank 0, None elsewhere.
+    distribute=False: every rank passes ALL keys (each keeps its buckets);
+    distribute=True: each rank passes its own slice of the input; the keys are routed to
+    their owners with one all-to-all."""
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    sh = Shard(keys_tensor, leaf_size, bucket_size, rank, world, rotation_fitting, global_seed, stream)
+    total = 0
+    if distribute:
+        total = allreduce_sum(keys_tensor.numel(), group)
+        routed, counts = route_keys(keys_tensor, total, bucket_size, world, global_seed, stream)
+        keys_tensor = exchange_keys(routed, counts, group)
+        del routed
+    sh = Shard(keys_tensor, leaf_size, bucket_size, rank, world, rotation_fitting, global_seed, stream, total)
     try:
         allsum = exchange_summaries(sh.summary, group)
         step = allreduce_min(sh.min_step(allsum), group)

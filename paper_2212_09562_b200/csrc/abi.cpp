@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <memory>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -59,11 +60,13 @@ rs::BuildParams params_of(size_t n, uint32_t leaf, uint32_t b, const recsplit_op
     p.device = -1;
     p.shards = 1;
     if (opt) {
-        if (opt->struct_size < sizeof(recsplit_options)) throw rs::Error(RECSPLIT_E_INVALID, "bad options struct_size");
+        if (opt->struct_size < offsetof(recsplit_options, reserved))
+            throw rs::Error(RECSPLIT_E_INVALID, "bad options struct_size");
         p.rf = opt->rotation_fitting != 0;
         p.g = opt->global_seed;
         p.device = opt->device;
         p.shards = opt->virtual_shards ? opt->virtual_shards : 1;
+        if (opt->struct_size >= offsetof(recsplit_options, total_keys) + sizeof(uint64_t)) p.n_total = opt->total_keys;
     }
     return p;
 }
@@ -568,10 +571,13 @@ struct recsplit_shard {
 int recsplit_shard_begin(const uint64_t* d_keys, size_t n, uint32_t leaf_size, uint32_t bucket_size,
                          const recsplit_options* opt, int32_t rank, int32_t world, void* stream, recsplit_shard** out,
                          uint64_t summary[8]) {
-    if (!out || !summary || !d_keys) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    if (!out || !summary || (!d_keys && n)) return fail(RECSPLIT_E_INVALID, "NULL argument");
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) return fail(RECSPLIT_E_INVALID, "bad rank/world");
-    int rc = check_args(n, leaf_size, bucket_size);
+    // routed shards (opt->total_keys > 0) may hold no key at all; the build's count is checked
+    const bool routed = opt && opt->struct_size >= sizeof(recsplit_options) && opt->total_keys;
+    if (routed && opt->total_keys < n) return fail(RECSPLIT_E_INVALID, "total_keys < n");
+    int rc = check_args(routed ? opt->total_keys : n, leaf_size, bucket_size);
     if (rc) return rc;
     return guarded([&]() -> int {
         std::lock_guard<std::mutex> g(g_build_mu);
@@ -587,6 +593,21 @@ int recsplit_shard_begin(const uint64_t* d_keys, size_t n, uint32_t leaf_size, u
         cudaGetDevice(&h->device);
         memcpy(summary, h->shard->summary, 64);
         *out = h;
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_route_keys(const uint64_t* d_keys, size_t n, uint64_t total_keys, uint32_t bucket_size,
+                        const recsplit_options* opt, int32_t world, void* stream, uint64_t* d_out, uint64_t* counts) {
+    if (!counts || ((!d_keys || !d_out) && n)) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    if (world < 1) return fail(RECSPLIT_E_INVALID, "world must be >= 1");
+    if (bucket_size == 0) return fail(RECSPLIT_E_INVALID, "bucket_size must be >= 1");
+    if (total_keys < n || total_keys == 0 || total_keys >= (1ull << 32))
+        return fail(RECSPLIT_E_INVALID, "total_keys must be in [max(n, 1), 2^32)");
+    return guarded([&]() -> int {
+        rs::BuildParams p = params_of(total_keys, 2, bucket_size, opt);
+        select_device(p.device);
+        rs::route_keys(d_keys, n, total_keys, bucket_size, p.g, (uint32_t)world, (cudaStream_t)stream, d_out, counts);
         return RECSPLIT_OK;
     });
 }

@@ -2,7 +2,11 @@
 // detection, counting sort by bucket.
 // P:106-108 (initial hash, buckets of expected size b), P:319 (sort by bucket index,
 // determine borders), P:389 (random integers as MHC).
+#include <algorithm>
+#include <vector>
+
 #include "kernels.h"
+#include "pipeline.h"
 
 namespace rs {
 
@@ -205,6 +209,101 @@ void launch_mhc_strings(const u8* data, const u64* off, u64 n, u64 g, u64* mhc, 
     if (grid == 0) grid = 1;
     k_mhc_strings<<<grid, 256, 0, st>>>(data, off, n, g, mhc);
     g_launches++;
+}
+
+}  // namespace rs
+
+namespace rs {
+using namespace rsd;
+namespace {
+
+// owner rank of bucket i under the contiguous split [floor(rB/W), floor((r+1)B/W))
+__device__ __forceinline__ u32 owner_of(u64 i, u64 B, u32 W) {
+    u32 r = (u32)((i * W) / B);  // floor(rB/W) <= i for this r or r - 1
+    while (r + 1 < W && (B * (r + 1)) / W <= i) ++r;
+    while (r > 0 && (B * r) / W > i) --r;
+    return r;
+}
+
+// pass 1: keys per destination rank (block histogram in shared memory)
+__global__ void k_route_count(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 W, u64* __restrict__ counts) {
+    extern __shared__ unsigned long long rc[];
+    for (u32 i = threadIdx.x; i < W; i += blockDim.x) rc[i] = 0;
+    __syncthreads();
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 h = remix64(keys[i] ^ g ^ MHC_SALT_HI);
+        atomicAdd(rc + owner_of(((h >> 32) * B) >> 32, B, W), 1ull);
+    }
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < W; i += blockDim.x)
+        if (rc[i]) atomicAdd((unsigned long long*)counts + i, rc[i]);
+}
+
+// pass 2: scatter every key to its destination's segment (cursor = segment start, advanced
+// with one atomic per destination per block)
+__global__ void k_route_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 W,
+                                u64* __restrict__ cursor, u64* __restrict__ out) {
+    extern __shared__ unsigned long long rs_[];
+    unsigned long long* cnt = rs_;       // W
+    unsigned long long* base = rs_ + W;  // W
+    const u64 per = (u64)blockDim.x * 8;
+    for (u64 t0 = (u64)blockIdx.x * per; t0 < n; t0 += (u64)gridDim.x * per) {
+        for (u32 i = threadIdx.x; i < W; i += blockDim.x) cnt[i] = 0;
+        __syncthreads();
+        u32 dst[8];
+        unsigned long long pos[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const u64 i = t0 + (u64)q * blockDim.x + threadIdx.x;
+            dst[q] = 0xffffffffu;
+            if (i < n) {
+                const u64 h = remix64(keys[i] ^ g ^ MHC_SALT_HI);
+                dst[q] = owner_of(((h >> 32) * B) >> 32, B, W);
+                pos[q] = atomicAdd(cnt + dst[q], 1ull);
+            }
+        }
+        __syncthreads();
+        for (u32 i = threadIdx.x; i < W; i += blockDim.x)
+            base[i] = cnt[i] ? atomicAdd((unsigned long long*)cursor + i, cnt[i]) : 0;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (dst[q] != 0xffffffffu) out[base[dst[q]] + pos[q]] = keys[t0 + (u64)q * blockDim.x + threadIdx.x];
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+void route_keys(const u64* d_keys, u64 n, u64 total, u32 bucket, u64 g, u32 world, cudaStream_t st, u64* d_out,
+                u64* counts) {
+    const u64 B = (total + bucket - 1) / bucket;  // R12, global
+    u64* d = nullptr;
+    if (cudaMallocAsync(&d, 16 * (size_t)world, st) != cudaSuccess) throw Error(RECSPLIT_E_NOMEM, "route buffer");
+    struct Free {
+        u64* p;
+        cudaStream_t s;
+        ~Free() { cudaFreeAsync(p, s); }
+    } fr{d, st};
+    cudaMemsetAsync(d, 0, 8 * (size_t)world, st);
+    const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>((n + 1023) / 1024, 148ull * 4));
+    if (n) {
+        k_route_count<<<grid, 1024, world * 8, st>>>(d_keys, n, g, B, world, d);
+        g_launches++;
+    }
+    if (cudaMemcpyAsync(counts, d, 8 * (size_t)world, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        throw Error(RECSPLIT_E_CUDA, "route count failed");
+    std::vector<u64> start(world, 0);
+    for (u32 r = 1; r < world; ++r) start[r] = start[r - 1] + counts[r - 1];
+    cudaMemcpyAsync(d + world, start.data(), 8 * (size_t)world, cudaMemcpyHostToDevice, st);
+    if (n) {
+        const unsigned g2 = (unsigned)std::max<u64>(1, std::min<u64>((n + 8191) / 8192, 148ull * 4));
+        k_route_scatter<<<g2, 1024, world * 16, st>>>(d_keys, n, g, B, world, d + world, d_out);
+        g_launches++;
+    }
+    if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+        throw Error(RECSPLIT_E_CUDA, "route scatter failed");
 }
 
 }  // namespace rs

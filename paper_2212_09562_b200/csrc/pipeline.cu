@@ -215,6 +215,7 @@ Globals compute_globals(const uint64_t* all, int world, int rank) {
         if (x[SUM_MINB] < mn) mn = x[SUM_MINB];
         if (x[SUM_DUP]) G.dup = 1;
         if (x[SUM_ERR]) G.err = 1;
+        if (x[SUM_NTOT] != all[SUM_NTOT]) G.err = 2;  // ranks disagree on the build's key count
     }
     G.dC = mn == UINT64_MAX ? 0 : mn;
     G.beta = G.n ? (uint64_t)(((unsigned __int128)G.D << 20) / G.n) : 0;
@@ -267,7 +268,8 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     I.world = world;
     const uint64_t n = p.n;
     const uint32_t leaf = p.leaf;
-    const uint64_t B = (n + p.bucket - 1) / p.bucket;  // R12
+    const uint64_t ntot = p.n_total ? p.n_total : n;  // routed shards: the whole build's count
+    const uint64_t B = (ntot + p.bucket - 1) / p.bucket;  // R12
     I.B = B;
     I.b0 = B * (uint64_t)rank / (uint64_t)world;
     I.b1 = B * (uint64_t)(rank + 1) / (uint64_t)world;
@@ -284,6 +286,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     summary[SUM_B0] = I.b0;
     summary[SUM_B1] = I.b1;
     summary[SUM_MINB] = UINT64_MAX;
+    summary[SUM_NTOT] = ntot;
     Arena& A = I.A;
     Timer tm(st);
     const int e0 = tm.mark();
@@ -516,8 +519,12 @@ long long Shard::min_step(const uint64_t* all) {
     Impl& I = *impl_;
     I.G = compute_globals(all, I.world, I.rank);
     if (I.G.dup) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
+    if (I.G.err == 2) throw Error(RECSPLIT_E_INVALID, "ranks disagree on the total key count");
     if (I.G.err) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
-    if (I.G.n != I.p.n) throw Error(RECSPLIT_E_CUDA, "shard summaries do not add up to n");
+    const uint64_t ntot = I.p.n_total ? I.p.n_total : I.p.n;
+    if (I.G.n != ntot)
+        throw Error(RECSPLIT_E_INVALID, "the shards' keys do not add up to the build's key count "
+                                        "(a key was given to a rank that does not own its bucket)");
     if (I.Bl == 0) return LLONG_MAX;
     IndexView v{I.b0, I.Bl, I.G.key_base, I.G.bit_base, I.G.beta};
     long long* d = I.A.alloc<long long>(1);

@@ -24,6 +24,7 @@ struct BuildParams {
     int device;
     uint32_t shards;  // virtual shards (>= 1)
     bool strings = false;  // keys are precomputed master hash codes of strings (2 u64 each, R16)
+    uint64_t n_total = 0;  // keys of the whole build (0 = n): routed shards hold only their own keys
 };
 
 struct BuildOutput {
@@ -33,7 +34,7 @@ struct BuildOutput {
 };
 
 // ---- shards (multi-GPU / virtual shards), DESIGN.md section 13
-enum { SUM_KEYS = 0, SUM_BITS = 1, SUM_MINB = 2, SUM_B0 = 3, SUM_B1 = 4, SUM_DUP = 5, SUM_ERR = 6 };
+enum { SUM_KEYS = 0, SUM_BITS = 1, SUM_MINB = 2, SUM_B0 = 3, SUM_B1 = 4, SUM_DUP = 5, SUM_ERR = 6, SUM_NTOT = 7 };
 
 struct Globals {
     uint64_t n = 0, D = 0, dC = 0, beta = 0, key_base = 0, bit_base = 0, UC = 0, UP = 0;
@@ -69,6 +70,12 @@ class Shard {
 
 // OR all parts' slices into the serialized MPHF
 void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::vector<uint8_t>& blob);
+
+// SURVEY 8(e)(ii) key routing: group n device keys by the rank owning their bucket in a
+// build of `total` keys over `world` ranks (B = ceil(total / bucket)); d_out gets the keys
+// rank by rank, counts[r] (host) the number for rank r.  Synchronises st.
+void route_keys(const uint64_t* d_keys, uint64_t n, uint64_t total, uint32_t bucket, uint64_t g, uint32_t world,
+                cudaStream_t st, uint64_t* d_out, uint64_t* counts);
 
 // string keys (R16): master hash codes of data[off[i] .. off[i+1]) into mhc (2 u64 per key)
 void launch_mhc_strings(const uint8_t* data, const uint64_t* off, uint64_t n, uint64_t g, uint64_t* mhc,

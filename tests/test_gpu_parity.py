@@ -310,7 +310,56 @@ def test_shard_protocol_in_process():
     assert rs.stitch(parts) == rs.build(keys, 12, 1000) == oracle.build(keys, 12, 1000, threads=os.cpu_count())
 
 
-def _sharded_worker(rank, world, port, q):
+@pytest.mark.parametrize("n,leaf,b,world", [(60_000, 12, 1000, 3), (200_000, 8, 100, 5), (50, 8, 100, 3),
+                                            (7_000, 16, 2000, 8)])
+def test_routed_shard_protocol_in_process(n, leaf, b, world):
+    """SURVEY 8(e)(ii) in one process: each simulated rank routes its slice of the input
+    (recsplit_route_keys), a local all-to-all hands every rank exactly its keys, the shards
+    run with total_keys = n; the stitched bytes equal the single-GPU build (and the
+    oracle's).  (50 keys, b = 100: one bucket, so two of three ranks own nothing.)"""
+    import torch
+    keys = synth.keys(n, 5 + world)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    sl = [kt[r * n // world:(r + 1) * n // world] for r in range(world)]
+    routed = [rs.route_keys(x, n, b, world) for x in sl]
+    owned = []
+    for dst in range(world):
+        segs = []
+        for src in range(world):
+            out, cnt = routed[src]
+            st = sum(cnt[:dst])
+            segs.append(out[st:st + cnt[dst]])
+        owned.append(torch.cat(segs).contiguous())
+    assert sum(o.numel() for o in owned) == n
+    shards = [rs.Shard(owned[r], leaf, b, r, world, total_keys=n) for r in range(world)]
+    allsum = np.stack([s.summary for s in shards])
+    step = min(s.min_step(allsum) for s in shards)
+    parts = [s.finish(step) for s in shards]
+    for s in shards:
+        s.close()
+    blob = rs.stitch(parts)
+    assert blob == rs.build(keys, leaf, b)
+    if n <= 60_000:
+        assert blob == oracle.build(keys, leaf, b, threads=os.cpu_count())
+
+
+def test_misrouted_keys_rejected():
+    """A shard given keys it does not own (total_keys set) fails the build's key count."""
+    import torch
+    keys = synth.keys(20_000, 9)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    world = 2
+    shards = [rs.Shard(kt[: 10_000] if r == 0 else kt[10_000:], 8, 100, r, world, total_keys=20_000)
+              for r in range(world)]
+    allsum = np.stack([s.summary for s in shards])
+    with pytest.raises(rs.RecSplitError) as e:
+        shards[0].min_step(allsum)
+    assert e.value.code == rs.E_INVALID
+    for s in shards:
+        s.close()
+
+
+def _sharded_worker(rank, world, port, q, distribute=False):
     import sys as _sys
     _sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
@@ -325,21 +374,25 @@ def _sharded_worker(rank, world, port, q):
     try:
         keys = synth_.keys(200_000, 12)
         kt = torch.from_numpy(keys.view(np.int64)).cuda()
-        blob = rs_.build_sharded(kt, 12, 1000)
+        if distribute:  # each rank starts from its own half of the input
+            kt = kt[rank * 100_000:(rank + 1) * 100_000].contiguous()
+        blob = rs_.build_sharded(kt, 12, 1000, distribute=distribute)
         if rank == 0:
             q.put(blob == rs_.build(keys, 12, 1000))
     finally:
         dist.destroy_process_group()
 
 
-def test_build_sharded_two_ranks_gloo():
-    """build_sharded over torch.distributed (2 ranks on one GPU, gloo collectives):
-    same bytes as the single-GPU build."""
+@pytest.mark.parametrize("distribute", [False, True])
+def test_build_sharded_two_ranks_gloo(distribute):
+    """build_sharded over torch.distributed (2 ranks on one GPU, gloo collectives), with
+    every rank holding all keys or with routed slices (all-to-all): same bytes as the
+    single-GPU build."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 30500 + os.getpid() % 1000
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    port = 30500 + os.getpid() % 1000 + 7 * distribute
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q, distribute)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
