@@ -53,6 +53,7 @@ struct Args {
     u32 batch;     // nodes per cursor atomic in batch mode
     u32 cp_l1;     // early-rejection checkpoint (key groups of 4) for full lower-level-1 nodes, 0 = off
     u32 cp_l2;     // same for full lower-level-2 nodes
+    u32 cp_leaf;   // leaves: early rejection on (0 = off)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -240,11 +241,12 @@ __device__ __forceinline__ u32 count_left(const KeysView& K, u32 s, u32 sigma, u
 // Leaf masks over all groups: a = OR of 2^{remap(h, m)} over A keys, b over B keys
 // (padding keys have mA = mB = 0).
 template <int MODE>
-__device__ __forceinline__ void leaf_masks(const KeysView& K, u32 ng, u32 m, u32 base, u32& a, u32& b) {
-    u32 a0 = 0, b0 = 0;
-    const u32* __restrict__ g = K.G;
+__device__ __forceinline__ void leaf_masks(const KeysView& K, u32 ng, u32 m, u32 base, u32& a, u32& b, u32 q0 = 0,
+                                           u32 a_init = 0, u32 b_init = 0) {
+    u32 a0 = a_init, b0 = b_init;
+    const u32* __restrict__ g = K.G + 20 * q0;
 #pragma unroll 1
-    for (u32 q = 0; q < ng; ++q, g += 20) {
+    for (u32 q = q0; q < ng; ++q, g += 20) {
         u32 h[4];
         hash4<MODE>(g, base, h, K.H);
         const uint4 ma = *reinterpret_cast<const uint4*>(g + 12);
@@ -381,6 +383,11 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
         }
         if (valid) mg = ~(u32)k;
         c.full = (1u << s) - 1u;
+        // early rejection checkpoint (key groups): a fit needs no collision inside A or B, so
+        // a base seed whose first 4*cp keys already collide fails; best measured-by-simulation
+        // checkpoints: 8 keys for m = 10..19, 12 keys for m = 20..24
+        c.cp = A.cp_leaf && s >= 10 ? (s < 20 ? 2u : 3u) : 0u;
+        c.kW = 0;
     } else {
         for (u32 j = lane; j < s; j += 32) {
             const u64 k = A.lo[rec.key_off + j];
@@ -542,6 +549,72 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
     return false;
 }
 
+// Early rejection with warp compaction for leaves (no-carry path): stage 1 ORs the masks
+// of the first 4*c.cp keys (full groups) for 32 base seeds; a seed whose partial masks show a
+// collision (popc(a) + popc(b) < keys so far) cannot fit (P:252 pruning, applied early).
+// Survivors queue in seed order with their partial masks; stage 2 completes 32 of them and
+// runs the fit (rotation fitting: lowest lane with a fit and its smallest r; brute force:
+// a == full).  Every other seed of the window failed, so the first hit is the window's minimum.
+template <int KIND>
+__device__ __forceinline__ bool run_window_leaf_cp(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
+                                                   u32 lane, u32* qs, u32* qa, u32* qb, u64* val) {
+    const u32 wrel = (u32)(wstart - c.kW);
+    const u32 ng = (c.s + 3) >> 2, k1 = 4 * c.cp;
+    const u32 lt = lanemask_lt();
+    u32 qn = 0;
+    for (u32 it = 0; it <= A.iters; ++it) {
+        if (it < A.iters) {
+            const u32 sig = wrel + it * 32 + lane;
+            u32 a, b;
+            leaf_masks<0>(K, c.cp, c.s, KIND == SK_LEAF_RF ? sig * c.s : sig, a, b);
+            const bool keep = (u32)(__popc(a) + __popc(b)) == k1;
+            const u32 bal = __ballot_sync(FULL, keep);
+            if (keep) {
+                const u32 pos = qn + __popc(bal & lt);
+                qs[pos] = sig;
+                qa[pos] = a;
+                qb[pos] = b;
+            }
+            qn += __popc(bal);
+            __syncwarp();
+            if (qn < 32) continue;
+        } else if (qn == 0) {
+            break;
+        }
+        const bool have = lane < qn;
+        const u32 sig = have ? qs[lane] : 0;
+        u32 a = have ? qa[lane] : 0, b = have ? qb[lane] : 0;
+        leaf_masks<0>(K, ng, c.s, KIND == SK_LEAF_RF ? sig * c.s : sig, a, b, c.cp, a, b);
+        if (!have) a = b = 0;  // no entry: cannot fit (m >= 10 keys)
+        int r = 0;
+        const bool ok = KIND == SK_LEAF_BF ? a == c.full : fit_rotation_warp(a, b, c.s, c.full, lane, r);
+        const u32 bal = __ballot_sync(FULL, ok);
+        if (bal) {
+            const int win = __ffs(bal) - 1;
+            const u64 k = c.kW + __shfl_sync(FULL, sig, win);
+            *val = KIND == SK_LEAF_RF ? k * c.s + (u32)__shfl_sync(FULL, r, win) : k;
+            return true;
+        }
+        __syncwarp();
+        const u32 rest = qn > 32 ? qn - 32 : 0;
+        u32 x = 0, y = 0, z = 0;
+        if (lane < rest) {
+            x = qs[32 + lane];
+            y = qa[32 + lane];
+            z = qb[32 + lane];
+        }
+        __syncwarp();
+        if (lane < rest) {
+            qs[lane] = x;
+            qa[lane] = y;
+            qb[lane] = z;
+        }
+        __syncwarp();
+        qn = rest;
+    }
+    return false;
+}
+
 template <int KIND, int VAR>
 __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, NodeCtx& c, u64 wstart,
                                            u32 lane, u64* val, u32* qs, u32* qc) {
@@ -560,6 +633,8 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, Nod
         if (VAR == V_CP && KIND == SK_LOWER && c.cp)
             return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, qc, val)
                         : run_window_cp<0>(A, K, c, wstart, lane, qs, qc, val);
+        if (VAR == V_CP && (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) && c.cp)
+            return run_window_leaf_cp<KIND>(A, K, c, wstart, lane, qs, qc, qc + 64, val);
         for (u32 it = 0; it < A.iters; ++it) {
             int r = 0;
             const bool ok = trial_fast<KIND, 0, VAR == V_WIDE>(K, c, wrel + it * 32 + lane, lane, r);
@@ -637,10 +712,10 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     const u32 cap = A.warp_cap;                    // keys (multiple of 4)
     const u32 gwords = GW * (cap / 4 + 1);         // key groups
     const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
-    u32* G = smem32 + (size_t)wib * (gwords + twords + 128);
+    u32* G = smem32 + (size_t)wib * (gwords + twords + 192);
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
-    u32* QS = G + gwords + twords;  // early-rejection queue: seeds, partial counters (64 each)
-    u32* QC = QS + 64;
+    u32* QS = G + gwords + twords;  // early-rejection queue (64 entries): seeds, partial counters
+    u32* QC = QS + 64;              // (splits) or partial masks a, b (leaves)
     const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
     if (KIND == SK_LOWER) {  // shift tables of full nodes: part p -> p*w (p < f-1), 32 for the last
         for (u32 t = threadIdx.x; t < 64; t += blockDim.x) {
@@ -759,13 +834,15 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         static const int cp2 = getenv("RS_CP2") ? atoi(getenv("RS_CP2")) : 940;
         A.cp_l1 = (u32)((u64)P.u1 * cp1 / 4000);
         A.cp_l2 = (u32)((u64)P.u2 * cp2 / 4000);
+        static const int cpl = getenv("RS_CPL") ? atoi(getenv("RS_CPL")) : 1;
+        A.cp_leaf = cpl ? 1u : 0u;
     }
     // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
     const u32 GW = (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) ? 20 : 12;
-    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + 128) * sizeof(u32);
+    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + 192) * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;
@@ -805,8 +882,18 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
                 launch_kind<SK_LOWER>(P, A, wpb, smem, grid, st);
             break;
         }
-        case SK_LEAF_RF: launch_kind<SK_LEAF_RF>(P, A, wpb, smem, grid, st); break;
-        case SK_LEAF_BF: launch_kind<SK_LEAF_BF>(P, A, wpb, smem, grid, st); break;
+        case SK_LEAF_RF:
+            if (A.cp_leaf && P.max_size >= 10)
+                launch_kind<SK_LEAF_RF, V_CP>(P, A, wpb, smem, grid, st);
+            else
+                launch_kind<SK_LEAF_RF>(P, A, wpb, smem, grid, st);
+            break;
+        case SK_LEAF_BF:
+            if (A.cp_leaf && P.max_size >= 10)
+                launch_kind<SK_LEAF_BF, V_CP>(P, A, wpb, smem, grid, st);
+            else
+                launch_kind<SK_LEAF_BF>(P, A, wpb, smem, grid, st);
+            break;
     }
     g_launches++;
 }
