@@ -57,7 +57,7 @@ struct PhaseLaunch {
     const u8* ab;
     u64* values;    // by slot; initialised to ~0
     u32* next_win;  // by slot; initialised to 0
-    u32* cursor;    // zeroed
+    u32* cursor;    // two zeroed counters: batch-mode cursor, tail (help-mode) cursor
     int* active;    // n_warps entries, set to -1
     u32* err;
     const u32* dup;  // nonzero: duplicate keys, searches return immediately

@@ -384,10 +384,10 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     u32* pcnt_d = A.alloc<u32>(NP + 32);
     const u32 nslots = search_active_slots(sms);
     int* active = A.alloc<int>(nslots);
-    u32* cursors = A.alloc<u32>(NP + 1);
+    u32* cursors = A.alloc<u32>(2 * NP + 2);  // two per phase: batch cursor, tail (help) cursor
     CK(cudaMemsetAsync(values_d, 0xff, total_nodes * 8, st));
     CK(cudaMemsetAsync(next_win, 0, total_nodes * 4, st));
-    CK(cudaMemsetAsync(cursors, 0, (NP + 1) * 4, st));
+    CK(cudaMemsetAsync(cursors, 0, (2 * NP + 2) * 4, st));
     std::vector<u32> pc32(NP);
     for (uint32_t q = 0; q < NP; ++q) pc32[q] = (u32)pcount[q];
     CK(cudaMemcpyAsync(pcnt_d, pc32.data(), NP * 4, cudaMemcpyHostToDevice, st));
@@ -437,7 +437,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
         P.ab = ab_a;
         P.values = values_d;
         P.next_win = next_win;
-        P.cursor = cursors + q;
+        P.cursor = cursors + 2 * q;
         P.active = active;
         P.err = small + 4;
         P.dup = small + 2;
@@ -839,7 +839,7 @@ static void search_nodes_host(const uint64_t* lo, const uint8_t* isb, const uint
         CK(cudaMemcpy(d_nodes, groups[g].data(), groups[g].size() * sizeof(rsd::NodeRec), cudaMemcpyHostToDevice));
         u32 cnt = (u32)groups[g].size();
         CK(cudaMemcpy(small + 6, &cnt, 4, cudaMemcpyHostToDevice));
-        CK(cudaMemset(small, 0, 4));
+        CK(cudaMemset(small, 0, 8));  // batch and tail cursors
         CK(cudaMemset(active, 0xff, nslots * 4));
         PhaseLaunch P{};
         P.kind = mode == 1 ? SK_LEAF_RF : mode == 2 ? SK_LEAF_BF : (g == 0 ? SK_UPPER : SK_LOWER);

@@ -51,6 +51,7 @@ struct Args {
     u32 warp_cap;
     int help;
     u32 batch;     // nodes per cursor atomic in batch mode
+    u32 tail;      // batch mode: the last `tail` nodes run in help mode (no straggler batches)
     u32 cp_l1;     // early-rejection checkpoint (key groups of 4) for full lower-level-1 nodes, 0 = off
     u32 cp_l2;     // same for full lower-level-2 nodes
     u32 cp_leaf;   // leaves: early rejection on (0 = off)
@@ -128,6 +129,8 @@ enum { V_PLAIN = 0, V_CP = 1, V_WIDE = 2 };
 // index 0 = lower level 1 (f1 parts of l), 1 = lower level 2 (f2 parts of u1).  Static
 // shared arrays have link-time addresses, so the lookup is LDS [part + imm].
 __shared__ u8 s_full_tab[2][32];
+// early-rejection masks of the two full classes: {me, ke, ce, mo, ko, co} (run_window_cp)
+__shared__ u32 s_cp_masks[2][6];
 
 // increment 1 << s_full_tab[c][remap(h, f)]
 template <int CL>
@@ -453,7 +456,7 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
 // v - kW on lo + kW, so a window of large values becomes a window of small ones and stays
 // on the no-carry path (a window of span <= margin never carries).
 template <u32 GW>
-__device__ __noinline__ void rebase_keys(u32* G, u32 s, u64 delta, u32 lane, u32& margin) {
+__device__ __forceinline__ void rebase_keys(u32* G, u32 s, u64 delta, u32 lane, u32& margin) {
     __syncwarp();
     u32 mg = FULL;
     for (u32 j = lane; j < s; j += 32) {
@@ -486,22 +489,9 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
     const u32 wrel = (u32)(wstart - c.kW);  // window start relative to the key rebase
     // packed "some field > unit" test: ((cnt & me) + ke) & ce | ((cnt & mo) + ko) & co, fields
     // 0..f-2 split into even and odd ones so that the added carries stay inside a field gap
-    u32 me = 0, mo = 0, ke = 0, ko = 0, ce = 0, co = 0;
-    {
-        const u32 fm = (1u << c.w) - 1, kadd = fm - c.unit;  // field + kadd >= 2^w <=> field > unit
-        for (u32 j = 0; j + 1 < c.f; ++j) {
-            const u32 sh = j * c.w;
-            if (j & 1) {
-                mo |= fm << sh;
-                ko |= kadd << sh;
-                co |= 1u << (sh + c.w);
-            } else {
-                me |= fm << sh;
-                ke |= kadd << sh;
-                ce |= 1u << (sh + c.w);
-            }
-        }
-    }
+    // (class constants, filled at kernel start)
+    const u32 me = s_cp_masks[CL][0], ke = s_cp_masks[CL][1], ce = s_cp_masks[CL][2];
+    const u32 mo = s_cp_masks[CL][3], ko = s_cp_masks[CL][4], co = s_cp_masks[CL][5];
     const u32 lt = lanemask_lt();
     u32 qn = 0;
     for (u32 it = 0; it <= A.iters; ++it) {
@@ -723,6 +713,28 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             const u32 unit = cl ? A.u1 : A.leaf, f = cl ? A.u2 / A.u1 : A.u1 / A.leaf;
             const u32 w = 32 - __clz(unit + 1);
             s_full_tab[cl][p] = (u8)part_shift(p, f, w);
+            if (p == 0) {
+                u32 me = 0, ke = 0, ce = 0, mo = 0, ko = 0, co = 0;
+                const u32 fm = (1u << w) - 1, kadd = fm - unit;  // field + kadd >= 2^w <=> field > unit
+                for (u32 j = 0; j + 1 < f && (j + 1) * w <= 32; ++j) {
+                    const u32 sh = j * w, cb = (j + 1) * w < 32 ? 1u << (sh + w) : 0u;
+                    if (j & 1) {
+                        mo |= fm << sh;
+                        ko |= kadd << sh;
+                        co |= cb;
+                    } else {
+                        me |= fm << sh;
+                        ke |= kadd << sh;
+                        ce |= cb;
+                    }
+                }
+                s_cp_masks[cl][0] = me;
+                s_cp_masks[cl][1] = ke;
+                s_cp_masks[cl][2] = ce;
+                s_cp_masks[cl][3] = mo;
+                s_cp_masks[cl][4] = ko;
+                s_cp_masks[cl][5] = co;
+            }
         }
         __syncthreads();
     }
@@ -731,14 +743,18 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     const u64 ws = 32ull * A.iters;
     NodeCtx c{};
 
+    u32 hbase = 0;  // help mode covers nodes [hbase, nn)
     if (!A.help) {
-        // batch mode: A.batch nodes per cursor atomic, each searched alone
+        // batch mode: A.batch nodes per cursor atomic, each searched alone, for all but the
+        // last A.tail nodes; those then run in help mode so that no warp is left with a
+        // straggler batch while the others idle
+        hbase = nn > A.tail ? nn - A.tail : 0;
         for (;;) {
             u32 n0 = 0;
             if (lane == 0) n0 = atomicAdd(A.cursor, A.batch);
             n0 = __shfl_sync(FULL, n0, 0);
-            if (n0 >= nn) break;
-            const u32 n1 = min(n0 + A.batch, nn);
+            if (n0 >= hbase) break;
+            const u32 n1 = min(n0 + A.batch, hbase);
             for (u32 n = n0; n < n1; ++n) {
                 load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c);
                 u64 val = 0;
@@ -754,15 +770,16 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                 __syncwarp();
             }
         }
-        return;
+        if (A.tail == 0) return;
     }
 
     // help mode: per-node window dispenser + helping
+    u32* const hcursor = A.help ? A.cursor : A.cursor + 1;
     u32 node = NONE;
     for (;;) {
         if (node == NONE) {
             u32 n = 0;
-            if (lane == 0) n = atomicAdd(A.cursor, 1u);
+            if (lane == 0) n = hbase + atomicAdd(hcursor, 1u);
             n = __shfl_sync(FULL, n, 0);
             if (n >= nn) {
                 n = find_help(A, gw, lane, nn);
@@ -864,6 +881,10 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         u64 b = P.n_nodes_host / (slots * 8);
         A.batch = (u32)std::max<u64>(1, std::min<u64>(8, b));
         grid = std::min<u32>(grid, (P.n_nodes_host + A.batch * wpb - 1) / (A.batch * wpb));
+    }
+    {
+        static const int tl = getenv("RS_TAIL") ? atoi(getenv("RS_TAIL")) : 0;  // x resident warps (off: measured slower)
+        A.tail = P.help ? 0u : (u32)tl * grid * wpb;
     }
     if (grid == 0) grid = 1;
     A.n_warps = grid * wpb;
