@@ -168,10 +168,15 @@ __device__ __forceinline__ u32 shl_clamp(u32 x, u32 s) {
     return r;
 }
 
-// 1 << s with clamping (s >= 32 gives 0), immediate source operand
+// 1 << s with clamping (s >= 32 gives 0): a one-bit mask at position s (BMSK with an
+// immediate width, so no register has to hold the constant 1)
 __device__ __forceinline__ u32 bit_clamp(u32 s) {
     u32 r;
+#if RS_BITCLAMP_SHL
     asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(s));
+#else
+    asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(r) : "r"(s));
+#endif
     return r;
 }
 

@@ -128,13 +128,14 @@ enum { V_PLAIN = 0, V_CP = 1, V_WIDE = 2 };
 // Block-wide shift tables of the FULL lower-level nodes of a phase (all share f and w):
 // index 0 = lower level 1 (f1 parts of l), 1 = lower level 2 (f2 parts of u1).  Static
 // shared arrays have link-time addresses, so the lookup is LDS [part + imm].
-__shared__ u8 s_full_tab[2][32];
+__shared__ __align__(16) u8 s_full_tab[2][32];
 // early-rejection masks of the two full classes: {me, ke, ce, mo, ko, co} (run_window_cp)
 __shared__ u32 s_cp_masks[2][6];
 
 // increment 1 << s_full_tab[c][remap(h, f)]
 template <int CL>
 __device__ __forceinline__ u32 inc_full(u32 h, u32 f) { return bit_clamp(s_full_tab[CL][__umulhi(h, f)]); }
+
 
 // increment 1 << table[remap(h, r)]: the byte address comes straight out of mad.hi
 // (hi(h * r) + table base), the shift amount is >= 32 for the last part (adds 0).
