@@ -19,6 +19,11 @@
  *                                    query-semantics search, statistics)
  *   build / encode / EF / query .... pinned (exhaustive bijectivity, decode
  *                                    round trip, bits/object vs paper)
+ *   mhc_string (reading R16) ....... an invented definition (the paper names no
+ *                                    string hash): pinned by properties only
+ *                                    (no collisions on 2e4 strings, length and
+ *                                    seed sensitivity, balanced A/B bit) --
+ *                                    parity unpinned against the paper
  *   seed values themselves ......... parity unpinned against the paper (no
  *                                    worked example exists); pinned only by the
  *                                    definitions above.
