@@ -248,18 +248,22 @@ def _subtree_nodes(leaf):
 
 
 @pytest.mark.slow
-def test_c3_sampled_bucket_parity_and_properties():
-    """C3 at full size (n=5e6, l=16, b=2000) as bench.py builds it: the values of
-    sampled buckets equal the oracle's, the MPHF is bijective, bits/object ~ 1.560
-    (P:581)."""
-    cfg = synth.CONFIGS["C3"]
+@pytest.mark.parametrize("name,bits,tol", [("C3", 1.560, 0.004), ("C5", 1.6208, 0.004)])
+def test_full_size_sampled_bucket_parity_and_properties(name, bits, tol):
+    """C3 (n=5e6, l=16, b=2000) and C5 (n=1e8, l=12, b=1000) at full size, as bench.py
+    builds them: the values of sampled buckets (incl. the largest) equal the oracle's, the
+    MPHF is bijective (GPU query + GPU bijectivity check), bits/object matches the paper
+    (C3: 1.560) or the survey's model of this format (C5: 1.6208)."""
+    import torch
+    cfg = synth.CONFIGS[name]
     keys = synth.keys(cfg["n"], cfg["seed"])
     leaf, b = cfg["leaf"], cfg["bucket"]
     blob, vals = rs.build_values(keys, leaf, b)
-    q = rs.query_many(blob, keys)
-    assert np.array_equal(np.sort(q), np.arange(len(keys), dtype=np.uint64))
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    assert rs.check_bijective_device(rs.query_device(blob, kt)) == 0
+    del kt
     bpk = rs.bits_per_key(blob)
-    assert abs(bpk - 1.560) < 0.004, bpk
+    assert abs(bpk - bits) < tol, bpk
     hi, _ = _mhc_np(keys)
     B = (len(keys) + b - 1) // b
     bucket = ((hi >> np.uint64(32)) * np.uint64(B)) >> np.uint64(32)
