@@ -288,7 +288,12 @@ def main():
     evals = float(np.mean([s["algo_evals"][cls] for s in stats]))
     kt_s = float(np.mean([s["t_search"][cls] for s in stats]))
     peaks = _peaks()
-    max_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if "sm_max_mhz" in peaks:
+        max_mhz, mhz_src = float(peaks["sm_max_mhz"]), "MEASURED_PEAKS sm_max_mhz"
+    elif clocks.get("sm_max_mhz"):
+        max_mhz, mhz_src = float(clocks["sm_max_mhz"]), "nvidia-smi clocks.max.sm during the run"
+    else:
+        max_mhz, mhz_src = 1965.0, "fallback: B200 max SM clock"
     peak = int32_peak_evals(sms, max_mhz) / 1e9
     achieved = evals / kt_s / 1e9
     traffic = None
@@ -315,7 +320,7 @@ def main():
         "roofline": {"bound": "alu", "kernel": "k_search<SK_LOWER> (lower level 1 splits)",
                      "achieved": achieved, "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
                      "traffic": traffic,
-                     "peak_note": f"{sms} SMs x {max_mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz) x 6.10 evals/clk/SM"},
+                     "peak_note": f"{sms} SMs x {max_mhz:.0f} MHz ({mhz_src}) x 6.10 evals/clk/SM"},
         "phases_s": {"partition": st0["t_partition"], "tree": st0["t_tree"], "upper": st0["t_search"][0],
                      "lower2": st0["t_search"][1], "lower1": st0["t_search"][2], "leaves": st0["t_search"][3],
                      "reorder": st0["t_reorder"], "encode": st0["t_encode"], "d2h": st0["t_d2h"]},

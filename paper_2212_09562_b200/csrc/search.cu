@@ -55,6 +55,7 @@ struct Args {
     u32 cp_l1;     // early-rejection checkpoint (key groups of 4) for full lower-level-1 nodes, 0 = off
     u32 cp_l2;     // same for full lower-level-2 nodes
     u32 cp_leaf;   // leaves: early rejection on (0 = off)
+    u32 cp_last;   // full lower nodes: also reject when the last part already overflows (0 = off)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -129,8 +130,10 @@ enum { V_PLAIN = 0, V_CP = 1, V_WIDE = 2 };
 // index 0 = lower level 1 (f1 parts of l), 1 = lower level 2 (f2 parts of u1).  Static
 // shared arrays have link-time addresses, so the lookup is LDS [part + imm].
 __shared__ __align__(16) u8 s_full_tab[2][32];
-// early-rejection masks of the two full classes: {me, ke, ce, mo, ko, co} (run_window_cp)
-__shared__ u32 s_cp_masks[2][6];
+// early-rejection constants of the two full classes (run_window_cp): {me, ke, ce, mo, ko, co}
+// for the "some field > unit" test, then {Me, Mo, tope | topo << 8 | w << 16, thr} for the
+// last-part test (sum of fields 0..f-2 < thr = keys so far - unit; thr = 0: off)
+__shared__ u32 s_cp_masks[2][10];
 
 // increment 1 << s_full_tab[c][remap(h, f)]
 template <int CL>
@@ -493,13 +496,21 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
     // (class constants, filled at kernel start)
     const u32 me = s_cp_masks[CL][0], ke = s_cp_masks[CL][1], ce = s_cp_masks[CL][2];
     const u32 mo = s_cp_masks[CL][3], ko = s_cp_masks[CL][4], co = s_cp_masks[CL][5];
+    const u32 Me = s_cp_masks[CL][6], Mo = s_cp_masks[CL][7], tops = s_cp_masks[CL][8], thr = s_cp_masks[CL][9];
+    const u32 tope = tops & 0xff, topo = (tops >> 8) & 0xff, fw = tops >> 16;
+    const u32 m2w = (1u << (2 * fw)) - 1u;
     const u32 lt = lanemask_lt();
     u32 qn = 0;
     for (u32 it = 0; it <= A.iters; ++it) {
         if (it < A.iters) {
             const u32 sig = wrel + it * 32 + lane;
             const u32 cnt = count_lower<0, CL, false>(K, c.s, sig, c.r, 0, c.cp);
-            const bool rej = ((((cnt & me) + ke) & ce) | (((cnt & mo) + ko) & co)) != 0;
+            // the last part (not held in the counter) overflows iff the fields' sum is below
+            // keys-so-far - unit; the sum of the even / odd fields is one coefficient of a
+            // product with a spread multiplier (partial sums < 2^{2w}: no carries between them)
+            const u32 se = (u32)(((u64)(cnt & me) * Me) >> tope) & m2w;
+            const u32 so = (u32)(((u64)((cnt & mo) >> fw) * Mo) >> topo) & m2w;
+            const bool rej = ((((cnt & me) + ke) & ce) | (((cnt & mo) + ko) & co)) != 0 || se + so < thr;
             const u32 bal = __ballot_sync(FULL, !rej);
             if (!rej) {
                 const u32 pos = qn + __popc(bal & lt);
@@ -735,6 +746,19 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                 s_cp_masks[cl][3] = mo;
                 s_cp_masks[cl][4] = ko;
                 s_cp_masks[cl][5] = co;
+                // last-part test: Me / Mo = sum over the even / odd fields i of 2^{2 w i'} (i' = the
+                // field's rank among them); valid while the keys counted so far stay < 2^{2w}
+                u32 ne = 0, no = 0, Me = 0, Mo = 0;
+                for (u32 j = 0; j + 1 < f && (j + 1) * w <= 32; ++j) {
+                    if (j & 1) Mo |= 1u << (2 * w * no++);
+                    else Me |= 1u << (2 * w * ne++);
+                }
+                const u32 kcp = 4 * (cl ? A.cp_l2 : A.cp_l1);
+                const bool ok = 2 * w < 32 && kcp < (1u << (2 * w)) && kcp > unit && (f - 1) * w <= 31;
+                s_cp_masks[cl][6] = Me;
+                s_cp_masks[cl][7] = Mo;
+                s_cp_masks[cl][8] = (ne ? 2 * w * (ne - 1) : 0) | (no ? 2 * w * (no - 1) : 0) << 8 | w << 16;
+                s_cp_masks[cl][9] = ok && A.cp_last ? kcp - unit : 0u;
             }
         }
         __syncthreads();
@@ -854,6 +878,8 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         A.cp_l2 = (u32)((u64)P.u2 * cp2 / 4000);
         static const int cpl = getenv("RS_CPL") ? atoi(getenv("RS_CPL")) : 1;
         A.cp_leaf = cpl ? 1u : 0u;
+        static const int cplast = getenv("RS_CPLAST") ? atoi(getenv("RS_CPLAST")) : 1;
+        A.cp_last = cplast ? 1u : 0u;
     }
     // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
