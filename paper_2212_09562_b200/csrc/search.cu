@@ -54,6 +54,8 @@ struct Args {
     u32 tail;      // batch mode: the last `tail` nodes run in help mode (no straggler batches)
     u32 cp_l1;     // early-rejection checkpoint (key groups of 4) for full lower-level-1 nodes, 0 = off
     u32 cp_l2;     // same for full lower-level-2 nodes
+    u32 cp_l1b;    // second checkpoints (key groups; off unless above the first)
+    u32 cp_l2b;
     u32 cp_leaf;   // leaves: early rejection on (0 = off)
     u32 cp_last;   // full lower nodes: also reject when the last part already overflows (0 = off)
 };
@@ -132,8 +134,9 @@ enum { V_PLAIN = 0, V_CP = 1, V_WIDE = 2 };
 __shared__ __align__(16) u8 s_full_tab[2][32];
 // early-rejection constants of the two full classes (run_window_cp): {me, ke, ce, mo, ko, co}
 // for the "some field > unit" test, then {Me, Mo, tope | topo << 8 | w << 16, thr} for the
-// last-part test (sum of fields 0..f-2 < thr = keys so far - unit; thr = 0: off)
-__shared__ u32 s_cp_masks[2][10];
+// last-part test (sum of fields 0..f-2 < thr = keys so far - unit; thr = 0: off), then thr of
+// the second checkpoint
+__shared__ u32 s_cp_masks[2][11];
 
 // increment 1 << s_full_tab[c][remap(h, f)]
 template <int CL>
@@ -298,6 +301,7 @@ struct NodeCtx {
     u32 l2;  // lower level 2 node (s > u1)
     u64 target64, mask64;
     u32 cp;  // early rejection (full lower nodes): checkpoint in key groups, 0 = off
+    u32 cp2; // second checkpoint (key groups), 0 = single stage
     u64 kW;  // key rebase: the buffered keys are lo + kW (values are tried relative to kW)
 };
 
@@ -425,6 +429,8 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
             c.l2 = s > A.u1;
             const u32 cpg = c.l2 ? A.cp_l2 : A.cp_l1;
             c.cp = c.full && cpg < (s >> 2) && (f - 1) * w <= 31 ? cpg : 0;
+            const u32 cpg2 = c.l2 ? A.cp_l2b : A.cp_l1b;
+            c.cp2 = c.cp && cpg2 >= cpg + 2 && cpg2 < (s >> 2) ? cpg2 : 0;  // a 1-group stage does not pay
             if (!c.wide) {
                 u32 t = 0;
                 for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
@@ -477,76 +483,118 @@ __device__ __forceinline__ void rebase_keys(u32* G, u32 s, u64 delta, u32 lane, 
     __syncwarp();
 }
 
+// Early rejection of a full class CL (run_window_cp): true if a seed whose packed counter
+// after the first keys is cnt cannot succeed: a field of parts 0..f-2 above unit
+// (((cnt & me) + ke) & ce | ((cnt & mo) + ko) & co, even and odd fields apart so that the
+// added carries stay inside a field gap), or the last part (not held in the counter) above
+// unit, i.e. the fields' sum below thr = keys so far - unit; the sum of the even / odd fields
+// is one coefficient of a product with a spread multiplier (partial sums < 2^{2w}: no carries
+// between the coefficients).  The class constants are read from shared memory at the test
+// (once per seed) so that they hold no registers across the counting loops.
+template <int CL>
+__device__ __forceinline__ bool cp_reject(u32 cnt, int ti) {
+    const volatile u32* m = s_cp_masks[CL];
+    const u32 me = m[0], mo = m[3], tops = m[8];
+    const u32 fw = tops >> 16, m2w = (1u << (2 * fw)) - 1u;
+    const u32 se = (u32)(((u64)(cnt & me) * m[6]) >> (tops & 0xff)) & m2w;
+    const u32 so = (u32)(((u64)((cnt & mo) >> fw) * m[7]) >> ((tops >> 8) & 0xff)) & m2w;
+    return ((((cnt & me) + m[1]) & m[2]) | (((cnt & mo) + m[4]) & m[5])) != 0 || se + so < m[ti];
+}
+
+// drop the first nb entries of a warp queue of qn (<= 64) entries (seeds, counters)
+__device__ __forceinline__ void queue_pop(u32* qs, u32* qc, u32& qn, u32 nb, u32 lane) {
+    const u32 rest = qn - nb;  // <= 32
+    u32 a = 0, b = 0;
+    __syncwarp();
+    if (lane < rest) {
+        a = qs[nb + lane];
+        b = qc[nb + lane];
+    }
+    __syncwarp();
+    if (lane < rest) {
+        qs[lane] = a;
+        qc[lane] = b;
+    }
+    __syncwarp();
+    qn = rest;
+}
+
 // Search the window [wstart, wstart + 32*iters) of base values (seeds, or base seeds k for
 // RF) in order; on a hit returns true with the stored value in *val (warp-uniform).
-// Early rejection with warp compaction (full lower-level nodes, no-carry path).  Stage 1
-// counts the first c.cp key groups of 32 seeds; a seed whose packed counter already shows
-// a part above its target cannot succeed (a carry only happens when some count exceeds
-// 2^w - 1 > unit, so the test never rejects a valid seed).  Survivors go to a per-warp FIFO
-// queue in increasing seed order; whenever 32 are queued (and at the end of the window)
-// stage 2 finishes their counts over the remaining keys.  Survivors are completed in
-// increasing seed order and every other seed of the window was rejected, so the first
-// hit is the smallest successful seed of the window.
+// Early rejection with warp compaction (full lower-level nodes, no-carry path), a cascade of
+// up to two checkpoints.  Stage 1 counts the first c.cp key groups of 32 seeds; a seed that
+// CpTest rejects cannot succeed (a carry only happens when some count exceeds 2^w - 1 > unit,
+// so the test never rejects a valid seed).  Survivors go to a per-warp FIFO queue in
+// increasing seed order; whenever 32 are queued (and at the end of the window) the next stage
+// takes them: with a second checkpoint c.cp2, stage 2 counts groups [c.cp, c.cp2), tests again
+// and queues its survivors (in order) for stage 3, which finishes the counts over the
+// remaining keys; without it, stage 2 finishes them.  A batch is always the oldest entries of
+// its queue and a queue's entries are older than everything upstream, so survivors are
+// completed in increasing seed order; every other seed of the window was rejected, hence the
+// first hit is the smallest successful seed of the window.
 template <int CL>
 __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart, u32 lane,
-                                           u32* qs, u32* qc, u64* val) {
+                                           u32* qs, u64* val) {
     const u32 wrel = (u32)(wstart - c.kW);  // window start relative to the key rebase
-    // packed "some field > unit" test: ((cnt & me) + ke) & ce | ((cnt & mo) + ko) & co, fields
-    // 0..f-2 split into even and odd ones so that the added carries stay inside a field gap
-    // (class constants, filled at kernel start)
-    const u32 me = s_cp_masks[CL][0], ke = s_cp_masks[CL][1], ce = s_cp_masks[CL][2];
-    const u32 mo = s_cp_masks[CL][3], ko = s_cp_masks[CL][4], co = s_cp_masks[CL][5];
-    const u32 Me = s_cp_masks[CL][6], Mo = s_cp_masks[CL][7], tops = s_cp_masks[CL][8], thr = s_cp_masks[CL][9];
-    const u32 tope = tops & 0xff, topo = (tops >> 8) & 0xff, fw = tops >> 16;
-    const u32 m2w = (1u << (2 * fw)) - 1u;
-    const u32 lt = lanemask_lt();
-    u32 qn = 0;
-    for (u32 it = 0; it <= A.iters; ++it) {
-        if (it < A.iters) {
-            const u32 sig = wrel + it * 32 + lane;
-            const u32 cnt = count_lower<0, CL, false>(K, c.s, sig, c.r, 0, c.cp);
-            // the last part (not held in the counter) overflows iff the fields' sum is below
-            // keys-so-far - unit; the sum of the even / odd fields is one coefficient of a
-            // product with a spread multiplier (partial sums < 2^{2w}: no carries between them)
-            const u32 se = (u32)(((u64)(cnt & me) * Me) >> tope) & m2w;
-            const u32 so = (u32)(((u64)((cnt & mo) >> fw) * Mo) >> topo) & m2w;
-            const bool rej = ((((cnt & me) + ke) & ce) | (((cnt & mo) + ko) & co)) != 0 || se + so < thr;
-            const u32 bal = __ballot_sync(FULL, !rej);
-            if (!rej) {
-                const u32 pos = qn + __popc(bal & lt);
-                qs[pos] = sig;
-                qc[pos] = cnt;
-            }
-            qn += __popc(bal);
-            __syncwarp();
-            if (qn < 32) continue;
-        } else if (qn == 0) {
-            break;
-        }
-        // stage 2 on queue entries [0, min(qn, 32))
-        const bool have = lane < qn;
-        const u32 sig = have ? qs[lane] : 0;
-        u32 cnt = have ? qc[lane] : 0;
-        cnt = count_lower<0, CL, true>(K, c.s, sig, c.r, c.cp, 0xffffffffu, cnt);
+    const u32 g1 = c.cp, g2 = c.cp2;
+    u32* const qc = qs + 64;
+    u32* const qs2 = qs + 128;
+    u32* const qc2 = qs + 192;
+    u32 qn = 0, qn2 = 0;
+    // final stage on the first nb entries of queue (fs, fc) counted up to group gf
+    auto finish = [&](u32* fs, u32* fc, u32& fn, u32 nb, u32 gf) -> bool {
+        const bool have = lane < nb;
+        const u32 sig = have ? fs[lane] : 0;
+        u32 cnt = have ? fc[lane] : 0;
+        cnt = count_lower<0, CL, true>(K, c.s, sig, c.r, gf, 0xffffffffu, cnt);
         const u32 bal = __ballot_sync(FULL, have && (cnt & c.mask) == c.target);
         if (bal) {
             *val = c.kW + __shfl_sync(FULL, sig, __ffs(bal) - 1);
             return true;
         }
-        __syncwarp();
-        const u32 rest = qn > 32 ? qn - 32 : 0;
-        u32 a = 0, b = 0;
-        if (lane < rest) {
-            a = qs[32 + lane];
-            b = qc[32 + lane];
+        queue_pop(fs, fc, fn, nb, lane);
+        return false;
+    };
+    for (u32 it = 0; it <= A.iters; ++it) {
+        const bool last = it == A.iters;
+        if (!last) {
+            const u32 sig = wrel + it * 32 + lane;
+            const u32 cnt = count_lower<0, CL, false>(K, c.s, sig, c.r, 0, g1);
+            const bool keep = !cp_reject<CL>(cnt, 9);
+            const u32 bal = __ballot_sync(FULL, keep);
+            if (keep) {
+                const u32 pos = qn + __popc(bal & lanemask_lt());
+                qs[pos] = sig;
+                qc[pos] = cnt;
+            }
+            qn += __popc(bal);
+            __syncwarp();
         }
-        __syncwarp();
-        if (lane < rest) {
-            qs[lane] = a;
-            qc[lane] = b;
+        while (qn >= 32 || (last && qn > 0)) {
+            const u32 nb = min(qn, 32u);
+            if (!g2) {
+                if (finish(qs, qc, qn, nb, g1)) return true;
+                continue;
+            }
+            // stage 2: groups [g1, g2), survivors to queue 2
+            const bool have = lane < nb;
+            const u32 sig = have ? qs[lane] : 0;
+            u32 cnt = have ? qc[lane] : 0;
+            cnt = count_lower<0, CL, false>(K, c.s, sig, c.r, g1, g2, cnt);
+            const bool keep = have && !cp_reject<CL>(cnt, 10);
+            const u32 bal = __ballot_sync(FULL, keep);
+            if (keep) {
+                const u32 pos = qn2 + __popc(bal & lanemask_lt());
+                qs2[pos] = sig;
+                qc2[pos] = cnt;
+            }
+            qn2 += __popc(bal);
+            queue_pop(qs, qc, qn, nb, lane);
+            if (qn2 >= 32 && finish(qs2, qc2, qn2, 32, g2)) return true;
         }
-        __syncwarp();
-        qn = rest;
+        if (last)
+            while (qn2 > 0)
+                if (finish(qs2, qc2, qn2, min(qn2, 32u), g2)) return true;
     }
     return false;
 }
@@ -633,8 +681,8 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, Nod
     if (ws * sc - 1 <= c.margin) {
         const u32 wrel = (u32)(wstart - c.kW);
         if (VAR == V_CP && KIND == SK_LOWER && c.cp)
-            return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, qc, val)
-                        : run_window_cp<0>(A, K, c, wstart, lane, qs, qc, val);
+            return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, val)
+                        : run_window_cp<0>(A, K, c, wstart, lane, qs, val);
         if (VAR == V_CP && (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) && c.cp)
             return run_window_leaf_cp<KIND>(A, K, c, wstart, lane, qs, qc, qc + 64, val);
         for (u32 it = 0; it < A.iters; ++it) {
@@ -714,10 +762,11 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     const u32 cap = A.warp_cap;                    // keys (multiple of 4)
     const u32 gwords = GW * (cap / 4 + 1);         // key groups
     const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
-    u32* G = smem32 + (size_t)wib * (gwords + twords + 192);
+    u32* G = smem32 + (size_t)wib * (gwords + twords + 256);
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
-    u32* QS = G + gwords + twords;  // early-rejection queue (64 entries): seeds, partial counters
-    u32* QC = QS + 64;              // (splits) or partial masks a, b (leaves)
+    u32* QS = G + gwords + twords;  // early-rejection queues (64 entries each): seeds, partial
+    u32* QC = QS + 64;              // counters, and the second stage's seeds, counters (splits),
+                                    // or seeds and partial masks a, b (leaves)
     const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
     if (KIND == SK_LOWER) {  // shift tables of full nodes: part p -> p*w (p < f-1), 32 for the last
         for (u32 t = threadIdx.x; t < 64; t += blockDim.x) {
@@ -753,12 +802,14 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                     if (j & 1) Mo |= 1u << (2 * w * no++);
                     else Me |= 1u << (2 * w * ne++);
                 }
-                const u32 kcp = 4 * (cl ? A.cp_l2 : A.cp_l1);
+                const u32 kcp = 4 * (cl ? A.cp_l2 : A.cp_l1), kcp2 = 4 * (cl ? A.cp_l2b : A.cp_l1b);
                 const bool ok = 2 * w < 32 && kcp < (1u << (2 * w)) && kcp > unit && (f - 1) * w <= 31;
+                const bool ok2 = 2 * w < 32 && kcp2 < (1u << (2 * w)) && kcp2 > unit && (f - 1) * w <= 31;
                 s_cp_masks[cl][6] = Me;
                 s_cp_masks[cl][7] = Mo;
                 s_cp_masks[cl][8] = (ne ? 2 * w * (ne - 1) : 0) | (no ? 2 * w * (no - 1) : 0) << 8 | w << 16;
                 s_cp_masks[cl][9] = ok && A.cp_last ? kcp - unit : 0u;
+                s_cp_masks[cl][10] = ok2 && A.cp_last ? kcp2 - unit : 0u;
             }
         }
         __syncthreads();
@@ -872,10 +923,16 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.help = P.help;
     // early-rejection checkpoints (per mille of the node size; RS_CP1 / RS_CP2 override, 0 = off)
     {
-        static const int cp1 = getenv("RS_CP1") ? atoi(getenv("RS_CP1")) : 850;
+        // L1: two-stage cascade at 780 / 880 per mille; L2: one checkpoint at 940 (measured,
+        // DESIGN.md 5)
+        static const int cp1 = getenv("RS_CP1") ? atoi(getenv("RS_CP1")) : 780;
         static const int cp2 = getenv("RS_CP2") ? atoi(getenv("RS_CP2")) : 940;
+        static const int cp1b = getenv("RS_CP1B") ? atoi(getenv("RS_CP1B")) : 880;
+        static const int cp2b = getenv("RS_CP2B") ? atoi(getenv("RS_CP2B")) : 0;
         A.cp_l1 = (u32)((u64)P.u1 * cp1 / 4000);
         A.cp_l2 = (u32)((u64)P.u2 * cp2 / 4000);
+        A.cp_l1b = (u32)((u64)P.u1 * cp1b / 4000);
+        A.cp_l2b = (u32)((u64)P.u2 * cp2b / 4000);
         static const int cpl = getenv("RS_CPL") ? atoi(getenv("RS_CPL")) : 1;
         A.cp_leaf = cpl ? 1u : 0u;
         static const int cplast = getenv("RS_CPLAST") ? atoi(getenv("RS_CPLAST")) : 1;
@@ -886,7 +943,7 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
     const u32 GW = (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) ? 20 : 12;
-    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + 192) * sizeof(u32);
+    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + 256) * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;

@@ -484,19 +484,25 @@ for leaf, b, n in {cases!r}:
 """
 
 
-@pytest.mark.parametrize("cp", ["0:0:0", "100:100:1", "990:990:1", "500:0:0", "0:700:1"])
+@pytest.mark.parametrize("cp", ["0:0:0:0:0", "100:100:1:0:0", "990:990:1:0:0", "500:0:0:0:0", "0:700:1:0:0",
+                                "850:940:1:0:0", "100:100:1:200:300", "300:500:1:990:990", "780:940:1:880:0:0",
+                                "780:940:1:880:0:1", "750:900:1:860:950:1"])
 def test_early_rejection_checkpoints_do_not_change_output(cp):
     """The lower-level early rejection may only skip seeds that cannot succeed:
     the bytes equal the oracle's with it off, at degenerate checkpoints (almost no keys /
-    almost all keys before the test, i.e. a queue that fills on every iteration), and with
-    it on for one level only (RS_CP1 / RS_CP2, per mille of u1 / u2), and with the leaf
-    early rejection off / on (RS_CPL)."""
+    almost all keys before the test, i.e. a queue that fills on every iteration), with it on
+    for one level only (RS_CP1 / RS_CP2, per mille of u1 / u2), as a single stage and as a
+    two-stage cascade (second checkpoints RS_CP1B / RS_CP2B, early, late and the defaults),
+    with the last-part test off / on (RS_CPLAST) and the leaf early rejection off / on
+    (RS_CPL)."""
     import hashlib
     import subprocess
     import sys
     cases = [(16, 2000, 6000), (12, 1000, 30000), (8, 100, 20000), (5, 5, 20000), (20, 100, 600)]
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, RS_CP1=cp.split(":")[0], RS_CP2=cp.split(":")[1], RS_CPL=cp.split(":")[2])
+    v = cp.split(":")
+    env = dict(os.environ, RS_CP1=v[0], RS_CP2=v[1], RS_CPL=v[2], RS_CP1B=v[3], RS_CP2B=v[4],
+               RS_CPLAST=v[5] if len(v) > 5 else "1")
     out = subprocess.run([sys.executable, "-c", _CP_SNIPPET.format(root=root, cases=cases)], env=env,
                          capture_output=True, text=True, timeout=600, check=True).stdout.split()
     want = [hashlib.sha256(oracle.build(synth.keys(n, 1000 * leaf + b), leaf, b, threads=os.cpu_count()))
