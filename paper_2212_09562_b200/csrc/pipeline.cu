@@ -626,46 +626,78 @@ void Shard::finish(long long dR, std::vector<uint8_t>& part) {
     stats.t_d2h += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// Pinned host staging for the single-shard D2H (pageable copies run at a few GB/s; C2's
+// ~1.1 MB result took 0.3 ms), grown on demand and kept for the process.
+struct PinnedStage {
+    std::mutex mu;
+    uint8_t* p = nullptr;
+    size_t cap = 0;
+    uint8_t* get(size_t n) {
+        if (n > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            const size_t c = std::max<size_t>(n + n / 4, 1 << 20);
+            CK(cudaMallocHost(&p, c));
+            cap = c;
+        }
+        return p;
+    }
+};
+static PinnedStage g_stage;
+
 void Shard::finish_blob(long long dR, std::vector<uint8_t>& blob) {
     Impl& I = *impl_;
     if (I.world != 1) throw Error(RECSPLIT_E_INVALID, "finish_blob needs a single shard");
     auto t0 = std::chrono::steady_clock::now();
     const ShardSlices S = make_slices(I, dR);
     const Globals& G = I.G;
-    // single shard: every slice starts at bit 0 of its section -> D2H into the final layout
+    // single shard: every slice starts at bit 0 of its section -> the header and the five
+    // sections are laid out in a pinned buffer in their final order, then copied once
     auto nbytes = [](uint64_t bits) { return (size_t)(8 * ((bits + 63) / 64)); };
     const size_t size = 72 + 2 * 24 + nbytes(S.nbits[1]) + nbytes(S.nbits[2]) + nbytes(S.nbits[3]) +
                         nbytes(S.nbits[4]) + nbytes(S.nbits[0]);
-    blob.clear();
-    blob.reserve(size);
-    blob.push_back('R');
-    blob.push_back('S');
-    blob.push_back('R');
-    blob.push_back('F');
-    put_le(blob, 1, 2);
-    blob.push_back((uint8_t)I.p.leaf);
-    blob.push_back((uint8_t)((I.p.rf ? 1 : 0) | (I.p.strings ? 2 : 0)));
-    put_le(blob, I.p.bucket, 4);
-    put_le(blob, 0, 4);
-    for (uint64_t x : {I.p.g, G.n, I.B, G.D, G.dC, G.beta, (uint64_t)dR}) put_le(blob, x, 8);
-    auto section = [&](int q) {
-        put_le(blob, S.nbits[q], 8);
-        const size_t nb = nbytes(S.nbits[q]), at = blob.size();
-        blob.resize(at + nb);
-        if (nb) CK(cudaMemcpyAsync(blob.data() + at, S.dev[q], nb, cudaMemcpyDeviceToHost, I.st));
+    std::vector<uint8_t> head;
+    head.reserve(72);
+    head.push_back('R');
+    head.push_back('S');
+    head.push_back('R');
+    head.push_back('F');
+    put_le(head, 1, 2);
+    head.push_back((uint8_t)I.p.leaf);
+    head.push_back((uint8_t)((I.p.rf ? 1 : 0) | (I.p.strings ? 2 : 0)));
+    put_le(head, I.p.bucket, 4);
+    put_le(head, 0, 4);
+    for (uint64_t x : {I.p.g, G.n, I.B, G.D, G.dC, G.beta, (uint64_t)dR}) put_le(head, x, 8);
+    std::lock_guard<std::mutex> lk(g_stage.mu);
+    uint8_t* buf = g_stage.get(size);
+    size_t at = 0;
+    auto put = [&](const uint8_t* src, size_t nb) {
+        memcpy(buf + at, src, nb);
+        at += nb;
     };
-    blob.push_back((uint8_t)G.LC);
-    for (int z = 0; z < 7; ++z) blob.push_back(0);
+    auto put64 = [&](uint64_t x) {
+        for (int b = 0; b < 8; ++b) buf[at++] = (uint8_t)(x >> (8 * b));
+    };
+    auto section = [&](int q) {
+        put64(S.nbits[q]);
+        const size_t nb = nbytes(S.nbits[q]);
+        if (nb) CK(cudaMemcpyAsync(buf + at, S.dev[q], nb, cudaMemcpyDeviceToHost, I.st));
+        at += nb;
+    };
+    put(head.data(), head.size());
+    put64(G.LC);  // u8 L then 7 pad bytes, little-endian
     section(1);
     section(2);
-    blob.push_back((uint8_t)G.LP);
-    for (int z = 0; z < 7; ++z) blob.push_back(0);
+    put64(G.LP);
     section(3);
     section(4);
-    const size_t nb = nbytes(S.nbits[0]), at = blob.size();
-    blob.resize(at + nb);
-    if (nb) CK(cudaMemcpyAsync(blob.data() + at, S.dev[0], nb, cudaMemcpyDeviceToHost, I.st));
+    const size_t nb = nbytes(S.nbits[0]);
+    if (nb) CK(cudaMemcpyAsync(buf + at, S.dev[0], nb, cudaMemcpyDeviceToHost, I.st));
+    at += nb;
+    if (at != size) throw Error(RECSPLIT_E_INVALID, "internal: serialized size mismatch");
     CK(cudaStreamSynchronize(I.st));
+    blob.assign(buf, buf + size);
     stats.t_d2h += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
