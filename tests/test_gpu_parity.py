@@ -405,6 +405,43 @@ def test_build_sharded_two_ranks_gloo(distribute):
     assert q.get(timeout=10) is True
 
 
+def _nccl_worker(port, q):
+    import sys as _sys
+    _sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import paper_2212_09562_b200 as rs_
+    import synth as synth_
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        keys = synth_.keys(150_000, 13)
+        kt = torch.from_numpy(keys.view(np.int64)).cuda()
+        want = rs_.build(keys, 12, 1000)
+        ok = [rs_.build_sharded(kt, 12, 1000, distribute=d) == want for d in (False, True)]
+        q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_build_sharded_nccl_single_rank():
+    """The NCCL code path of build_sharded (device tensors in all_reduce, all_to_all_single,
+    all_gather_into_tensor, as bench.py uses at N > 1) on a one-rank NCCL group: same bytes as
+    the single-GPU build, with and without key routing."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31700 + os.getpid() % 1000
+    p = ctx.Process(target=_nccl_worker, args=(port, q))
+    p.start()
+    p.join(600)
+    assert p.exitcode == 0
+    assert q.get(timeout=10) == [True, True]
+
+
 # -------------------------------------------------------------- device query --
 
 @pytest.mark.parametrize("leaf,b,rf,n", [(8, 100, True, 10_000), (16, 2000, True, 20_000), (5, 5, False, 20_000),
