@@ -377,6 +377,9 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
     c.slot = rec.slot;
     const u32 s = c.s;
     u32 mg = FULL;  // carry margin: min over keys of 2^32 - 1 - k_lo
+    // the warp's previous node was read by every lane; order those reads before the rewrite
+    // (help mode reaches here through shuffles / ballots only, which do not order memory)
+    __syncwarp();
     if (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) {
         // natural key order; A/B select masks (global 1-bit hash); padding keys to
         // the next multiple of four get zero masks
