@@ -936,6 +936,11 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         A.cp_l2 = (u32)((u64)P.u2 * cp2 / 4000);
         A.cp_l1b = (u32)((u64)P.u1 * cp1b / 4000);
         A.cp_l2b = (u32)((u64)P.u2 * cp2b / 4000);
+        // batch-mode phases (expected < 1024 trials per node, 32-seed windows) flush a partial
+        // stage-2 batch at every window end, which costs more than the rejection saves (C2:
+        // L1 -14 %, L2 -5 % without it; tools/c2_knobs.sh); RS_CP_BATCH=1 keeps it (tests)
+        static const int cpbatch = getenv("RS_CP_BATCH") ? atoi(getenv("RS_CP_BATCH")) : 0;
+        if (!P.help && !cpbatch) A.cp_l1 = A.cp_l2 = A.cp_l1b = A.cp_l2b = 0;
         static const int cpl = getenv("RS_CPL") ? atoi(getenv("RS_CPL")) : 1;
         A.cp_leaf = cpl ? 1u : 0u;
         static const int cplast = getenv("RS_CPLAST") ? atoi(getenv("RS_CPLAST")) : 1;
