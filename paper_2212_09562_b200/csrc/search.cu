@@ -58,6 +58,7 @@ struct Args {
     u32 cp_l2b;
     u32 cp_leaf;   // leaves: early rejection on (0 = off)
     u32 cp_last;   // full lower nodes: also reject when the last part already overflows (0 = off)
+    u32 cp_wide;   // early rejection in the wide-counter kernel (l >= 19) too (0 = off)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -187,13 +188,15 @@ __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, 
 // parts hs..f-2 in the high word (hs = floor(32/w)); the table holds t = p*w (low word) or
 // 32 + (p-hs)*w (high word), 64 for the last part; increments 1 << t and 1 << (t-32), both
 // clamped to 0 out of range.  The exactness argument of DESIGN.md 5 holds per word.
-template <int MODE, int CL>
-__device__ __forceinline__ u64 count_lower_wide(const KeysView& K, u32 s, u32 sigma, u32 r) {
-    u32 lo = 0, hi = 0;
-    const u32 ng = s >> 2;
-    const u32* __restrict__ g = K.G;
+// Groups [g0, g1) (+ the s % 4 tail keys when TAIL), starting from the counter init.
+template <int MODE, int CL, bool TAIL = true>
+__device__ __forceinline__ u64 count_lower_wide(const KeysView& K, u32 s, u32 sigma, u32 r, u32 g0 = 0,
+                                                u32 g1 = 0xffffffffu, u64 init = 0) {
+    u32 lo = (u32)init, hi = (u32)(init >> 32);
+    const u32 ng = min(s >> 2, g1);
+    const u32* __restrict__ g = K.G + 12 * g0;
 #pragma unroll 1
-    for (u32 q = 0; q < ng; ++q, g += 12) {
+    for (u32 q = g0; q < ng; ++q, g += 12) {
         u32 h[4];
         hash4<MODE>(g, sigma, h, K.H);
 #pragma unroll
@@ -209,7 +212,8 @@ __device__ __forceinline__ u64 count_lower_wide(const KeysView& K, u32 s, u32 si
             hi += bit_clamp(t - 32);
         }
     }
-    for (u32 j = ng << 2; j < s; ++j) {
+    if (TAIL)
+    for (u32 j = (s >> 2) << 2; j < s; ++j) {
         const u32 h = hash1<MODE, 12>(K, j, sigma);
         u32 t;
         if (CL < 2)
@@ -431,9 +435,10 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
             c.r = c.full ? f : s;
             c.l2 = s > A.u1;
             const u32 cpg = c.l2 ? A.cp_l2 : A.cp_l1;
-            c.cp = c.full && cpg < (s >> 2) && (f - 1) * w <= 31 ? cpg : 0;
+            // (wide counters: early rejection by field extraction, run_window_cp_wide)
+            c.cp = c.full && cpg < (s >> 2) && ((f - 1) * w <= 31 || (WIDE && A.cp_wide)) ? cpg : 0;
             const u32 cpg2 = c.l2 ? A.cp_l2b : A.cp_l1b;
-            c.cp2 = c.cp && cpg2 >= cpg + 2 && cpg2 < (s >> 2) ? cpg2 : 0;  // a 1-group stage does not pay
+            c.cp2 = c.cp && !WIDE && cpg2 >= cpg + 2 && cpg2 < (s >> 2) ? cpg2 : 0;  // a 1-group stage does not pay
             if (!c.wide) {
                 u32 t = 0;
                 for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
@@ -668,6 +673,83 @@ __device__ __forceinline__ bool run_window_leaf_cp(const Args& A, const KeysView
     return false;
 }
 
+// Early rejection for the wide (64-bit) packed counters (l >= 19, (f-1)*w > 32), one
+// checkpoint: after k keys a seed cannot succeed if some part 0..f-2 holds more than unit
+// keys or the last part does (k - sum of the fields > unit).  The fields are extracted one by
+// one (once per seed, not per key).  A valid seed has every count <= unit < 2^w - 1, so its
+// fields are exact and it is never rejected; an overflowed field may hide a rejection, never
+// cause one.
+__device__ __forceinline__ bool wide_reject(u64 cnt, const NodeCtx& c, u32 k) {
+    const u32 fm = (1u << c.w) - 1u;
+    u32 sum = 0;
+    bool over = false;
+    for (u32 j = 0; j + 1 < c.f; ++j) {
+        const u32 v = (u32)(cnt >> part_shift(j, c.f, c.w)) & fm;
+        over |= v > c.unit;
+        sum += v;
+    }
+    return over || sum + c.unit < k;
+}
+
+// The wide counterpart of run_window_cp (single stage): survivors queue as (seed, counter
+// low word, counter high word) in seed order and are completed 32 at a time; the first hit is
+// the smallest successful seed of the window (same argument as run_window_cp).
+template <int CL>
+__device__ __forceinline__ bool run_window_cp_wide(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
+                                                   u32 lane, u32* qs, u64* val) {
+    const u32 wrel = (u32)(wstart - c.kW);
+    const u32 g1 = c.cp, k1 = 4 * c.cp;
+    u32* const qlo = qs + 64;
+    u32* const qhi = qs + 128;
+    u32 qn = 0;
+    for (u32 it = 0; it <= A.iters; ++it) {
+        const bool last = it == A.iters;
+        if (!last) {
+            const u32 sig = wrel + it * 32 + lane;
+            const u64 cnt = count_lower_wide<0, CL, false>(K, c.s, sig, c.r, 0, g1);
+            const bool keep = !wide_reject(cnt, c, k1);
+            const u32 bal = __ballot_sync(FULL, keep);
+            if (keep) {
+                const u32 pos = qn + __popc(bal & lanemask_lt());
+                qs[pos] = sig;
+                qlo[pos] = (u32)cnt;
+                qhi[pos] = (u32)(cnt >> 32);
+            }
+            qn += __popc(bal);
+            __syncwarp();
+        }
+        while (qn >= 32 || (last && qn > 0)) {
+            const u32 nb = min(qn, 32u);
+            const bool have = lane < nb;
+            const u32 sig = have ? qs[lane] : 0;
+            u64 cnt = have ? (((u64)qhi[lane] << 32) | qlo[lane]) : 0;
+            cnt = count_lower_wide<0, CL, true>(K, c.s, sig, c.r, g1, 0xffffffffu, cnt);
+            const u32 bal = __ballot_sync(FULL, have && (cnt & c.mask64) == c.target64);
+            if (bal) {
+                *val = c.kW + __shfl_sync(FULL, sig, __ffs(bal) - 1);
+                return true;
+            }
+            const u32 rest = qn - nb;
+            u32 x = 0, y = 0, z = 0;
+            __syncwarp();
+            if (lane < rest) {
+                x = qs[nb + lane];
+                y = qlo[nb + lane];
+                z = qhi[nb + lane];
+            }
+            __syncwarp();
+            if (lane < rest) {
+                qs[lane] = x;
+                qlo[lane] = y;
+                qhi[lane] = z;
+            }
+            __syncwarp();
+            qn = rest;
+        }
+    }
+    return false;
+}
+
 template <int KIND, int VAR>
 __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, NodeCtx& c, u64 wstart,
                                            u32 lane, u64* val, u32* qs, u32* qc) {
@@ -683,6 +765,9 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, Nod
     }
     if (ws * sc - 1 <= c.margin) {
         const u32 wrel = (u32)(wstart - c.kW);
+        if (VAR == V_WIDE && KIND == SK_LOWER && c.cp)
+            return c.l2 ? run_window_cp_wide<1>(A, K, c, wstart, lane, qs, val)
+                        : run_window_cp_wide<0>(A, K, c, wstart, lane, qs, val);
         if (VAR == V_CP && KIND == SK_LOWER && c.cp)
             return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, val)
                         : run_window_cp<0>(A, K, c, wstart, lane, qs, val);
@@ -945,6 +1030,8 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         A.cp_leaf = cpl ? 1u : 0u;
         static const int cplast = getenv("RS_CPLAST") ? atoi(getenv("RS_CPLAST")) : 1;
         A.cp_last = cplast ? 1u : 0u;
+        static const int cpw = getenv("RS_CPW") ? atoi(getenv("RS_CPW")) : 1;
+        A.cp_wide = cpw ? 1u : 0u;
     }
     // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
