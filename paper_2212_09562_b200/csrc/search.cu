@@ -33,6 +33,7 @@ namespace {
 
 constexpr u32 kWarpsPerBlockMax = 4;
 constexpr u64 kSeedCap = 1ull << 40;  // diagnostic trial cap per node (R11)
+constexpr u32 kQWords = 384;          // per-warp early-rejection queues: two stages x 3 x 64 words
 
 struct Args {
     const NodeRec* nodes;
@@ -59,6 +60,7 @@ struct Args {
     u32 cp_leaf;   // leaves: early rejection on (0 = off)
     u32 cp_last;   // full lower nodes: also reject when the last part already overflows (0 = off)
     u32 cp_wide;   // early rejection in the wide-counter kernel (l >= 19) too (0 = off)
+    u32 cp_leaf2;  // leaves: second checkpoint (0 = single stage)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -405,6 +407,9 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
         // a base seed whose first 4*cp keys already collide fails; best measured-by-simulation
         // checkpoints: 8 keys for m = 10..19, 12 keys for m = 20..24
         c.cp = A.cp_leaf && s >= 10 ? (s < 20 ? 2u : 3u) : 0u;
+        // second checkpoint (simulated cascade optimum: keys 8 / 12 for m = 14..19, 12 / 16 for
+        // m = 20..24; a single stage is better below m = 14)
+        c.cp2 = c.cp && A.cp_leaf2 && s >= 14 ? c.cp + 1 : 0u;
         c.kW = 0;
     } else {
         for (u32 j = lane; j < s; j += 32) {
@@ -607,42 +612,62 @@ __device__ __forceinline__ bool run_window_cp(const Args& A, const KeysView& K, 
     return false;
 }
 
-// Early rejection with warp compaction for leaves (no-carry path): stage 1 ORs the masks
-// of the first 4*c.cp keys (full groups) for 32 base seeds; a seed whose partial masks show a
-// collision (popc(a) + popc(b) < keys so far) cannot fit (P:252 pruning, applied early).
-// Survivors queue in seed order with their partial masks; stage 2 completes 32 of them and
-// runs the fit (rotation fitting: lowest lane with a fit and its smallest r; brute force:
-// a == full).  Every other seed of the window failed, so the first hit is the window's minimum.
+// Early rejection with warp compaction for leaves (no-carry path), a cascade of up to two
+// checkpoints: stage 1 ORs the masks of the first 4*c.cp keys (full groups) for 32 base seeds; a
+// seed whose partial masks show a collision (popc(a) + popc(b) < keys so far) cannot fit (P:252
+// pruning, applied early).  Survivors queue in seed order with their partial masks; with a second
+// checkpoint c.cp2, stage 2 extends 32 of them to 4*c.cp2 keys, tests again and queues its
+// survivors for stage 3; the last stage completes the masks and runs the fit (rotation fitting:
+// lowest lane with a fit and its smallest r; brute force: a == full).  Batches are the oldest
+// entries of their queue and every queue is older than everything upstream, so survivors are
+// completed in seed order; every other seed of the window failed, hence the first hit is the
+// window's minimum.
 template <int KIND>
 __device__ __forceinline__ bool run_window_leaf_cp(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
-                                                   u32 lane, u32* qs, u32* qa, u32* qb, u64* val) {
+                                                   u32 lane, u32* qs, u64* val) {
     const u32 wrel = (u32)(wstart - c.kW);
-    const u32 ng = (c.s + 3) >> 2, k1 = 4 * c.cp;
-    const u32 lt = lanemask_lt();
-    u32 qn = 0;
-    for (u32 it = 0; it <= A.iters; ++it) {
-        if (it < A.iters) {
-            const u32 sig = wrel + it * 32 + lane;
-            u32 a, b;
-            leaf_masks<0>(K, c.cp, c.s, KIND == SK_LEAF_RF ? sig * c.s : sig, a, b);
-            const bool keep = (u32)(__popc(a) + __popc(b)) == k1;
-            const u32 bal = __ballot_sync(FULL, keep);
-            if (keep) {
-                const u32 pos = qn + __popc(bal & lt);
-                qs[pos] = sig;
-                qa[pos] = a;
-                qb[pos] = b;
-            }
-            qn += __popc(bal);
-            __syncwarp();
-            if (qn < 32) continue;
-        } else if (qn == 0) {
-            break;
+    const u32 ng = (c.s + 3) >> 2, g1 = c.cp, g2 = c.cp2;
+    u32* const qa = qs + 64;
+    u32* const qb = qs + 128;
+    u32* const qs2 = qs + 192;
+    u32* const qa2 = qs + 256;
+    u32* const qb2 = qs + 320;
+    u32 qn = 0, qn2 = 0;
+    auto base_of = [&](u32 sig) { return KIND == SK_LEAF_RF ? sig * c.s : sig; };
+    auto push = [&](bool keep, u32 sig, u32 a, u32 b, u32* ds, u32* da, u32* db, u32& dn) {
+        const u32 bal = __ballot_sync(FULL, keep);
+        if (keep) {
+            const u32 pos = dn + __popc(bal & lanemask_lt());
+            ds[pos] = sig;
+            da[pos] = a;
+            db[pos] = b;
         }
-        const bool have = lane < qn;
-        const u32 sig = have ? qs[lane] : 0;
-        u32 a = have ? qa[lane] : 0, b = have ? qb[lane] : 0;
-        leaf_masks<0>(K, ng, c.s, KIND == SK_LEAF_RF ? sig * c.s : sig, a, b, c.cp, a, b);
+        dn += __popc(bal);
+        __syncwarp();
+    };
+    auto pop = [&](u32* ds, u32* da, u32* db, u32& dn, u32 nb) {
+        const u32 rest = dn - nb;
+        u32 x = 0, y = 0, z = 0;
+        if (lane < rest) {
+            x = ds[nb + lane];
+            y = da[nb + lane];
+            z = db[nb + lane];
+        }
+        __syncwarp();
+        if (lane < rest) {
+            ds[lane] = x;
+            da[lane] = y;
+            db[lane] = z;
+        }
+        __syncwarp();
+        dn = rest;
+    };
+    // last stage on the first nb entries of (fs, fa, fb), masks completed from group gf
+    auto finish = [&](u32* fs, u32* fa, u32* fb, u32& fn, u32 nb, u32 gf) -> bool {
+        const bool have = lane < nb;
+        const u32 sig = have ? fs[lane] : 0;
+        u32 a = have ? fa[lane] : 0, b = have ? fb[lane] : 0;
+        leaf_masks<0>(K, ng, c.s, base_of(sig), a, b, gf, a, b);
         if (!have) a = b = 0;  // no entry: cannot fit (m >= 10 keys)
         int r = 0;
         const bool ok = KIND == SK_LEAF_BF ? a == c.full : fit_rotation_warp(a, b, c.s, c.full, lane, r);
@@ -654,21 +679,34 @@ __device__ __forceinline__ bool run_window_leaf_cp(const Args& A, const KeysView
             return true;
         }
         __syncwarp();
-        const u32 rest = qn > 32 ? qn - 32 : 0;
-        u32 x = 0, y = 0, z = 0;
-        if (lane < rest) {
-            x = qs[32 + lane];
-            y = qa[32 + lane];
-            z = qb[32 + lane];
+        pop(fs, fa, fb, fn, nb);
+        return false;
+    };
+    for (u32 it = 0; it <= A.iters; ++it) {
+        const bool last = it == A.iters;
+        if (!last) {
+            const u32 sig = wrel + it * 32 + lane;
+            u32 a, b;
+            leaf_masks<0>(K, g1, c.s, base_of(sig), a, b);
+            push((u32)(__popc(a) + __popc(b)) == 4 * g1, sig, a, b, qs, qa, qb, qn);
         }
-        __syncwarp();
-        if (lane < rest) {
-            qs[lane] = x;
-            qa[lane] = y;
-            qb[lane] = z;
+        while (qn >= 32 || (last && qn > 0)) {
+            const u32 nb = min(qn, 32u);
+            if (!g2) {
+                if (finish(qs, qa, qb, qn, nb, g1)) return true;
+                continue;
+            }
+            const bool have = lane < nb;
+            const u32 sig = have ? qs[lane] : 0;
+            u32 a = have ? qa[lane] : 0, b = have ? qb[lane] : 0;
+            leaf_masks<0>(K, g2, c.s, base_of(sig), a, b, g1, a, b);
+            push(have && (u32)(__popc(a) + __popc(b)) == 4 * g2, sig, a, b, qs2, qa2, qb2, qn2);
+            pop(qs, qa, qb, qn, nb);
+            if (qn2 >= 32 && finish(qs2, qa2, qb2, qn2, 32, g2)) return true;
         }
-        __syncwarp();
-        qn = rest;
+        if (last)
+            while (qn2 > 0)
+                if (finish(qs2, qa2, qb2, qn2, min(qn2, 32u), g2)) return true;
     }
     return false;
 }
@@ -772,7 +810,7 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, Nod
             return c.l2 ? run_window_cp<1>(A, K, c, wstart, lane, qs, val)
                         : run_window_cp<0>(A, K, c, wstart, lane, qs, val);
         if (VAR == V_CP && (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) && c.cp)
-            return run_window_leaf_cp<KIND>(A, K, c, wstart, lane, qs, qc, qc + 64, val);
+            return run_window_leaf_cp<KIND>(A, K, c, wstart, lane, qs, val);
         for (u32 it = 0; it < A.iters; ++it) {
             int r = 0;
             const bool ok = trial_fast<KIND, 0, VAR == V_WIDE>(K, c, wrel + it * 32 + lane, lane, r);
@@ -850,11 +888,10 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     const u32 cap = A.warp_cap;                    // keys (multiple of 4)
     const u32 gwords = GW * (cap / 4 + 1);         // key groups
     const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
-    u32* G = smem32 + (size_t)wib * (gwords + twords + 256);
+    u32* G = smem32 + (size_t)wib * (gwords + twords + kQWords);
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
-    u32* QS = G + gwords + twords;  // early-rejection queues (64 entries each): seeds, partial
-    u32* QC = QS + 64;              // counters, and the second stage's seeds, counters (splits),
-                                    // or seeds and partial masks a, b (leaves)
+    u32* QS = G + gwords + twords;  // early-rejection queues, kQWords per warp (64 entries each):
+    u32* QC = QS + 64;              // seeds + partial counters / masks, for up to two stages
     const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
     if (KIND == SK_LOWER) {  // shift tables of full nodes: part p -> p*w (p < f-1), 32 for the last
         for (u32 t = threadIdx.x; t < 64; t += blockDim.x) {
@@ -1032,13 +1069,15 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         A.cp_last = cplast ? 1u : 0u;
         static const int cpw = getenv("RS_CPW") ? atoi(getenv("RS_CPW")) : 1;
         A.cp_wide = cpw ? 1u : 0u;
+        static const int cpl2 = getenv("RS_CPL2") ? atoi(getenv("RS_CPL2")) : 1;
+        A.cp_leaf2 = cpl2 ? 1u : 0u;
     }
     // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
     const u32 GW = (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) ? 20 : 12;
-    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + 256) * sizeof(u32);
+    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + kQWords) * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;

@@ -523,7 +523,7 @@ for leaf, b, n in {cases!r}:
 
 @pytest.mark.parametrize("cp", ["0:0:0:0:0", "100:100:1:0:0", "990:990:1:0:0", "500:0:0:0:0", "0:700:1:0:0",
                                 "850:940:1:0:0", "100:100:1:200:300", "300:500:1:990:990", "780:940:1:880:0:0",
-                                "780:940:1:880:0:1", "750:900:1:860:950:1", "780:940:1:880:0:1:0"])
+                                "780:940:1:880:0:1", "750:900:1:860:950:1", "780:940:1:880:0:1:0", "780:940:1:880:0:1:1:0"])
 def test_early_rejection_checkpoints_do_not_change_output(cp):
     """The lower-level early rejection may only skip seeds that cannot succeed:
     the bytes equal the oracle's with it off, at degenerate checkpoints (almost no keys /
@@ -531,8 +531,9 @@ def test_early_rejection_checkpoints_do_not_change_output(cp):
     for one level only (RS_CP1 / RS_CP2, per mille of u1 / u2), as a single stage and as a
     two-stage cascade (second checkpoints RS_CP1B / RS_CP2B, early, late and the defaults),
     with the last-part test off / on (RS_CPLAST) and the leaf early rejection off / on
-    (RS_CPL); small-node (batch-mode) phases keep the rejection (RS_CP_BATCH=1) except in the
-    last case, the shipped default."""
+    (RS_CPL, with the leaves' second checkpoint RS_CPL2 on, and off in the last case);
+    small-node (batch-mode) phases keep the split rejection (RS_CP_BATCH=1) except where the
+    seventh field is 0, the shipped default."""
     import hashlib
     import subprocess
     import sys
@@ -540,7 +541,8 @@ def test_early_rejection_checkpoints_do_not_change_output(cp):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     v = cp.split(":")
     env = dict(os.environ, RS_CP1=v[0], RS_CP2=v[1], RS_CPL=v[2], RS_CP1B=v[3], RS_CP2B=v[4],
-               RS_CPLAST=v[5] if len(v) > 5 else "1", RS_CP_BATCH=v[6] if len(v) > 6 else "1")
+               RS_CPLAST=v[5] if len(v) > 5 else "1", RS_CP_BATCH=v[6] if len(v) > 6 else "1",
+               RS_CPL2=v[7] if len(v) > 7 else "1")
     out = subprocess.run([sys.executable, "-c", _CP_SNIPPET.format(root=root, cases=cases)], env=env,
                          capture_output=True, text=True, timeout=600, check=True).stdout.split()
     want = [hashlib.sha256(oracle.build(synth.keys(n, 1000 * leaf + b), leaf, b, threads=os.cpu_count()))
