@@ -61,6 +61,7 @@ struct Args {
     u32 cp_last;   // full lower nodes: also reject when the last part already overflows (0 = off)
     u32 cp_wide;   // early rejection in the wide-counter kernel (l >= 19) too (0 = off)
     u32 cp_leaf2;  // leaves: second checkpoint (0 = single stage)
+    u32 cp_wide2;  // wide-counter splits: second checkpoint too (0 = single stage)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -443,7 +444,7 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
             // (wide counters: early rejection by field extraction, run_window_cp_wide)
             c.cp = c.full && cpg < (s >> 2) && ((f - 1) * w <= 31 || (WIDE && A.cp_wide)) ? cpg : 0;
             const u32 cpg2 = c.l2 ? A.cp_l2b : A.cp_l1b;
-            c.cp2 = c.cp && !WIDE && cpg2 >= cpg + 2 && cpg2 < (s >> 2) ? cpg2 : 0;  // a 1-group stage does not pay
+            c.cp2 = c.cp && (!WIDE || A.cp_wide2) && cpg2 >= cpg + 2 && cpg2 < (s >> 2) ? cpg2 : 0;  // a 1-group stage does not pay
             if (!c.wide) {
                 u32 t = 0;
                 for (u32 j = 0; j + 1 < f; ++j) t += unit << (j * w);
@@ -729,61 +730,88 @@ __device__ __forceinline__ bool wide_reject(u64 cnt, const NodeCtx& c, u32 k) {
     return over || sum + c.unit < k;
 }
 
-// The wide counterpart of run_window_cp (single stage): survivors queue as (seed, counter
-// low word, counter high word) in seed order and are completed 32 at a time; the first hit is
-// the smallest successful seed of the window (same argument as run_window_cp).
+// The wide counterpart of run_window_cp, with the same cascade of up to two checkpoints:
+// survivors queue as (seed, counter low word, counter high word) in seed order; stage 2 (when
+// c.cp2 is set) extends 32 of them to the second checkpoint and queues its survivors; the last
+// stage completes 32 at a time.  The first hit is the smallest successful seed of the window
+// (same argument as run_window_cp).
 template <int CL>
 __device__ __forceinline__ bool run_window_cp_wide(const Args& A, const KeysView& K, const NodeCtx& c, u64 wstart,
                                                    u32 lane, u32* qs, u64* val) {
     const u32 wrel = (u32)(wstart - c.kW);
-    const u32 g1 = c.cp, k1 = 4 * c.cp;
+    const u32 g1 = c.cp, g2 = c.cp2;
     u32* const qlo = qs + 64;
     u32* const qhi = qs + 128;
-    u32 qn = 0;
+    u32* const qs2 = qs + 192;
+    u32* const qlo2 = qs + 256;
+    u32* const qhi2 = qs + 320;
+    u32 qn = 0, qn2 = 0;
+    auto push = [&](bool keep, u32 sig, u64 cnt, u32* ds, u32* dl, u32* dh, u32& dn) {
+        const u32 bal = __ballot_sync(FULL, keep);
+        if (keep) {
+            const u32 pos = dn + __popc(bal & lanemask_lt());
+            ds[pos] = sig;
+            dl[pos] = (u32)cnt;
+            dh[pos] = (u32)(cnt >> 32);
+        }
+        dn += __popc(bal);
+        __syncwarp();
+    };
+    auto pop = [&](u32* ds, u32* dl, u32* dh, u32& dn, u32 nb) {
+        const u32 rest = dn - nb;
+        u32 x = 0, y = 0, z = 0;
+        if (lane < rest) {
+            x = ds[nb + lane];
+            y = dl[nb + lane];
+            z = dh[nb + lane];
+        }
+        __syncwarp();
+        if (lane < rest) {
+            ds[lane] = x;
+            dl[lane] = y;
+            dh[lane] = z;
+        }
+        __syncwarp();
+        dn = rest;
+    };
+    auto finish = [&](u32* fs, u32* fl, u32* fh, u32& fn, u32 nb, u32 gf) -> bool {
+        const bool have = lane < nb;
+        const u32 sig = have ? fs[lane] : 0;
+        u64 cnt = have ? (((u64)fh[lane] << 32) | fl[lane]) : 0;
+        cnt = count_lower_wide<0, CL, true>(K, c.s, sig, c.r, gf, 0xffffffffu, cnt);
+        const u32 bal = __ballot_sync(FULL, have && (cnt & c.mask64) == c.target64);
+        if (bal) {
+            *val = c.kW + __shfl_sync(FULL, sig, __ffs(bal) - 1);
+            return true;
+        }
+        __syncwarp();
+        pop(fs, fl, fh, fn, nb);
+        return false;
+    };
     for (u32 it = 0; it <= A.iters; ++it) {
         const bool last = it == A.iters;
         if (!last) {
             const u32 sig = wrel + it * 32 + lane;
             const u64 cnt = count_lower_wide<0, CL, false>(K, c.s, sig, c.r, 0, g1);
-            const bool keep = !wide_reject(cnt, c, k1);
-            const u32 bal = __ballot_sync(FULL, keep);
-            if (keep) {
-                const u32 pos = qn + __popc(bal & lanemask_lt());
-                qs[pos] = sig;
-                qlo[pos] = (u32)cnt;
-                qhi[pos] = (u32)(cnt >> 32);
-            }
-            qn += __popc(bal);
-            __syncwarp();
+            push(!wide_reject(cnt, c, 4 * g1), sig, cnt, qs, qlo, qhi, qn);
         }
         while (qn >= 32 || (last && qn > 0)) {
             const u32 nb = min(qn, 32u);
+            if (!g2) {
+                if (finish(qs, qlo, qhi, qn, nb, g1)) return true;
+                continue;
+            }
             const bool have = lane < nb;
             const u32 sig = have ? qs[lane] : 0;
             u64 cnt = have ? (((u64)qhi[lane] << 32) | qlo[lane]) : 0;
-            cnt = count_lower_wide<0, CL, true>(K, c.s, sig, c.r, g1, 0xffffffffu, cnt);
-            const u32 bal = __ballot_sync(FULL, have && (cnt & c.mask64) == c.target64);
-            if (bal) {
-                *val = c.kW + __shfl_sync(FULL, sig, __ffs(bal) - 1);
-                return true;
-            }
-            const u32 rest = qn - nb;
-            u32 x = 0, y = 0, z = 0;
-            __syncwarp();
-            if (lane < rest) {
-                x = qs[nb + lane];
-                y = qlo[nb + lane];
-                z = qhi[nb + lane];
-            }
-            __syncwarp();
-            if (lane < rest) {
-                qs[lane] = x;
-                qlo[lane] = y;
-                qhi[lane] = z;
-            }
-            __syncwarp();
-            qn = rest;
+            cnt = count_lower_wide<0, CL, false>(K, c.s, sig, c.r, g1, g2, cnt);
+            push(have && !wide_reject(cnt, c, 4 * g2), sig, cnt, qs2, qlo2, qhi2, qn2);
+            pop(qs, qlo, qhi, qn, nb);
+            if (qn2 >= 32 && finish(qs2, qlo2, qhi2, qn2, 32, g2)) return true;
         }
+        if (last)
+            while (qn2 > 0)
+                if (finish(qs2, qlo2, qhi2, qn2, min(qn2, 32u), g2)) return true;
     }
     return false;
 }
@@ -1071,6 +1099,8 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         A.cp_wide = cpw ? 1u : 0u;
         static const int cpl2 = getenv("RS_CPL2") ? atoi(getenv("RS_CPL2")) : 1;
         A.cp_leaf2 = cpl2 ? 1u : 0u;
+        static const int cpw2 = getenv("RS_CPW2") ? atoi(getenv("RS_CPW2")) : 1;
+        A.cp_wide2 = cpw2 ? 1u : 0u;
     }
     // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
     u32 cap = (P.max_size + 3) & ~3u;
