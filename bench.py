@@ -325,6 +325,15 @@ def main():
                      "lower2": st0["t_search"][1], "lower1": st0["t_search"][2], "leaves": st0["t_search"][3],
                      "reorder": st0["t_reorder"], "encode": st0["t_encode"], "d2h": st0["t_d2h"]},
         "algo_evals_per_step": [int(x) for x in st0["algo_evals"]],
+        # INT32 fraction per search phase: that phase's algorithmic evaluations /
+        # its CUDA-event time / the same peak; "step" = all evaluations / the whole step
+        "int32_frac_by_phase": {
+            nm: (float(np.mean([x["algo_evals"][k] for x in stats])) /
+                 float(np.mean([x["t_search"][k] for x in stats])) / 1e9 / peak)
+            if float(np.mean([x["t_search"][k] for x in stats])) > 0 else None
+            for k, nm in enumerate(["upper", "lower2", "lower1", "leaves"])},
+        "int32_frac_step": (float(np.mean([sum(x["algo_evals"]) for x in stats])) / t_max / 1e9 / peak)
+        if world == 1 else None,
         "clocks": clocks,
     }
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only
