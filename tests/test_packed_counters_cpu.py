@@ -76,3 +76,49 @@ def test_packed_overflow_and_last_part_tests_are_exact(leaf, unit, f, w):
             # field overflows its width; carries only move upward)
             if max(cnt_parts[: f - 1]) <= (1 << w) - 1:
                 assert flag != 0
+
+
+def part_shift(p, f, w):
+    """Field position of part p (narrow p*w; wide split words, 64 = not held)."""
+    if (f - 1) * w <= 32:
+        return p * w if p + 1 < f else 32
+    hs = 32 // w
+    return 64 if p + 1 >= f else (p * w if p < hs else 32 + (p - hs) * w)
+
+
+@pytest.mark.parametrize("leaf", range(19, 25))
+def test_wide_counter_field_extraction_is_exact(leaf):
+    """The wide (64-bit, two-word) packed counters of l >= 19 and their early-rejection test
+    (fields extracted one by one, k - sum > unit for the last part): a valid prefix is never
+    rejected and the test rejects exactly the prefixes with a part above unit; the final
+    comparison (cnt & mask) == target holds iff every part count equals unit."""
+    f1, f2, u1, u2 = shape(leaf)
+    rng = random.Random(leaf)
+    for unit, f in ((leaf, f1), (u1, f2)):
+        w = (unit + 1).bit_length()
+        if (f - 1) * w <= 32:
+            continue
+        fm = (1 << w) - 1
+        mask = sum(fm << part_shift(j, f, w) for j in range(f - 1))
+        target = sum(unit << part_shift(j, f, w) for j in range(f - 1))
+        s = f * unit
+        for trial in range(300):
+            k = rng.randrange(1, s + 1)
+            parts = [0] * f
+            for _ in range(k):
+                parts[rng.randrange(f)] += 1
+            lo = hi = 0
+            for p, c in enumerate(parts):  # increments 1 << t and 1 << (t - 32), clamped
+                t = part_shift(p, f, w)
+                lo = (lo + (c << t if t < 32 else 0)) & 0xFFFFFFFF
+                hi = (hi + (c << (t - 32) if 32 <= t < 64 else 0)) & 0xFFFFFFFF
+            cnt = (hi << 32) | lo
+            vals = [(cnt >> part_shift(j, f, w)) & fm for j in range(f - 1)]
+            reject = any(v > unit for v in vals) or sum(vals) + unit < k
+            valid = all(c <= unit for c in parts)
+            if valid:
+                assert not reject and vals == parts[: f - 1]
+            elif max(parts[: f - 1]) < (1 << w):  # no field overflowed its width: exact verdict
+                assert reject
+            if k == s:
+                assert ((cnt & mask) == target) == (parts == [unit] * f)
