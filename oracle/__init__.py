@@ -63,6 +63,8 @@ def lib():
         L.oracle_query_many.argtypes = [P8, u64, P64, u64, P64]
         L.oracle_free.restype, L.oracle_free.argtypes = None, [C.c_void_p]
         L.oracle_mhc_string.restype = None
+        L.oracle_murmur3_x64_128.restype = None
+        L.oracle_murmur3_x64_128.argtypes = [P8, u64, u32, P64, P64]
         L.oracle_mhc_string.argtypes = [P8, u64, u64, P64, P64]
         L.oracle_build_strings.restype = i32
         L.oracle_build_strings.argtypes = [P8, P64, u64, u32, u32, i32, u64, i32, C.POINTER(P8), C.POINTER(u64)]
@@ -208,6 +210,13 @@ def query_many(blob: bytes, keys) -> np.ndarray:
 
 def _p8(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def murmur3_x64_128(s: bytes, seed: int = 0) -> tuple[int, int]:
+    buf = np.frombuffer(s, dtype=np.uint8) if len(s) else np.zeros(1, np.uint8)
+    h1, h2 = C.c_uint64(), C.c_uint64()
+    lib().oracle_murmur3_x64_128(_p8(buf), len(s), seed, C.byref(h1), C.byref(h2))
+    return h1.value, h2.value
 
 
 def mhc_string(s: bytes, g: int = 0) -> tuple[int, int]:

@@ -19,11 +19,9 @@
  *                                    query-semantics search, statistics)
  *   build / encode / EF / query .... pinned (exhaustive bijectivity, decode
  *                                    round trip, bits/object vs paper)
- *   mhc_string (reading R16) ....... an invented definition (the paper names no
- *                                    string hash): pinned by properties only
- *                                    (no collisions on 2e4 strings, length and
- *                                    seed sensitivity, balanced A/B bit) --
- *                                    parity unpinned against the paper
+ *   mhc_string (reading R16) ....... MurmurHash3_x64_128 (the paper names no string
+ *                                    hash): pinned by the published SMHasher
+ *                                    verification value and test vectors
  *   seed values themselves ......... parity unpinned against the paper (no
  *                                    worked example exists); pinned only by the
  *                                    definitions above.
@@ -64,23 +62,85 @@ void oracle_mhc(u64 key, u64 g, u64 *hi, u64 *lo) {
     *lo = oracle_remix(key ^ g ^ 0xC2B2AE3D27D4EB4FULL);
 }
 
-/* Reading R16 (string keys; the paper's competitor workload P:386-388):
- * MHC of a byte string = two length-salted SplitMix64 chains over its 8-byte little-endian
- * chunks (last chunk zero-padded): h = seed ^ len*0x9E3779B97F4A7C15; h = remix(h ^ chunk)
- * per chunk; result remix(h).  hi uses seed g^C_HI, lo uses seed g^C_LO. */
-static u64 str_chain(const u8 *s, u64 len, u64 seed) {
-    u64 h = seed ^ (len * 0x9E3779B97F4A7C15ULL);
-    for (u64 i = 0; i < len; i += 8) {
-        u64 c = 0;
-        for (u64 t = 0; t < 8 && i + t < len; t++) c |= (u64)s[i + t] << (8 * t);
-        h = oracle_remix(h ^ c);
+/* Reading R16 (string keys; the paper's competitor workload P:386-388:
+ * "strings of uniform random length in [10, 50]" hashed with "a high quality hash
+ * function"): the master hash code of a byte string is MurmurHash3_x64_128 (Austin
+ * Appleby's published, public-domain 128-bit hash; algorithm restated step by step below),
+ * with seed = low 32 bits of g XOR its high 32 bits; hi = h1, lo = h2 (the two output words).
+ * Pinned by the SMHasher verification value 0x6384BA69 and published vectors
+ * (tests/test_oracle_pins.py). */
+static u64 mm3_rotl64(u64 x, int r) { return (x << r) | (x >> (64 - r)); }
+
+static u64 mm3_fmix64(u64 k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdULL;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ULL;
+    k ^= k >> 33;
+    return k;
+}
+
+/* little-endian u64 from bytes p[0..nb) (nb <= 8), missing bytes zero */
+static u64 mm3_le(const u8 *p, u64 nb) {
+    u64 x = 0;
+    for (u64 t = 0; t < nb; t++) x |= (u64)p[t] << (8 * t);
+    return x;
+}
+
+void oracle_murmur3_x64_128(const u8 *s, u64 len, u32 seed, u64 *h1_out, u64 *h2_out) {
+    const u64 c1 = 0x87c37b91114253d5ULL, c2 = 0x4cf5ad432745937fULL;
+    u64 h1 = seed, h2 = seed;
+    const u64 nblocks = len / 16;
+    /* body: 16-byte blocks as two little-endian words */
+    for (u64 i = 0; i < nblocks; i++) {
+        u64 k1 = mm3_le(s + 16 * i, 8), k2 = mm3_le(s + 16 * i + 8, 8);
+        k1 *= c1;
+        k1 = mm3_rotl64(k1, 31);
+        k1 *= c2;
+        h1 ^= k1;
+        h1 = mm3_rotl64(h1, 27);
+        h1 += h2;
+        h1 = h1 * 5 + 0x52dce729;
+        k2 *= c2;
+        k2 = mm3_rotl64(k2, 33);
+        k2 *= c1;
+        h2 ^= k2;
+        h2 = mm3_rotl64(h2, 31);
+        h2 += h1;
+        h2 = h2 * 5 + 0x38495ab5;
     }
-    return oracle_remix(h);
+    /* tail: the remaining len % 16 bytes; bytes 8..15 form k2, bytes 0..7 form k1 */
+    const u8 *tail = s + 16 * nblocks;
+    const u64 rest = len & 15;
+    if (rest > 8) {
+        u64 k2 = mm3_le(tail + 8, rest - 8);
+        k2 *= c2;
+        k2 = mm3_rotl64(k2, 33);
+        k2 *= c1;
+        h2 ^= k2;
+    }
+    if (rest > 0) {
+        u64 k1 = mm3_le(tail, rest < 8 ? rest : 8);
+        k1 *= c1;
+        k1 = mm3_rotl64(k1, 31);
+        k1 *= c2;
+        h1 ^= k1;
+    }
+    /* finalization */
+    h1 ^= len;
+    h2 ^= len;
+    h1 += h2;
+    h2 += h1;
+    h1 = mm3_fmix64(h1);
+    h2 = mm3_fmix64(h2);
+    h1 += h2;
+    h2 += h1;
+    *h1_out = h1;
+    *h2_out = h2;
 }
 
 void oracle_mhc_string(const u8 *s, u64 len, u64 g, u64 *hi, u64 *lo) {
-    *hi = str_chain(s, len, g ^ 0x9E3779B97F4A7C15ULL);
-    *lo = str_chain(s, len, g ^ 0xC2B2AE3D27D4EB4FULL);
+    oracle_murmur3_x64_128(s, len, (u32)g ^ (u32)(g >> 32), hi, lo);
 }
 
 /* Reading R3: "a hash function modulo l" as the fixed-point reduction
