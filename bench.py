@@ -36,14 +36,16 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
-PAPER_KEYS_PER_S = {"C3": 1.0e6}  # GPURecSplit RF, l=16 b=2000: 1.0 us/object on RTX 3090
+# the paper's own GPU figure, other hardware: context only, never the baseline (vs_baseline = null)
+PAPER_CONTEXT = {"C3": "GPURecSplit RF, l=16 b=2000: 1.0 us/object = 1.0e6 keys/s on an RTX 3090 incl. transfers (P:581)"}
 WORKLOAD_TEXT = {
     "C1": "C1: n=1e4 random u64 keys, l=8, b=100, rotation fitting",
     "C2": "C2: n=5e6 random u64 keys, l=8, b=100, rotation fitting",
     "C3": "C3: n=5e6 random u64 keys, l=16, b=2000, rotation fitting",
-    "C5": "C5: n=1e8 random u64 keys, l=12, b=1000, rotation fitting (strong scaling over ranks)",
+    "C5": "C5: n=1e8 random u64 keys, l=12, b=1000, rotation fitting",
 }
-STRONG = {"C5"}  # total keys fixed as N grows; the others: n keys per rank (weak scaling)
+# Scaling: strong by default (BASELINE.json: C3 "1 and 8 B200", C5 "sharded across 2/4/8"
+# -- the total key count is the config's n for every N); --weak builds N x n keys.
 
 
 def _peaks():
@@ -143,6 +145,7 @@ def main():
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--weak", action="store_true", help="n keys per rank (one MPHF of N x n keys)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -169,7 +172,7 @@ def main():
         print(json.dumps({
             "impl": "reference", "metric": "MPHF construction keys/s", "value": v, "unit": "keys/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot_t / max(1, args.steps), "higher_is_better": True, "scaling": "strong" if args.config in STRONG else "weak",
+            "ms_per_step": 1e3 * tot_t / max(1, args.steps), "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.config], "n": cfg["n"], "leaf": cfg["leaf"],
                        "bucket": cfg["bucket"]},
@@ -188,6 +191,10 @@ def main():
         dev_index = 0 if os.environ.get("RS_BENCH_SAME_DEVICE") else local
         torch.cuda.set_device(dev_index)
         dist.init_process_group(backend)
+        # rank check: every rank prints its communicator size and device (stderr)
+        nccl_v = ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None
+        print(f"[rank {rank}] backend={backend} world_size={dist.get_world_size()} nccl={nccl_v} "
+              f"device={torch.cuda.current_device()} ({torch.cuda.get_device_name()})", file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
@@ -196,7 +203,7 @@ def main():
     # buckets (bucket-range sharding).  Each rank starts from its own n-key slice of
     # the input; inside the build the keys are routed to their bucket owners with one
     # all-to-all, so per-rank memory and H2D stay at n keys.
-    strong = args.config in STRONG
+    strong = not args.weak
     n_total = cfg["n"] if strong else cfg["n"] * world
     keys_all = synth.keys(n_total, cfg["seed"])
     keys = keys_all[rank * n_total // world:(rank + 1) * n_total // world]
@@ -308,12 +315,16 @@ def main():
         "metric": "MPHF construction keys/s", "value": value, "unit": "keys/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": 1e3 * t_max,
         "higher_is_better": True, "scaling": "strong" if strong else "weak",
-        "vs_baseline": (value / PAPER_KEYS_PER_S[args.config]) if args.config in PAPER_KEYS_PER_S else None,
+        "vs_baseline": None,  # BASELINE.md publishes no B200 number for this metric
+        "paper_context": PAPER_CONTEXT.get(args.config),
         "dtype": "u64", "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.config], "n": n_total, "leaf": cfg["leaf"],
                    "bucket": cfg["bucket"], "keys_per_rank": len(keys), "l2": "flushed between steps",
                    "bits_per_key": rs.bits_per_key(blob),
-                   "parallelism": f"bucket-range shards x{world} (one MPHF)" if world > 1 else "1gpu"},
+                   "parallelism": f"bucket-range shards x{world} (one MPHF, work-balanced ranges)" if world > 1 else "1gpu",
+                   "comm": ({"backend": backend, "world_size": world,
+                             "nccl": ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None}
+                            if world > 1 else None)},
         "e2e": {"value": e2e_value, "unit": "keys/s", "h2d_bytes_per_step": int(n_total * 8),  # whole job
                 "d2h_bytes_per_step": len(blob)},
         "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) * (args.steps if world > 1 else 1),
@@ -338,9 +349,16 @@ def main():
     }
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only
         k, t, nb = cpu_sample(cfg, keys, args.cpu_budget, threads)
+        # threads = 1: the same oracle on one core, on whole buckets
+        # for about a third of the budget; per-key work is constant in n at fixed (l, b), so
+        # keys/s on the sample is the single-thread rate (a full C3 build would take ~2 h)
+        k1, t1, nb1 = cpu_sample(cfg, keys, args.cpu_budget / 3, 1)
         line["cpu_baseline"] = {"value": k / t, "unit": "keys/s", "cores": threads, "kind": "oracle",
                                 "sample": f"{nb} whole buckets ({k} keys) of the {args.config} workload, "
-                                          f"{threads} threads over contiguous buckets"}
+                                          f"{threads} threads over contiguous buckets",
+                                "single_thread": {"value": k1 / t1, "unit": "keys/s", "cores": 1,
+                                                  "sample": f"{nb1} whole buckets ({k1} keys), one thread",
+                                                  "full_build_s_extrapolated": cfg["n"] * t1 / k1}}
     print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()

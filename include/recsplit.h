@@ -77,6 +77,12 @@ typedef struct {
     uint64_t total_keys;       /* recsplit_shard_begin only: keys of the WHOLE sharded build when
                                   each rank passes just the keys it owns (routed with
                                   recsplit_route_keys); 0 = n (every rank passes all keys) */
+    const uint64_t *bucket_cuts; /* HOST, world + 1 global bucket indices or NULL: rank r owns
+                                  buckets [cuts[r], cuts[r+1]) (cuts[0] = 0, cuts[world] = B,
+                                  nondecreasing; e.g. from recsplit_balanced_cuts).  Used by
+                                  recsplit_shard_begin, recsplit_route_keys and virtual_shards.
+                                  NULL = equal bucket counts [floor(rB/W), floor((r+1)B/W)).
+                                  The output bytes do not depend on the cuts. */
 } recsplit_options;
 
 /* Per-build statistics (optional output). Times are device (CUDA event) seconds. */
@@ -101,7 +107,12 @@ typedef struct {
 /* Library version (format version is the header's u16 version = 1). */
 RECSPLIT_API int recsplit_version(void);
 
-/* Largest bucket (keys) the device path supports; larger buckets -> RECSPLIT_E_INVALID. */
+/* Largest bucket (keys) a build accepts: 65536.  Any bucket_size >= 1 is a valid argument
+ * (SURVEY 8(b)); the limit applies to the ACTUAL bucket sizes, which are Poisson(n/B) around
+ * bucket_size (so bucket_size up to about 60000 is safe).  It is not a search limit (nodes
+ * above the 8192-key shared-memory capacity run through a global-memory path): it bounds
+ * the per-size preorder templates (about 1.4 s / leaf_size nodes of 24 B for each distinct
+ * bucket size s) the node table is expanded from.  A larger bucket -> RECSPLIT_E_INVALID. */
 RECSPLIT_API uint32_t recsplit_max_bucket_keys(void);
 
 /*
@@ -215,7 +226,8 @@ RECSPLIT_API int recsplit_tau(uint32_t leaf_size, uint32_t s, uint32_t rotation_
 /*
  * Sharded construction (buckets are independent; contiguous bucket ranges per
  * worker; per-worker sequences concatenated and one Elias-Fano index over all buckets).
- * Rank r of `world` owns buckets [floor(r B / W), floor((r+1) B / W)), B = ceil(n / b).
+ * Rank r of `world` owns buckets [floor(r B / W), floor((r+1) B / W)), B = ceil(n / b), or
+ * [cuts[r], cuts[r+1]) with opt->bucket_cuts.
  * Every rank passes ALL n keys (DEVICE pointer, on its own device); the output bytes are
  * identical to recsplit_build's for any world size.  Protocol (collectives are the
  * caller's, e.g. torch.distributed over NCCL):
@@ -241,7 +253,8 @@ RECSPLIT_API int recsplit_stitch(const uint8_t *const *parts, const size_t *size
 RECSPLIT_API void recsplit_shard_free(recsplit_shard *sh); /* NULL-safe */
 
 /* Key routing for sharded builds: rank r of `world` owns the buckets
- * [floor(rB/world), floor((r+1)B/world)), B = ceil(total_keys / bucket_size) (R12), bucket =
+ * [floor(rB/world), floor((r+1)B/world)) (or [cuts[r], cuts[r+1]) with opt->bucket_cuts),
+ * B = ceil(total_keys / bucket_size) (R12), bucket =
  * remap(hi, B) of the master hash code (R2, R3, global_seed from opt).  Groups the n DEVICE
  * keys d_keys (this rank's slice of the input) by owner: d_out (DEVICE, n u64) receives the
  * keys for rank 0, then rank 1, ...; counts (HOST, world u64) the number per rank.  After an
@@ -251,6 +264,18 @@ RECSPLIT_API void recsplit_shard_free(recsplit_shard *sh); /* NULL-safe */
 RECSPLIT_API int recsplit_route_keys(const uint64_t *d_keys, size_t n, uint64_t total_keys,
                                      uint32_t bucket_size, const recsplit_options *opt, int32_t world,
                                      void *stream, uint64_t *d_out, uint64_t *counts);
+/* Work-balanced bucket ranges: d_hist (DEVICE, B = ceil(total_keys / bucket_size)
+ * u32, zeroed by the caller) += the number of this rank's n DEVICE keys in each global bucket
+ * (R2, R3; global_seed from opt).  Sum the ranks' histograms (an allreduce), then
+ * recsplit_balanced_cuts.  Enqueued on `stream` (no synchronisation). */
+RECSPLIT_API int recsplit_bucket_histogram(const uint64_t *d_keys, size_t n, uint64_t total_keys,
+                                           uint32_t bucket_size, const recsplit_options *opt, void *stream,
+                                           uint32_t *d_hist);
+/* cuts (HOST, world + 1) of contiguous bucket ranges with about equal expected remix
+ * evaluations (sum over each bucket's tree of size / success probability per node, from the
+ * bucket sizes hist[0..B) (HOST)); deterministic, so every rank computes the same cuts. */
+RECSPLIT_API int recsplit_balanced_cuts(const uint32_t *hist, uint64_t B, uint32_t leaf_size,
+                                        uint32_t rotation_fitting, int32_t world, uint64_t *cuts);
 /* Host arithmetic of step 3 (tests): out = {n, D, delta_C, beta, key_base, bit_base}. */
 RECSPLIT_API int recsplit_shard_globals(const uint64_t *summaries, int32_t world, int32_t rank,
                                         uint64_t out[6]);

@@ -26,7 +26,8 @@ SYMBOLS = [
     "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch", "recsplit_shard_free",
     "recsplit_shard_globals", "recsplit_query_device", "recsplit_build_strings", "recsplit_query_strings",
     "recsplit_open", "recsplit_handle_query_many", "recsplit_handle_query_device", "recsplit_close",
-    "recsplit_check_bijective_device", "recsplit_route_keys",
+    "recsplit_check_bijective_device", "recsplit_route_keys", "recsplit_bucket_histogram",
+    "recsplit_balanced_cuts",
 ]
 
 
@@ -43,7 +44,8 @@ class Bytes(C.Structure):
 class Options(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("rotation_fitting", C.c_uint32),
                 ("global_seed", C.c_uint64), ("device", C.c_int32), ("virtual_shards", C.c_uint32),
-                ("reserved", C.c_uint32), ("total_keys", C.c_uint64)]
+                ("reserved", C.c_uint32), ("total_keys", C.c_uint64),
+                ("bucket_cuts", C.POINTER(C.c_uint64))]
 
 
 class Stats(C.Structure):
@@ -121,6 +123,10 @@ def lib():
         L.recsplit_route_keys.argtypes = [C.c_void_p, sz, u64, u32, C.POINTER(Options), C.c_int32, C.c_void_p,
                                           C.c_void_p, P64]
         L.recsplit_route_keys.restype = i32
+        L.recsplit_bucket_histogram.argtypes = [C.c_void_p, sz, u64, u32, C.POINTER(Options), C.c_void_p, C.c_void_p]
+        L.recsplit_bucket_histogram.restype = i32
+        L.recsplit_balanced_cuts.argtypes = [P32, u64, u32, u32, C.c_int32, P64]
+        L.recsplit_balanced_cuts.restype = i32
         L.recsplit_close.argtypes = [C.c_void_p]
         L.recsplit_close.restype = None
         for name in ("recsplit_shard_begin", "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch",
@@ -144,9 +150,11 @@ def _p64(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_uint64))
 
 
-def _opts(rotation_fitting: bool, global_seed: int, device: int, virtual_shards: int, total_keys: int = 0):
+def _opts(rotation_fitting: bool, global_seed: int, device: int, virtual_shards: int, total_keys: int = 0,
+          cuts=None):
+    """Options struct; `cuts` (uint64 array of world + 1 bucket indices) must outlive the call."""
     return Options(C.sizeof(Options), int(bool(rotation_fitting)), global_seed, device, virtual_shards, 0,
-                   total_keys)
+                   total_keys, _p64(cuts) if cuts is not None else None)
 
 
 def _take(b: Bytes) -> bytes:
@@ -156,12 +164,14 @@ def _take(b: Bytes) -> bytes:
 
 
 def build(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool = True, global_seed: int = 0,
-          device: int = -1, virtual_shards: int = 0, stats: bool = False):
-    """Build from host keys (uint64 array).  Returns bytes (and a stats dict)."""
+          device: int = -1, virtual_shards: int = 0, stats: bool = False, cuts=None):
+    """Build from host keys (uint64 array).  Returns bytes (and a stats dict).  With
+    virtual_shards > 1, `cuts` (virtual_shards + 1 bucket indices) sets the shard ranges."""
     keys = np.ascontiguousarray(keys, dtype=np.uint64)
     b = Bytes()
     st = Stats()
-    o = _opts(rotation_fitting, global_seed, device, virtual_shards)
+    cuts = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.uint64)
+    o = _opts(rotation_fitting, global_seed, device, virtual_shards, cuts=cuts)
     _check(lib().recsplit_build_ex(_p64(keys), len(keys), leaf_size, bucket_size, C.byref(o), C.byref(b),
                                    C.byref(st)))
     blob = _take(b)
@@ -357,7 +367,8 @@ class Shard:
     """One rank's share of a sharded build (include/recsplit.h, recsplit_shard_*)."""
 
     def __init__(self, keys_tensor, leaf_size: int, bucket_size: int, rank: int, world: int,
-                 rotation_fitting: bool = True, global_seed: int = 0, stream=None, total_keys: int = 0):
+                 rotation_fitting: bool = True, global_seed: int = 0, stream=None, total_keys: int = 0,
+                 cuts=None):
         """keys_tensor: all keys (total_keys = 0), or exactly the keys this rank owns after
         route_keys + all-to-all (total_keys = the whole build's key count)."""
         import torch
@@ -368,7 +379,8 @@ class Shard:
             stream = torch.cuda.current_stream(keys_tensor.device)
         self._h = C.c_void_p()
         self.summary = np.zeros(8, dtype=np.uint64)
-        o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, 0, total_keys)
+        cuts = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.uint64)
+        o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, 0, total_keys, cuts)
         _check(lib().recsplit_shard_begin(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), leaf_size,
                                           bucket_size, C.byref(o), rank, world, C.c_void_p(stream.cuda_stream),
                                           C.byref(self._h), _p64(self.summary)))
@@ -437,7 +449,8 @@ def allreduce_min(x: int, group=None) -> int:
 
 
 def gather_parts(part: bytes, dst: int = 0, group=None):
-    """Variable-length byte parts to rank dst (list on dst, None elsewhere)."""
+    """Variable-length byte parts to rank dst only (list on dst, None elsewhere): the sizes
+    are all-gathered (one u64 per rank), the padded parts gathered to dst."""
     import torch
     import torch.distributed as dist
 
@@ -451,15 +464,44 @@ def gather_parts(part: bytes, dst: int = 0, group=None):
     buf = torch.zeros(mx, dtype=torch.uint8)
     buf[:len(part)] = torch.frombuffer(bytearray(part), dtype=torch.uint8)
     buf = buf.to(dev)
-    out = torch.empty(world * mx, dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(out, buf, group=group)
-    if dist.get_rank(group) != dst:
+    me = dist.get_rank(group)
+    dst_g = dist.get_global_rank(group, dst) if group is not None else dst
+    if me != dst:
+        dist.gather(buf, None, dst=dst_g, group=group)
         return None
-    host = out.cpu().numpy()
-    return [host[r * mx: r * mx + sizes[r]].tobytes() for r in range(world)]
+    outs = [torch.empty(mx, dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.gather(buf, outs, dst=dst_g, group=group)
+    return [outs[r][:sizes[r]].cpu().numpy().tobytes() for r in range(world)]
 
 
-def route_keys(keys_tensor, total_keys: int, bucket_size: int, world: int, global_seed: int = 0, stream=None):
+def bucket_histogram(keys_tensor, total_keys: int, bucket_size: int, global_seed: int = 0, stream=None,
+                     out=None):
+    """Per-global-bucket key counts of this rank's CUDA keys (int32 CUDA tensor of B)."""
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream(keys_tensor.device)
+    B = (total_keys + bucket_size - 1) // bucket_size
+    if out is None:
+        out = torch.zeros(B, dtype=torch.int32, device=keys_tensor.device)
+    o = _opts(True, global_seed, keys_tensor.device.index, 0)
+    _check(lib().recsplit_bucket_histogram(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), total_keys,
+                                           bucket_size, C.byref(o), C.c_void_p(stream.cuda_stream),
+                                           C.c_void_p(out.data_ptr())))
+    return out
+
+
+def balanced_cuts(hist, leaf_size: int, world: int, rotation_fitting: bool = True) -> np.ndarray:
+    """world + 1 bucket cuts with about equal expected work (recsplit_balanced_cuts)."""
+    h = np.ascontiguousarray(hist, dtype=np.uint32)
+    cuts = np.zeros(world + 1, dtype=np.uint64)
+    _check(lib().recsplit_balanced_cuts(h.ctypes.data_as(C.POINTER(C.c_uint32)), len(h), leaf_size,
+                                        int(rotation_fitting), world, _p64(cuts)))
+    return cuts
+
+
+def route_keys(keys_tensor, total_keys: int, bucket_size: int, world: int, global_seed: int = 0, stream=None,
+               cuts=None):
     """Group this rank's CUDA keys by the rank that owns their bucket (recsplit_route_keys):
     returns (keys grouped rank by rank, list of per-rank counts)."""
     import torch
@@ -468,7 +510,8 @@ def route_keys(keys_tensor, total_keys: int, bucket_size: int, world: int, globa
         stream = torch.cuda.current_stream(keys_tensor.device)
     out = torch.empty_like(keys_tensor)
     counts = np.zeros(world, dtype=np.uint64)
-    o = _opts(True, global_seed, keys_tensor.device.index, 0)
+    cuts = None if cuts is None else np.ascontiguousarray(cuts, dtype=np.uint64)
+    o = _opts(True, global_seed, keys_tensor.device.index, 0, cuts=cuts)
     _check(lib().recsplit_route_keys(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), total_keys,
                                      bucket_size, C.byref(o), world, C.c_void_p(stream.cuda_stream),
                                      C.c_void_p(out.data_ptr()), _p64(counts)))
@@ -505,24 +548,48 @@ def allreduce_sum(x: int, group=None) -> int:
     return int(t.item())
 
 
+def global_histogram(keys_tensor, total_keys: int, bucket_size: int, global_seed: int = 0, group=None,
+                     stream=None, distributed: bool = True) -> np.ndarray:
+    """Bucket sizes of the whole build (B entries, host): this rank's histogram, summed over
+    the group when each rank holds a slice (distributed=True, one allreduce of B int32)."""
+    import torch.distributed as dist
+
+    h = bucket_histogram(keys_tensor, total_keys, bucket_size, global_seed, stream)
+    if distributed and dist.get_world_size(group) > 1:
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(h, group=group)
+        else:
+            hc = h.cpu()
+            dist.all_reduce(hc, group=group)
+            h = hc
+    return h.cpu().numpy().astype(np.uint32)
+
+
 def build_sharded(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
-                  global_seed: int = 0, group=None, stream=None, distribute: bool = False):
+                  global_seed: int = 0, group=None, stream=None, distribute: bool = False, balance: bool = True):
     """Multi-GPU build of ONE MPHF over the torch.distributed group (one rank per GPU):
     bucket ranges per rank, allgather of summaries, allreduce-min of the residual step,
     parts gathered to rank 0 and stitched.  Returns the bytes on rank 0, None elsewhere.
     distribute=False: every rank passes ALL keys (each keeps its buckets);
     distribute=True: each rank passes its own slice of the input; the keys are routed to
-    their owners with one all-to-all."""
+    their owners with one all-to-all.
+    balance=True: contiguous bucket ranges of about equal expected work (bucket-size
+    histogram -> recsplit_balanced_cuts; one extra allreduce of B int32 when distributed);
+    False: equal bucket counts.  The output bytes are the same either way."""
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    total = 0
+    total = allreduce_sum(keys_tensor.numel(), group) if distribute else keys_tensor.numel()
+    cuts = None
+    if balance and world > 1:
+        hist = global_histogram(keys_tensor, total, bucket_size, global_seed, group, stream, distribute)
+        cuts = balanced_cuts(hist, leaf_size, world, rotation_fitting)
     if distribute:
-        total = allreduce_sum(keys_tensor.numel(), group)
-        routed, counts = route_keys(keys_tensor, total, bucket_size, world, global_seed, stream)
+        routed, counts = route_keys(keys_tensor, total, bucket_size, world, global_seed, stream, cuts)
         keys_tensor = exchange_keys(routed, counts, group)
         del routed
-    sh = Shard(keys_tensor, leaf_size, bucket_size, rank, world, rotation_fitting, global_seed, stream, total)
+    sh = Shard(keys_tensor, leaf_size, bucket_size, rank, world, rotation_fitting, global_seed, stream,
+               total if distribute else 0, cuts)
     try:
         allsum = exchange_summaries(sh.summary, group)
         step = allreduce_min(sh.min_step(allsum), group)

@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -21,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["scan.cu", "partition.cu", "search.cu", "encode.cu", "pipeline.cu", "query.cu", "tables.cpp", "format.cpp",
            "abi.cpp"]
-HEADERS = ["device.cuh", "kernels.h", "pipeline.h", "tables.h", "format.h"]
+HEADERS = ["device.cuh", "kernels.h", "pipeline.h", "tables.h", "format.h", "murmur3.h"]
 
 
 def _stale() -> bool:
@@ -39,9 +40,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     obj_dir = os.path.join(OUT_DIR, "obj")
     os.makedirs(obj_dir, exist_ok=True)
-    objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
-    for src in SOURCES:
+
+    def compile_one(src):
         path = os.path.join(CSRC, src)
         obj = os.path.join(obj_dir, src + ".o")
         cmd = [NVCC, *ARCH, *common, *EXTRA, "-c", path, "-o", obj]
@@ -53,7 +54,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose and (r.stdout or r.stderr):
             sys.stderr.write(r.stdout + r.stderr)
-        objs.append(obj)
+        return obj
+
+    # the translation units are independent: compile them concurrently
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
            "-Xlinker", "--exclude-libs,ALL", "-lpthread"]

@@ -16,6 +16,7 @@
 #include "../../include/recsplit.h"
 #include "pipeline.h"
 #include "format.h"
+#include "murmur3.h"
 #include "tables.h"
 
 namespace {
@@ -50,7 +51,7 @@ int check_args(size_t n, uint32_t leaf, uint32_t b) {
     return RECSPLIT_OK;
 }
 
-rs::BuildParams params_of(size_t n, uint32_t leaf, uint32_t b, const recsplit_options* opt) {
+rs::BuildParams params_of(size_t n, uint32_t leaf, uint32_t b, const recsplit_options* opt, int cuts_world = 0) {
     rs::BuildParams p;
     p.n = n;
     p.leaf = leaf;
@@ -67,6 +68,12 @@ rs::BuildParams params_of(size_t n, uint32_t leaf, uint32_t b, const recsplit_op
         p.device = opt->device;
         p.shards = opt->virtual_shards ? opt->virtual_shards : 1;
         if (opt->struct_size >= offsetof(recsplit_options, total_keys) + sizeof(uint64_t)) p.n_total = opt->total_keys;
+        if (opt->struct_size >= offsetof(recsplit_options, bucket_cuts) + sizeof(void*) && opt->bucket_cuts) {
+            // virtual shards (build_ex) or the caller's world (shard_begin / route_keys); an
+            // unsharded build ignores them
+            const int w = p.shards > 1 ? (int)p.shards : cuts_world;
+            if (w >= 1) p.cuts.assign(opt->bucket_cuts, opt->bucket_cuts + w + 1);
+        }
     }
     return p;
 }
@@ -187,16 +194,6 @@ bool skip_ones(const uint8_t* d, uint64_t D, uint64_t& pos, uint64_t cnt) {
     return true;
 }
 
-// master hash code of a string key (R16): two length-salted chains over 8-byte chunks
-uint64_t str_chain(const uint8_t* s, uint64_t len, uint64_t seed) {
-    uint64_t h = seed ^ (len * 0x9E3779B97F4A7C15ULL);
-    for (uint64_t i = 0; i < len; i += 8) {
-        uint64_t c = 0;
-        for (uint64_t t = 0; t < 8 && i + t < len; ++t) c |= (uint64_t)s[i + t] << (8 * t);
-        h = remix(h ^ c);
-    }
-    return remix(h);
-}
 
 int query_mhc(const Parsed& M, uint64_t hi, uint64_t lo, uint64_t* out);
 
@@ -287,7 +284,7 @@ extern "C" {
 
 int recsplit_version(void) { return 1; }
 
-uint32_t recsplit_max_bucket_keys(void) { return 8192; }
+uint32_t recsplit_max_bucket_keys(void) { return rs::kMaxBucketKeys; }
 
 int recsplit_build(const uint64_t* keys, size_t n, uint32_t leaf_size, uint32_t bucket_size, recsplit_bytes* out) {
     return build_host_keys(keys, n, leaf_size, bucket_size, nullptr, out, nullptr, nullptr, false);
@@ -505,8 +502,9 @@ int recsplit_query_strings(const uint8_t* mphf, size_t size, const uint8_t* data
         for (size_t i = 0; i < n; ++i) {
             const uint8_t* s = data + offsets[i];
             const uint64_t len = offsets[i + 1] - offsets[i];
-            rc = query_mhc(M, str_chain(s, len, M.g ^ 0x9E3779B97F4A7C15ULL),
-                           str_chain(s, len, M.g ^ 0xC2B2AE3D27D4EB4FULL), out + i);
+            uint64_t hi, lo;
+            rsm::mhc_string(s, len, M.g, hi, lo);
+            rc = query_mhc(M, hi, lo, out + i);
             if (rc) return rc;
         }
         return RECSPLIT_OK;
@@ -575,13 +573,14 @@ int recsplit_shard_begin(const uint64_t* d_keys, size_t n, uint32_t leaf_size, u
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) return fail(RECSPLIT_E_INVALID, "bad rank/world");
     // routed shards (opt->total_keys > 0) may hold no key at all; the build's count is checked
-    const bool routed = opt && opt->struct_size >= sizeof(recsplit_options) && opt->total_keys;
+    const bool routed =
+        opt && opt->struct_size >= offsetof(recsplit_options, total_keys) + sizeof(uint64_t) && opt->total_keys;
     if (routed && opt->total_keys < n) return fail(RECSPLIT_E_INVALID, "total_keys < n");
     int rc = check_args(routed ? opt->total_keys : n, leaf_size, bucket_size);
     if (rc) return rc;
     return guarded([&]() -> int {
         std::lock_guard<std::mutex> g(g_build_mu);
-        rs::BuildParams p = params_of(n, leaf_size, bucket_size, opt);
+        rs::BuildParams p = params_of(n, leaf_size, bucket_size, opt, world);
         select_device(p.device);
         auto* h = new recsplit_shard;
         try {
@@ -605,9 +604,36 @@ int recsplit_route_keys(const uint64_t* d_keys, size_t n, uint64_t total_keys, u
     if (total_keys < n || total_keys == 0 || total_keys >= (1ull << 32))
         return fail(RECSPLIT_E_INVALID, "total_keys must be in [max(n, 1), 2^32)");
     return guarded([&]() -> int {
-        rs::BuildParams p = params_of(total_keys, 2, bucket_size, opt);
+        rs::BuildParams p = params_of(total_keys, 2, bucket_size, opt, world);
         select_device(p.device);
-        rs::route_keys(d_keys, n, total_keys, bucket_size, p.g, (uint32_t)world, (cudaStream_t)stream, d_out, counts);
+        rs::route_keys(d_keys, n, total_keys, bucket_size, p.g, (uint32_t)world, p.cuts.empty() ? nullptr : p.cuts.data(),
+                       (cudaStream_t)stream, d_out, counts);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_bucket_histogram(const uint64_t* d_keys, size_t n, uint64_t total_keys, uint32_t bucket_size,
+                              const recsplit_options* opt, void* stream, uint32_t* d_hist) {
+    if (!d_hist || (!d_keys && n)) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    if (bucket_size == 0) return fail(RECSPLIT_E_INVALID, "bucket_size must be >= 1");
+    if (total_keys < n || total_keys == 0 || total_keys >= (1ull << 32))
+        return fail(RECSPLIT_E_INVALID, "total_keys must be in [max(n, 1), 2^32)");
+    return guarded([&]() -> int {
+        rs::BuildParams p = params_of(total_keys, 2, bucket_size, opt, 1);
+        select_device(p.device);
+        rs::bucket_histogram(d_keys, n, total_keys, bucket_size, p.g, (cudaStream_t)stream, d_hist);
+        return RECSPLIT_OK;
+    });
+}
+
+int recsplit_balanced_cuts(const uint32_t* hist, uint64_t B, uint32_t leaf_size, uint32_t rotation_fitting,
+                           int32_t world, uint64_t* cuts) {
+    if (!cuts || (!hist && B)) return fail(RECSPLIT_E_INVALID, "NULL argument");
+    if (world < 1) return fail(RECSPLIT_E_INVALID, "world must be >= 1");
+    if (leaf_size < 2 || leaf_size > 24) return fail(RECSPLIT_E_INVALID, "leaf_size must be in [2, 24]");
+    return guarded([&]() -> int {
+        const std::vector<uint64_t> c = rs::balanced_cuts(hist, B, leaf_size, rotation_fitting != 0, world);
+        memcpy(cuts, c.data(), 8 * c.size());
         return RECSPLIT_OK;
     });
 }

@@ -2,6 +2,7 @@
 // Elias-Fano sequences into C[] (bucket key offsets) and P[] (bucket bit offsets).
 #include "format.h"
 
+#include <algorithm>
 #include <cstring>
 
 #include "../../include/recsplit.h"
@@ -108,6 +109,28 @@ int parse_mphf(const uint8_t* blob, size_t size, Parsed& M, std::string* err) {
     if (smax > (1u << 20)) return fail(RECSPLIT_E_FORMAT, "bucket too large");
     M.smax = smax;
     M.T = get_tables(M.leaf, M.rf, (uint32_t)smax);
+    // Per-bucket structure (R15): the fixed parts take F(s) bits and the unary region that
+    // follows holds exactly N(s) terminating ones.  A query descends inside its bucket, reads
+    // at most F(s) fixed bits and skips at most N(s) ones, so with this check neither the
+    // host nor the device query (k_query) can read past the bucket, whatever the stored
+    // values are; a corrupt blob is rejected here with RECSPLIT_E_FORMAT.
+    const Tables& T = *M.T;
+    auto ones = [&](uint64_t a, uint64_t b) {  // one-bits of data in [a, b)
+        uint64_t c = 0;
+        while (a < b) {
+            const uint64_t w = word_at(M.data, a >> 6) >> (a & 63);
+            const uint64_t take = std::min<uint64_t>(64 - (a & 63), b - a);
+            c += __builtin_popcountll(take == 64 ? w : (w & ((1ull << take) - 1)));
+            a += take;
+        }
+        return c;
+    };
+    for (uint64_t i = 0; i < M.B; ++i) {
+        const uint64_t s = M.C[i + 1] - M.C[i];
+        const uint64_t u0 = M.P[i] + T.F[s];
+        if (u0 > M.P[i + 1] || ones(u0, M.P[i + 1]) != T.N[s])
+            return fail(RECSPLIT_E_FORMAT, "bucket encoding inconsistent with its size");
+    }
     return RECSPLIT_OK;
 }
 

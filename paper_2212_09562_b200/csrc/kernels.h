@@ -29,15 +29,16 @@ void launch_hash(const u64* keys, const u64* mhc, u64 n, u64 g, u64 B, u64 b0, u
                  u32* hist, cudaStream_t st);
 // string keys: master hash codes (R16) of data[off[i] .. off[i+1]) into mhc (2 u64 per key)
 void launch_mhc_strings(const u8* data, const u64* off, u64 n, u64 g, u64* mhc, cudaStream_t st);
-// exact duplicate check per bucket after the scatter (dup[0..1] zeroed)
-void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, cudaStream_t st);
+// exact duplicate check per bucket after the scatter (dup[0..1] zeroed); buckets above
+// kSmallBucketKeys use open-addressing tables in big_scratch (kDedupeBigBlocks * 2^ceil(log2(2 smax)) u64)
+constexpr u32 kDedupeBigBlocks = 64;
+void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, u64* big_scratch, cudaStream_t st);
 // max/min bucket size and the histogram of bucket sizes (size_hist zeroed, cap+1 entries)
 void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u32* size_hist, u32 cap,
                          cudaStream_t st);
 // scatter (lo, ab) to bucket order (cursor = copy of exclusive offsets)
 void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cursor, u64* lo2,
                     u8* ab2, cudaStream_t st);
-constexpr u32 kMaxBucketKeys = 8192;
 
 // ---- tree (encode.cu): node counts per bucket, node expansion into phase lists.
 void launch_bucket_counts(const u64* C, u64 B, const u32* N, const u32* phase_cnt, u32 NP,
@@ -71,8 +72,10 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st);
 u32 search_active_slots(int sm_count);
 
 // key redistribution after a split phase (A7), in place for the phase's nodes
+// (big_scratch: kReorderBigWarps * 2 * max_size u64 when max_size > 8192, else unused)
+constexpr u32 kReorderBigWarps = 64;
 void launch_reorder(const rsd::NodeRec* nodes, u32 n_nodes, const u64* values, u64* lo, u8* ab, u32 leaf,
-                    u32 u1, u32 u2, u32 max_size, int sm_count, cudaStream_t st);
+                    u32 u1, u32 u2, u32 max_size, int sm_count, u64* big_scratch, cudaStream_t st);
 
 // ---- encode (encode.cu), steps A10-A11.
 // bucket bit lengths: F(s) + N(s) + sum (x >> tau); also algorithmic-evals statistics

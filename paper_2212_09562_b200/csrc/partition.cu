@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "murmur3.h"
 #include "pipeline.h"
 
 namespace rs {
@@ -135,15 +136,18 @@ void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cur
 
 // Exact duplicate check after the scatter: equal keys have equal lo (remix is a bijection,
 // R2) and land in the same bucket, so each bucket inserts its lo values into an open-
-// addressing set in shared memory (0 marks an empty slot; lo == 0 is counted instead).
+// addressing set (0 marks an empty slot; lo == 0 is counted instead): in shared memory for
+// buckets of up to kSmallBucketKeys keys, in a per-block global table (BIG) above that.
 // dup[0] |= 1 on a repeated value, dup[1] += keys with lo == 0 (> 1 is a duplicate).
+template <bool BIG>
 __global__ void __launch_bounds__(256) k_dedupe(const u64* __restrict__ lo, const u64* __restrict__ C, u64 nb,
-                                                u32 slots, u32* dup) {
-    extern __shared__ unsigned long long tab[];
+                                                u32 dup_cap, u32* dup, unsigned long long* gtab) {
+    extern __shared__ unsigned long long stab[];
+    unsigned long long* tab = BIG ? gtab + (size_t)blockIdx.x * 2 * dup_cap : stab;
     for (u64 b = blockIdx.x; b < nb; b += gridDim.x) {
         const u64 c0 = C[b], s = C[b + 1] - c0;
         __syncthreads();
-        if (s < 2) continue;
+        if (s < 2 || (BIG ? s <= kSmallBucketKeys : s > kSmallBucketKeys)) continue;
         u32 ts = 64;
         while (ts < 2 * s) ts <<= 1;
         for (u32 i = threadIdx.x; i < ts; i += blockDim.x) tab[i] = 0;
@@ -166,40 +170,38 @@ __global__ void __launch_bounds__(256) k_dedupe(const u64* __restrict__ lo, cons
             }
         }
     }
-    (void)slots;
 }
 
-void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, cudaStream_t st) {
+void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, u64* big_scratch, cudaStream_t st) {
     if (nb == 0) return;
+    const u32 sm = std::min(smax, kSmallBucketKeys);
     u32 ts = 64;
-    while (ts < 2 * smax) ts <<= 1;
+    while (ts < 2 * sm) ts <<= 1;
     const size_t smem = (size_t)ts * 8;
-    cudaFuncSetAttribute(k_dedupe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dedupe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const u32 threads = smax <= 128 ? 128 : 256;
     unsigned grid = nb < 148ull * 64 ? (unsigned)nb : 148u * 64;
-    k_dedupe<<<grid, threads, smem, st>>>(lo, C, nb, ts, dup);
+    k_dedupe<false><<<grid, threads, smem, st>>>(lo, C, nb, 0, dup, nullptr);
     g_launches++;
+    if (smax > kSmallBucketKeys) {
+        u32 tb = 64;
+        while (tb < 2 * smax) tb <<= 1;  // per-block table of tb entries (dup_cap = tb / 2)
+        const unsigned g2 = nb < kDedupeBigBlocks ? (unsigned)nb : kDedupeBigBlocks;
+        k_dedupe<true><<<g2, 256, 0, st>>>(lo, C, nb, tb / 2, dup, (unsigned long long*)big_scratch);
+        g_launches++;
+    }
 }
 
 // String keys (reading R16): master hash code of bytes[off[i] .. off[i+1])
-// = two length-salted SplitMix64 chains over 8-byte little-endian chunks.  One thread per key.
-__device__ __forceinline__ u64 str_chain(const u8* __restrict__ s, u64 len, u64 seed) {
-    u64 h = seed ^ (len * 0x9E3779B97F4A7C15ULL);
-    for (u64 i = 0; i < len; i += 8) {
-        u64 c = 0;
-        const u64 m = len - i < 8 ? len - i : 8;
-        for (u64 t = 0; t < m; ++t) c |= (u64)s[i + t] << (8 * t);
-        h = remix64(h ^ c);
-    }
-    return remix64(h);
-}
-
+// = MurmurHash3_x64_128 (murmur3.h).  One thread per key.
 __global__ void k_mhc_strings(const u8* __restrict__ data, const u64* __restrict__ off, u64 n, u64 g,
                               u64* __restrict__ mhc) {
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 a = off[i], len = off[i + 1] - a;
-        mhc[2 * i] = str_chain(data + a, len, g ^ MHC_SALT_HI);
-        mhc[2 * i + 1] = str_chain(data + a, len, g ^ MHC_SALT_LO);
+        u64 hi, lo;
+        rsm::mhc_string(data + a, len, g, hi, lo);
+        mhc[2 * i] = hi;
+        mhc[2 * i + 1] = lo;
     }
 }
 
@@ -217,22 +219,29 @@ namespace rs {
 using namespace rsd;
 namespace {
 
-// owner rank of bucket i under the contiguous split [floor(rB/W), floor((r+1)B/W))
-__device__ __forceinline__ u32 owner_of(u64 i, u64 B, u32 W) {
-    u32 r = (u32)((i * W) / B);  // floor(rB/W) <= i for this r or r - 1
-    while (r + 1 < W && (B * (r + 1)) / W <= i) ++r;
-    while (r > 0 && (B * r) / W > i) --r;
-    return r;
+// owner rank of bucket i: the r with cuts[r] <= i < cuts[r+1] (ranks with an
+// empty range own nothing); cuts = world + 1 entries in shared memory
+__device__ __forceinline__ u32 owner_of(u64 i, const unsigned long long* cuts, u32 W) {
+    u32 lo = 0, hi = W;  // invariant: cuts[lo] <= i < cuts[hi]
+    while (hi - lo > 1) {
+        const u32 mid = (lo + hi) >> 1;
+        if (cuts[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    return lo;
 }
 
 // pass 1: keys per destination rank (block histogram in shared memory)
-__global__ void k_route_count(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 W, u64* __restrict__ counts) {
+__global__ void k_route_count(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 W, const u64* __restrict__ gcuts,
+                              u64* __restrict__ counts) {
     extern __shared__ unsigned long long rc[];
+    unsigned long long* cuts = rc + W;  // W + 1
     for (u32 i = threadIdx.x; i < W; i += blockDim.x) rc[i] = 0;
+    for (u32 i = threadIdx.x; i <= W; i += blockDim.x) cuts[i] = gcuts[i];
     __syncthreads();
     for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 h = remix64(keys[i] ^ g ^ MHC_SALT_HI);
-        atomicAdd(rc + owner_of(((h >> 32) * B) >> 32, B, W), 1ull);
+        atomicAdd(rc + owner_of(((h >> 32) * B) >> 32, cuts, W), 1ull);
     }
     __syncthreads();
     for (u32 i = threadIdx.x; i < W; i += blockDim.x)
@@ -241,11 +250,13 @@ __global__ void k_route_count(const u64* __restrict__ keys, u64 n, u64 g, u64 B,
 
 // pass 2: scatter every key to its destination's segment (cursor = segment start, advanced
 // with one atomic per destination per block)
-__global__ void k_route_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 W,
+__global__ void k_route_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 W, const u64* __restrict__ gcuts,
                                 u64* __restrict__ cursor, u64* __restrict__ out) {
     extern __shared__ unsigned long long rs_[];
-    unsigned long long* cnt = rs_;       // W
-    unsigned long long* base = rs_ + W;  // W
+    unsigned long long* cnt = rs_;           // W
+    unsigned long long* base = rs_ + W;      // W
+    unsigned long long* cuts = rs_ + 2 * W;  // W + 1
+    for (u32 i = threadIdx.x; i <= W; i += blockDim.x) cuts[i] = gcuts[i];
     const u64 per = (u64)blockDim.x * 8;
     for (u64 t0 = (u64)blockIdx.x * per; t0 < n; t0 += (u64)gridDim.x * per) {
         for (u32 i = threadIdx.x; i < W; i += blockDim.x) cnt[i] = 0;
@@ -258,7 +269,7 @@ __global__ void k_route_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 
             dst[q] = 0xffffffffu;
             if (i < n) {
                 const u64 h = remix64(keys[i] ^ g ^ MHC_SALT_HI);
-                dst[q] = owner_of(((h >> 32) * B) >> 32, B, W);
+                dst[q] = owner_of(((h >> 32) * B) >> 32, cuts, W);
                 pos[q] = atomicAdd(cnt + dst[q], 1ull);
             }
         }
@@ -273,22 +284,64 @@ __global__ void k_route_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 
     }
 }
 
+// per-bucket key counts of a rank's keys (work-balanced cuts)
+__global__ void k_bucket_hist(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32* __restrict__ hist,
+                              int smem_hist) {
+    extern __shared__ u32 bh[];
+    if (smem_hist) {
+        for (u32 i = threadIdx.x; i < B; i += blockDim.x) bh[i] = 0;
+        __syncthreads();
+    }
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 h = remix64(keys[i] ^ g ^ MHC_SALT_HI);
+        const u64 b = ((h >> 32) * B) >> 32;
+        atomicAdd((smem_hist ? bh : hist) + b, 1u);
+    }
+    if (smem_hist) {
+        __syncthreads();
+        for (u32 i = threadIdx.x; i < B; i += blockDim.x)
+            if (bh[i]) atomicAdd(hist + i, bh[i]);
+    }
+}
+
 }  // namespace
 
-void route_keys(const u64* d_keys, u64 n, u64 total, u32 bucket, u64 g, u32 world, cudaStream_t st, u64* d_out,
-                u64* counts) {
+void bucket_histogram(const u64* d_keys, u64 n, u64 total, u32 bucket, u64 g, cudaStream_t st, u32* d_hist) {
+    if (!n) return;
     const u64 B = (total + bucket - 1) / bucket;  // R12, global
-    u64* d = nullptr;
-    if (cudaMallocAsync(&d, 16 * (size_t)world, st) != cudaSuccess) throw Error(RECSPLIT_E_NOMEM, "route buffer");
+    const int smem_hist = B <= 12288;
+    const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>((n + 1023) / 1024, smem_hist ? 148ull * 2 : 148ull * 8));
+    cudaFuncSetAttribute(k_bucket_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    k_bucket_hist<<<grid, 1024, smem_hist ? B * 4 : 0, st>>>(d_keys, n, g, B, d_hist, smem_hist);
+    g_launches++;
+    if (cudaGetLastError() != cudaSuccess) throw Error(RECSPLIT_E_CUDA, "bucket histogram launch failed");
+}
+
+void route_keys(const u64* d_keys, u64 n, u64 total, u32 bucket, u64 g, u32 world, const u64* cuts_in,
+                cudaStream_t st, u64* d_out, u64* counts) {
+    const u64 B = (total + bucket - 1) / bucket;  // R12, global
+    std::vector<u64> cuts(world + 1);
+    if (cuts_in) {
+        if (cuts_in[0] != 0 || cuts_in[world] != B) throw Error(RECSPLIT_E_INVALID, "bucket_cuts must run from 0 to B");
+        for (u32 r = 0; r <= world; ++r) {
+            cuts[r] = cuts_in[r];
+            if (r && cuts[r] < cuts[r - 1]) throw Error(RECSPLIT_E_INVALID, "bucket_cuts must be nondecreasing");
+        }
+    } else {
+        for (u32 r = 0; r <= world; ++r) cuts[r] = B * r / world;
+    }
+    u64* d = nullptr;  // [counts W | cursors W | cuts W + 1]
+    if (cudaMallocAsync(&d, 8 * (3 * (size_t)world + 1), st) != cudaSuccess) throw Error(RECSPLIT_E_NOMEM, "route buffer");
     struct Free {
         u64* p;
         cudaStream_t s;
         ~Free() { cudaFreeAsync(p, s); }
     } fr{d, st};
     cudaMemsetAsync(d, 0, 8 * (size_t)world, st);
+    cudaMemcpyAsync(d + 2 * world, cuts.data(), 8 * (world + 1), cudaMemcpyHostToDevice, st);
     const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>((n + 1023) / 1024, 148ull * 4));
     if (n) {
-        k_route_count<<<grid, 1024, world * 8, st>>>(d_keys, n, g, B, world, d);
+        k_route_count<<<grid, 1024, (2 * world + 1) * 8, st>>>(d_keys, n, g, B, world, d + 2 * world, d);
         g_launches++;
     }
     if (cudaMemcpyAsync(counts, d, 8 * (size_t)world, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
@@ -299,7 +352,7 @@ void route_keys(const u64* d_keys, u64 n, u64 total, u32 bucket, u64 g, u32 worl
     cudaMemcpyAsync(d + world, start.data(), 8 * (size_t)world, cudaMemcpyHostToDevice, st);
     if (n) {
         const unsigned g2 = (unsigned)std::max<u64>(1, std::min<u64>((n + 8191) / 8192, 148ull * 4));
-        k_route_scatter<<<g2, 1024, world * 16, st>>>(d_keys, n, g, B, world, d + world, d_out);
+        k_route_scatter<<<g2, 1024, (3 * world + 1) * 8, st>>>(d_keys, n, g, B, world, d + 2 * world, d + world, d_out);
         g_launches++;
     }
     if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)

@@ -28,35 +28,62 @@ thread_local uint32_t g_launches = 0;
 
 namespace {
 
-// Stream-ordered device allocations released at scope exit.
+// The library's private stream-ordered memory pool per device (not the device's default
+// pool, which the rest of the process -- e.g. PyTorch -- may use).  It keeps up to
+// kPoolKeepBytes reserved between builds so repeated builds do not re-map memory; above
+// that, the driver returns the excess to the OS at the next synchronization.
+constexpr uint64_t kPoolKeepBytes = 8ull << 30;
+
+cudaMemPool_t device_pool(int dev) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    CK(cudaMemPoolCreate(&pool, &props));
+    uint64_t thr = kPoolKeepBytes;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    pools[dev] = pool;
+    return pool;
+}
+
+// Stream-ordered device allocations from the library pool, released at scope exit (or
+// earlier with release()).
 struct Arena {
     cudaStream_t st;
+    cudaMemPool_t pool;
     std::vector<void*> ptrs;
-    explicit Arena(cudaStream_t s) : st(s) {}
+    explicit Arena(cudaStream_t s) : st(s) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        pool = device_pool(dev);
+    }
     template <typename T>
     T* alloc(size_t count) {
         void* p = nullptr;
         size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-        CK(cudaMallocAsync(&p, bytes, st));
+        CK(cudaMallocFromPoolAsync(&p, bytes, pool, st));
         ptrs.push_back(p);
         return (T*)p;
+    }
+    void release(void* p) {  // stream-ordered free of one allocation before scope exit
+        auto it = std::find(ptrs.begin(), ptrs.end(), p);
+        if (it == ptrs.end()) return;
+        cudaFreeAsync(p, st);
+        ptrs.erase(it);
     }
     ~Arena() {
         for (void* p : ptrs) cudaFreeAsync(p, st);
     }
 };
 
-void init_device(int dev) {
-    static std::mutex mu;
-    static std::map<int, bool> done;
-    std::lock_guard<std::mutex> g(mu);
-    if (done[dev]) return;
-    cudaMemPool_t pool;
-    CK(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thr = UINT64_MAX;
-    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    done[dev] = true;
-}
+void init_device(int dev) { (void)device_pool(dev); }
 
 int sm_count(int dev) {
     int v = 0;
@@ -201,6 +228,20 @@ void phase_policy(const Tables& T, SearchKind kind, uint32_t typical, uint32_t& 
 // Elias-Fano sequences at their global bit positions.  stitch() ORs the slices of all
 // shards into the serialized MPHF; with one shard this is the plain single-GPU build.
 
+void shard_range(const BuildParams& p, uint64_t B, int rank, int world, uint64_t& b0, uint64_t& b1) {
+    if (p.cuts.empty()) {
+        b0 = B * (uint64_t)rank / (uint64_t)world;
+        b1 = B * (uint64_t)(rank + 1) / (uint64_t)world;
+        return;
+    }
+    if (p.cuts.size() != (size_t)world + 1 || p.cuts[0] != 0 || p.cuts[world] != B)
+        throw Error(RECSPLIT_E_INVALID, "bucket_cuts must have world + 1 entries from 0 to B");
+    for (int r = 0; r < world; ++r)
+        if (p.cuts[r] > p.cuts[r + 1]) throw Error(RECSPLIT_E_INVALID, "bucket_cuts must be nondecreasing");
+    b0 = p.cuts[rank];
+    b1 = p.cuts[rank + 1];
+}
+
 Globals compute_globals(const uint64_t* all, int world, int rank) {
     Globals G{};
     uint64_t mn = UINT64_MAX;
@@ -271,8 +312,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     const uint64_t ntot = p.n_total ? p.n_total : n;  // routed shards: the whole build's count
     const uint64_t B = (ntot + p.bucket - 1) / p.bucket;  // R12
     I.B = B;
-    I.b0 = B * (uint64_t)rank / (uint64_t)world;
-    I.b1 = B * (uint64_t)(rank + 1) / (uint64_t)world;
+    shard_range(p, B, rank, world, I.b0, I.b1);
     const uint64_t Bl = I.b1 - I.b0;
     I.Bl = Bl;
     int dev = 0;
@@ -301,7 +341,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     u64* cursor = A.alloc<u64>(Bl + 1);
     // [0] max, [1] min bucket size, [2] duplicate flag, [3] keys with lo == 0, [4] seed cap
     u32* small = A.alloc<u32>(8);
-    const uint32_t cap = kMaxBucketKeys;
+    const uint32_t cap = kSmallBucketKeys;  // sizes above it: second histogram pass below
     u32* size_hist_d = A.alloc<u32>(cap + 1);
     void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(Bl + 1, 1)) + 64);
     CK(cudaMemsetAsync(hist, 0, (Bl + 1) * 4, st));
@@ -339,17 +379,37 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     summary[SUM_KEYS] = nl;
     summary[SUM_MINB] = smin;
     S.max_bucket = smax;
-    if (smax > cap)
+    if (smax > kMaxBucketKeys)
         throw Error(RECSPLIT_E_INVALID, "bucket of " + std::to_string(smax) + " keys exceeds the supported maximum " +
-                                            std::to_string(cap) + " (use a smaller bucket_size)");
+                                            std::to_string(kMaxBucketKeys) + " (use a smaller bucket_size)");
+    if (smax > cap) {  // oversized buckets (bucket_size well above 8192): the full size histogram
+        u32* big_hist = A.alloc<u32>(smax + 1);
+        u32* mm2 = A.alloc<u32>(2);
+        CK(cudaMemsetAsync(big_hist, 0, (smax + 1) * 4, st));
+        launch_bucket_stats(hist, Bl, mm2, big_hist, smax, st);
+        CKL();
+        size_hist.assign(smax + 1, 0);
+        CK(cudaMemcpyAsync(size_hist.data(), big_hist, (smax + 1) * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    u64* big_scratch = nullptr;  // dedupe tables and reorder staging of oversized buckets
+    if (smax > kSmallBucketKeys) {
+        uint64_t tb = 64;
+        while (tb < 2ull * smax) tb <<= 1;
+        big_scratch = A.alloc<u64>(std::max<uint64_t>(kDedupeBigBlocks * tb, (uint64_t)kReorderBigWarps * 2 * smax));
+    }
     std::vector<uint8_t> present(smax + 1);
     for (uint32_t x = 0; x <= smax; ++x) present[x] = size_hist[x] != 0;
     u64* lo_a = A.alloc<u64>(nl);
     u8* ab_a = A.alloc<u8>(nl);
     launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
     CKL();
-    launch_dedupe(lo_a, C, Bl, smax, small + 2, st);
+    launch_dedupe(lo_a, C, Bl, smax, small + 2, big_scratch, st);
     CKL();
+    // the unsorted per-key arrays (13 B/key) are dead from here on
+    A.release(lo_t);
+    A.release(ab_t);
+    A.release(bkt);
     const int e1 = tm.mark();
 
     // ---- A3: node table --------------------------------------------------------
@@ -453,7 +513,8 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
         CKL();
         const int b = tm.mark();
         if (kind == SK_UPPER || kind == SK_LOWER) {
-            launch_reorder(nodes + poff[q], (u32)pcount[q], values_d, lo_a, ab_a, leaf, sh.u1, sh.u2, maxs, sms, st);
+            launch_reorder(nodes + poff[q], (u32)pcount[q], values_d, lo_a, ab_a, leaf, sh.u1, sh.u2, maxs, sms, big_scratch,
+                           st);
             CKL();
         }
         const int c = tm.mark();

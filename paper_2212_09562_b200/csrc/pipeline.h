@@ -11,6 +11,12 @@
 
 namespace rs {
 
+// Largest bucket a build accepts (the per-size preorder templates grow with the bucket size,
+// see include/recsplit.h recsplit_max_bucket_keys); buckets above 8192 keys run their upper
+// splits through k_search_upper_big / k_reorder_big and the dedupe through global tables.
+constexpr uint32_t kMaxBucketKeys = 1u << 16;
+constexpr uint32_t kSmallBucketKeys = 8192;  // size-histogram and shared-memory dedupe capacity
+
 struct Error : std::runtime_error {
     int code;
     Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
@@ -25,7 +31,11 @@ struct BuildParams {
     uint32_t shards;  // virtual shards (>= 1)
     bool strings = false;  // keys are precomputed master hash codes of strings (2 u64 each, R16)
     uint64_t n_total = 0;  // keys of the whole build (0 = n): routed shards hold only their own keys
+    std::vector<uint64_t> cuts;  // world + 1 bucket cuts (empty = equal bucket counts)
 };
+
+// the bucket range [b0, b1) of `rank` (cuts, else equal counts); validates the cuts
+void shard_range(const BuildParams& p, uint64_t B, int rank, int world, uint64_t& b0, uint64_t& b1);
 
 struct BuildOutput {
     std::vector<uint8_t> bytes;
@@ -75,7 +85,10 @@ void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::ve
 // build of `total` keys over `world` ranks (B = ceil(total / bucket)); d_out gets the keys
 // rank by rank, counts[r] (host) the number for rank r.  Synchronises st.
 void route_keys(const uint64_t* d_keys, uint64_t n, uint64_t total, uint32_t bucket, uint64_t g, uint32_t world,
-                cudaStream_t st, uint64_t* d_out, uint64_t* counts);
+                const uint64_t* cuts /*host, world + 1, or null*/, cudaStream_t st, uint64_t* d_out, uint64_t* counts);
+// d_hist[i] += keys of global bucket i (B = ceil(total / bucket) entries), enqueued on st
+void bucket_histogram(const uint64_t* d_keys, uint64_t n, uint64_t total, uint32_t bucket, uint64_t g,
+                      cudaStream_t st, uint32_t* d_hist);
 
 // string keys (R16): master hash codes of data[off[i] .. off[i+1]) into mhc (2 u64 per key)
 void launch_mhc_strings(const uint8_t* data, const uint64_t* off, uint64_t n, uint64_t g, uint64_t* mhc,

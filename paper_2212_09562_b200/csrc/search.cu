@@ -33,7 +33,8 @@ namespace {
 
 constexpr u32 kWarpsPerBlockMax = 4;
 constexpr u64 kSeedCap = 1ull << 40;  // diagnostic trial cap per node (R11)
-constexpr u32 kQWords = 384;          // per-warp early-rejection queues: two stages x 3 x 64 words
+constexpr u32 kQWords = 384;
+constexpr u32 kWarpKeyCap = 8192;     // largest node the warp engine holds in shared memory          // per-warp early-rejection queues: two stages x 3 x 64 words
 
 struct Args {
     const NodeRec* nodes;
@@ -985,6 +986,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             if (n0 >= hbase) break;
             const u32 n1 = min(n0 + A.batch, hbase);
             for (u32 n = n0; n < n1; ++n) {
+                if (KIND == SK_UPPER && A.nodes[n].size > kWarpKeyCap) continue;  // k_search_upper_big
                 load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c);
                 u64 val = 0;
                 for (u64 wstart = 0;; wstart += ws) {
@@ -1013,6 +1015,8 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             if (n >= nn) {
                 n = find_help(A, gw, lane, nn);
                 if (n == NONE) break;
+            } else if (KIND == SK_UPPER && A.nodes[n].size > kWarpKeyCap) {
+                continue;  // searched by k_search_upper_big
             }
             node = n;
             if (lane == 0) ((volatile int*)A.active)[gw] = (int)n;
@@ -1043,6 +1047,52 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
         u64 val;
         if (run_window<KIND, VAR>(A, K, c, wstart, lane, &val, QS, QC) && lane == 0)
             atomicMin((unsigned long long*)(A.values + c.slot), (unsigned long long)val);
+    }
+}
+
+// Upper splits of nodes above the warp engine's shared-memory capacity (kWarpKeyCap keys;
+// only buckets larger than that have such nodes, SURVEY 8(b) "bucket_size >= 1").  One block
+// per node, keys read from global memory (L2-resident); a window of 32 consecutive seeds per
+// step, warp i counting |{k : h_k < T}| for seed w + i (T = ceil(c0 2^32 / s), the same
+// predicate as count_left); the smallest seed of the first window with a hit is the minimal
+// seed.  These nodes need about sqrt(pi s / 2) trials (tens to hundreds), so this path is
+// not throughput-critical.
+__global__ void __launch_bounds__(1024) k_search_upper_big(const NodeRec* __restrict__ nodes, u32 n_nodes,
+                                                           const u64* __restrict__ lo, u64* __restrict__ values,
+                                                           u32 u2, u32* err, const u32* dup) {
+    __shared__ u32 s_hit;
+    const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    if (dup[0] || dup[1] > 1) return;
+    for (u32 n = blockIdx.x; n < n_nodes; n += gridDim.x) {
+        const NodeRec rec = nodes[n];
+        const u32 s = rec.size;
+        if (s <= kWarpKeyCap) continue;  // warp engine
+        const u32 c0 = (s / 2 + u2 - 1) / u2 * u2;  // R6
+        const u32 T = (u32)((((u64)c0 << 32) + s - 1) / s);
+        const u64* __restrict__ k = lo + rec.key_off;
+        u64 val = ~0ull;
+        for (u64 w = 0;; w += nwarps) {
+            if (w >= kSeedCap) {
+                if (threadIdx.x == 0) atomicOr(err, 1u);
+                val = w;
+                break;
+            }
+            if (threadIdx.x == 0) s_hit = NONE;
+            __syncthreads();
+            const u64 sigma = w + wib;
+            u32 cnt = 0;
+            for (u32 j = lane; j < s; j += 32) cnt += remix_hi(k[j] + sigma) < T;
+            cnt = __reduce_add_sync(FULL, cnt);
+            if (lane == 0 && cnt == c0) atomicMin(&s_hit, wib);
+            __syncthreads();
+            const u32 hit = s_hit;
+            __syncthreads();
+            if (hit != NONE) {
+                val = w + hit;
+                break;
+            }
+        }
+        if (threadIdx.x == 0) values[rec.slot] = val;
     }
 }
 
@@ -1102,8 +1152,13 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         static const int cpw2 = getenv("RS_CPW2") ? atoi(getenv("RS_CPW2")) : 1;
         A.cp_wide2 = cpw2 ? 1u : 0u;
     }
+    if (P.kind == SK_UPPER && P.max_size > kWarpKeyCap) {  // oversized upper nodes first
+        const u32 grid_big = std::min<u32>(P.n_nodes_host, (u32)P.sm_count * 2);
+        k_search_upper_big<<<grid_big, 1024, 0, st>>>(P.nodes, P.n_nodes_host, P.lo, P.values, P.u2, P.err, P.dup);
+        g_launches++;
+    }
     // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
-    u32 cap = (P.max_size + 3) & ~3u;
+    u32 cap = (std::min(P.max_size, kWarpKeyCap) + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
     const u32 GW = (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) ? 20 : 12;
@@ -1170,9 +1225,64 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
 // ------------------------------------------------------------------ reorder --
 
 // A7: stable partition of each split node's keys by child index with its found seed
-// (P:311-313), in place: one warp per node stages the node's (lo, A/B) in shared
-// memory, then writes every key to its child's sub-range (children occupy consecutive
-// sub-ranges in part order, so every child's keys are contiguous for the next phase).
+// (P:311-313), in place: one warp per node stages the node's (lo, A/B) (shared
+// memory; a global scratch slice for nodes above kReorderSmemCap keys), then writes every
+// key to its child's sub-range (children occupy consecutive sub-ranges in part order, so
+// every child's keys are contiguous for the next phase).
+constexpr u32 kReorderSmemCap = 8192;
+
+__device__ __forceinline__ void reorder_node(const NodeRec r, u64 sigma, u64* __restrict__ lo, u8* __restrict__ ab,
+                                             u64* slo, u8* sab, u32 leaf, u32 u1, u32 u2, u32 lane) {
+    const u32 s = r.size;
+    for (u32 j = lane; j < s; j += 32) {
+        slo[j] = lo[r.key_off + j];
+        sab[j] = ab[r.key_off + j];
+    }
+    __syncwarp();
+    u32 unit, f, c0 = 0;
+    const bool upper = s > u2;
+    if (upper) {
+        c0 = (s / 2 + u2 - 1) / u2 * u2;
+        f = 2;
+        unit = 0;
+    } else {
+        unit = s <= u1 ? leaf : u1;
+        f = (s + unit - 1) / unit;
+    }
+    u32 cnt[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) cnt[p] = 0;
+    const u32 lt = lanemask_lt();
+    for (u32 c = 0; c < s; c += 32) {
+        const u32 j = c + lane;
+        const bool valid = j < s;
+        u64 k = 0;
+        u8 b = 0;
+        u32 part = 0xff;
+        if (valid) {
+            k = slo[j];
+            b = sab[j];
+            const u32 v = __umulhi(remix_hi(k + sigma), s);
+            part = upper ? (v >= c0) : v / unit;
+        }
+        u32 dst = 0;
+#pragma unroll
+        for (u32 p = 0; p < 16; ++p) {
+            if (p < f) {
+                const u32 bal = __ballot_sync(FULL, part == p);
+                const u32 start = upper ? (p ? c0 : 0) : p * unit;
+                if (part == p) dst = start + cnt[p] + __popc(bal & lt);
+                cnt[p] += __popc(bal);
+            }
+        }
+        if (valid) {
+            lo[r.key_off + dst] = k;
+            ab[r.key_off + dst] = b;
+        }
+    }
+    __syncwarp();
+}
+
 __global__ void k_reorder(const NodeRec* __restrict__ nodes, u32 n_nodes, const u64* __restrict__ values,
                           u64* __restrict__ lo, u8* __restrict__ ab, u32 leaf, u32 u1, u32 u2, u32 cap) {
     extern __shared__ __align__(16) unsigned char rsm[];
@@ -1182,62 +1292,32 @@ __global__ void k_reorder(const NodeRec* __restrict__ nodes, u32 n_nodes, const 
     const u32 nwarps = gridDim.x * (blockDim.x >> 5);
     for (u32 n = blockIdx.x * (blockDim.x >> 5) + wib; n < n_nodes; n += nwarps) {
         const NodeRec r = nodes[n];
-        const u32 s = r.size;
-        const u64 sigma = values[r.slot];
-        for (u32 j = lane; j < s; j += 32) {
-            slo[j] = lo[r.key_off + j];
-            sab[j] = ab[r.key_off + j];
-        }
-        __syncwarp();
-        u32 unit, f, c0 = 0;
-        const bool upper = s > u2;
-        if (upper) {
-            c0 = (s / 2 + u2 - 1) / u2 * u2;
-            f = 2;
-            unit = 0;
-        } else {
-            unit = s <= u1 ? leaf : u1;
-            f = (s + unit - 1) / unit;
-        }
-        u32 cnt[16];
-#pragma unroll
-        for (int p = 0; p < 16; ++p) cnt[p] = 0;
-        const u32 lt = lanemask_lt();
-        for (u32 c = 0; c < s; c += 32) {
-            const u32 j = c + lane;
-            const bool valid = j < s;
-            u64 k = 0;
-            u8 b = 0;
-            u32 part = 0xff;
-            if (valid) {
-                k = slo[j];
-                b = sab[j];
-                const u32 v = __umulhi(remix_hi(k + sigma), s);
-                part = upper ? (v >= c0) : v / unit;
-            }
-            u32 dst = 0;
-#pragma unroll
-            for (u32 p = 0; p < 16; ++p) {
-                if (p < f) {
-                    const u32 bal = __ballot_sync(FULL, part == p);
-                    const u32 start = upper ? (p ? c0 : 0) : p * unit;
-                    if (part == p) dst = start + cnt[p] + __popc(bal & lt);
-                    cnt[p] += __popc(bal);
-                }
-            }
-            if (valid) {
-                lo[r.key_off + dst] = k;
-                ab[r.key_off + dst] = b;
-            }
-        }
-        __syncwarp();
+        if (r.size > cap) continue;  // k_reorder_big
+        reorder_node(r, values[r.slot], lo, ab, slo, sab, leaf, u1, u2, lane);
+    }
+}
+
+// nodes above the shared-memory capacity (upper splits of oversized buckets): the same
+// warp-per-node partition staged in a global scratch slice of `cap` keys per warp
+__global__ void k_reorder_big(const NodeRec* __restrict__ nodes, u32 n_nodes, const u64* __restrict__ values,
+                              u64* __restrict__ lo, u8* __restrict__ ab, u32 u2, u32 smem_cap, u32 cap,
+                              u64* __restrict__ scratch) {
+    const u32 lane = threadIdx.x & 31;
+    const u32 gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const u32 nwarps = gridDim.x * (blockDim.x >> 5);
+    u64* slo = scratch + (size_t)gw * cap * 2;  // cap u64 keys + cap bytes (rounded up)
+    u8* sab = reinterpret_cast<u8*>(slo + cap);
+    for (u32 n = gw; n < n_nodes; n += nwarps) {
+        const NodeRec r = nodes[n];
+        if (r.size <= smem_cap) continue;
+        reorder_node(r, values[r.slot], lo, ab, slo, sab, 0, 0, u2, lane);
     }
 }
 
 void launch_reorder(const NodeRec* nodes, u32 n_nodes, const u64* values, u64* lo, u8* ab, u32 leaf, u32 u1, u32 u2,
-                    u32 max_size, int sm_count, cudaStream_t st) {
+                    u32 max_size, int sm_count, u64* big_scratch, cudaStream_t st) {
     if (n_nodes == 0) return;
-    const u32 cap = (max_size + 15) & ~15u;
+    const u32 cap = (std::min(max_size, kReorderSmemCap) + 15) & ~15u;
     const size_t per_warp = (size_t)cap * 9;
     u32 wpb = 8;
     while (wpb > 1 && per_warp * wpb > 96 * 1024) --wpb;
@@ -1249,6 +1329,12 @@ void launch_reorder(const NodeRec* nodes, u32 n_nodes, const u64* values, u64* l
     blocks = std::min<u32>(blocks, (u32)(occ * sm_count));
     k_reorder<<<blocks, wpb * 32, per_warp * wpb, st>>>(nodes, n_nodes, values, lo, ab, leaf, u1, u2, cap);
     g_launches++;
+    if (max_size > kReorderSmemCap) {
+        // big_scratch holds kReorderBigWarps slices of 2 * max_size words
+        k_reorder_big<<<kReorderBigWarps / 4, 128, 0, st>>>(nodes, n_nodes, values, lo, ab, u2, cap, max_size,
+                                                          big_scratch);
+        g_launches++;
+    }
 }
 
 }  // namespace rs

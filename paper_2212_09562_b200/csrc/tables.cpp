@@ -100,6 +100,43 @@ int rice_tau(double p) {
     return best;
 }
 
+double expected_evals(const Shape& sh, bool rf, uint32_t s) {
+    if (s <= 1) return s;  // a size-1 leaf stores 0 without a search
+    if (s <= sh.leaf) {
+        const double p = leaf_probability(s, rf);
+        return rf ? 1.0 / p : (double)s / p;
+    }
+    uint32_t parts[64];
+    const int f = split_parts(sh, s, parts);
+    double e = (double)s / split_probability(sh, s);
+    for (int j = 0; j < f; ++j) e += expected_evals(sh, rf, parts[j]);
+    return e;
+}
+
+std::vector<uint64_t> balanced_cuts(const uint32_t* hist, uint64_t B, uint32_t leaf, bool rf, int world) {
+    const Shape sh = make_shape(leaf);
+    std::map<uint32_t, double> memo;
+    std::vector<double> pre(B + 1, 0.0);
+    for (uint64_t i = 0; i < B; ++i) {
+        const uint32_t s = hist[i];
+        auto it = memo.find(s);
+        if (it == memo.end()) it = memo.emplace(s, expected_evals(sh, rf, s)).first;
+        pre[i + 1] = pre[i] + it->second;
+    }
+    std::vector<uint64_t> cuts(world + 1, 0);
+    cuts[world] = B;
+    uint64_t i = 0;
+    for (int r = 1; r < world; ++r) {
+        const double target = pre[B] * r / world;
+        while (i < B && pre[i] < target) ++i;  // first cut point with prefix >= target
+        // take the nearer of i - 1 and i
+        uint64_t c = i;
+        if (c > 0 && target - pre[c - 1] < pre[c] - target) --c;
+        cuts[r] = std::max(c, cuts[r - 1]);
+    }
+    return cuts;
+}
+
 static void build_tables(Tables& T) {
     const Shape& sh = T.sh;
     const uint32_t S = T.S;

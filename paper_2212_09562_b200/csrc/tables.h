@@ -69,6 +69,16 @@ struct Tables {
     mutable std::unique_ptr<std::mutex> mu_{new std::mutex};
 };
 
+// Expected remix evaluations of a bucket of size s (SURVEY 8(d) unit): s/p(s) per split node,
+// 1/p per rotation-fitting leaf (m evaluations per base seed, 1/(m p) base seeds), m/p per
+// brute-force leaf, summed over the subtree.  Used to balance the ranks' bucket ranges.
+double expected_evals(const Shape& sh, bool rf, uint32_t s);
+
+// Contiguous bucket ranges for `world` ranks with about equal expected work: cuts[0] = 0,
+// cuts[world] = B, rank r owns [cuts[r], cuts[r+1]); hist[i] = size of global bucket i.
+// The output bytes do not depend on where the cuts fall.
+std::vector<uint64_t> balanced_cuts(const uint32_t* hist, uint64_t B, uint32_t leaf, bool rf, int world);
+
 // Built once per (leaf, rf) and grown on demand; cached process-wide.
 std::shared_ptr<const Tables> get_tables(uint32_t leaf, bool rf, uint32_t S);
 

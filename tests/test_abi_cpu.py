@@ -30,7 +30,7 @@ def test_header_symbols_exported():
     for name in declared:
         assert hasattr(L, name), name
     assert L.recsplit_version() == 1
-    assert L.recsplit_max_bucket_keys() == 8192
+    assert L.recsplit_max_bucket_keys() == 65536
 
 
 @pytest.mark.parametrize("leaf", [2, 3, 5, 8, 12, 16, 20, 24])
@@ -117,3 +117,33 @@ def test_host_handle_matches_blob_query():
         rs.Handle(blob[:-8])
     assert e.value.code == rs.E_FORMAT
     rs.lib().recsplit_close(None)
+
+
+def test_corrupt_blob_rejected_or_in_range():
+    """A corrupt blob never makes the query read past the data: every bucket's
+    unary region must hold exactly N(s) ones after its F(s) fixed bits (format.cpp), so a
+    flipped bit in a unary region -> RECSPLIT_E_FORMAT; a flipped fixed bit leaves a valid
+    structure whose queries stay in [0, n) (header contract).  Host parser = the same code
+    the GPU query's recsplit_open uses."""
+    keys = synth.keys(10_000, 1)
+    blob = oracle.build(keys, 8, 100)
+    n = len(keys)
+    rng = np.random.default_rng(5)
+    data_bits = int.from_bytes(blob[40:48], "little")
+    data_start = len(blob) - 8 * ((data_bits + 63) // 64)
+    rejected = 0
+    for _ in range(200):
+        b = bytearray(blob)
+        bit = int(rng.integers(0, data_bits))
+        b[data_start + bit // 8] ^= 1 << (bit % 8)
+        try:
+            q = rs.query_many(bytes(b), keys[:500])
+        except rs.RecSplitError as e:
+            assert e.code == rs.E_FORMAT
+            rejected += 1
+            continue
+        assert (q < n).all()
+    assert 0 < rejected < 200
+    # truncated / bit-flipped index words are rejected too
+    with pytest.raises(rs.RecSplitError):
+        rs.query_many(blob[:-8], keys[:10])

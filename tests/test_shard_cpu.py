@@ -56,8 +56,20 @@ def _decode(L, up, k):
     return ones - np.arange(k)
 
 
-def make_parts(blob, world):
-    """Cut the serialized MPHF into the parts the sharded pipeline would produce."""
+def bucket_sizes(blob):
+    """Bucket sizes C[i+1] - C[i] decoded from the EF index (independent reader)."""
+    h = _parse(blob)
+    B, dC = h["B"], h["dC"]
+    L, low, up = h["efs"][0]
+    hi = _decode(L, up, B + 1).astype(np.int64)
+    lo = np.array([sum(int(low[i * L + t]) << t for t in range(L)) for i in range(B + 1)], dtype=np.int64)
+    C = ((hi << L) | lo) + np.arange(B + 1) * dC
+    return np.diff(C)
+
+
+def make_parts(blob, world, cuts=None):
+    """Cut the serialized MPHF into the parts the sharded pipeline would produce (rank r owns
+    buckets [cuts[r], cuts[r+1]); default equal bucket counts)."""
     h = _parse(blob)
     n, B, D, dC, beta, dR = h["n"], h["B"], h["D"], h["dC"], h["beta"], h["dR"]
     (LC, cl, cu), (LP, pl, pu) = h["efs"]
@@ -72,7 +84,7 @@ def make_parts(blob, world):
     P = [int(Pp[i]) + i * dR + ((beta * C[i]) >> 20) for i in range(B + 1)]
     parts, summaries, steps = [], [], []
     for r in range(world):
-        b0, b1 = B * r // world, B * (r + 1) // world
+        b0, b1 = (B * r // world, B * (r + 1) // world) if cuts is None else (int(cuts[r]), int(cuts[r + 1]))
         last = r == world - 1
         cnt = b1 - b0 + (1 if last else 0)
         sizes = [C[i + 1] - C[i] for i in range(b0, b1)]
@@ -96,7 +108,7 @@ def make_parts(blob, world):
     return parts, np.array(summaries, dtype=np.uint64), steps, dR
 
 
-def _worker(rank, world, port, blob, q):
+def _worker(rank, world, port, blob, q, balanced=False):
     sys.path.insert(0, ROOT)
     import paper_2212_09562_b200 as rs
 
@@ -104,7 +116,8 @@ def _worker(rank, world, port, blob, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        parts, summaries, steps, dR = make_parts(blob, world)
+        cuts = rs.balanced_cuts(bucket_sizes(blob), blob[6], world) if balanced else None
+        parts, summaries, steps, dR = make_parts(blob, world, cuts)
         allsum = rs.exchange_summaries(summaries[rank])
         assert np.array_equal(allsum, summaries)
         g = rs.shard_globals(allsum, world, rank)
@@ -118,8 +131,8 @@ def _worker(rank, world, port, blob, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_sharded_exchange_and_stitch(world):
+@pytest.mark.parametrize("world,balanced", [(2, False), (2, True)])
+def test_gloo_sharded_exchange_and_stitch(world, balanced):
     sys.path.insert(0, ROOT)
     import oracle
     import synth
@@ -129,7 +142,8 @@ def test_gloo_sharded_exchange_and_stitch(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29500 + os.getpid() % 1000
-    procs = [ctx.Process(target=_worker, args=(r, world, port, blob, q)) for r in range(world)]
+    port += 7 * balanced
+    procs = [ctx.Process(target=_worker, args=(r, world, port, blob, q, balanced)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -207,3 +221,40 @@ def test_gloo_key_exchange_delivers_owned_keys(world):
     for r in range(world):
         want = sorted(int(k) for k in keys if _owner(k, B, world) == r)
         assert res[r] == want
+
+
+def _expected_evals_oracle(leaf, s, rf):
+    """SURVEY 8(d) unit written out with the oracle's probabilities: s / p per split node,
+    1/p per rotation-fitting leaf, m/p per brute-force leaf, over the subtree."""
+    import oracle
+    if s <= 1:
+        return float(s)
+    if s <= leaf:
+        p = oracle.bij_prob(s, rf)
+        return 1.0 / p if rf else s / p
+    return s / oracle.split_prob(leaf, s) + sum(_expected_evals_oracle(leaf, c, rf) for c in oracle.parts(leaf, s))
+
+
+@pytest.mark.parametrize("leaf,b,world", [(16, 2000, 8), (8, 100, 4), (12, 1000, 3), (5, 5, 8)])
+def test_balanced_cuts_equalise_expected_work(leaf, b, world):
+    """SURVEY 8(e) work-balanced bucket ranges: recsplit_balanced_cuts returns world + 1
+    nondecreasing cuts from 0 to B, and every rank's expected work (computed here from the
+    oracle's split / leaf probabilities) is within one bucket's work of the ideal share."""
+    sys.path.insert(0, ROOT)
+    import oracle
+    import paper_2212_09562_b200 as rs
+    import synth
+
+    n = 400 * b if b >= 100 else 4000
+    keys = synth.keys(n, 3)
+    B = (n + b - 1) // b
+    hi = np.array([oracle.mhc(int(k))[0] for k in keys], dtype=np.uint64)
+    bucket = ((hi >> np.uint64(32)) * np.uint64(B)) >> np.uint64(32)
+    hist = np.bincount(bucket.astype(np.int64), minlength=B).astype(np.uint32)
+    cuts = rs.balanced_cuts(hist, leaf, world)
+    assert cuts[0] == 0 and cuts[-1] == B and (np.diff(cuts.astype(np.int64)) >= 0).all()
+    memo = {}
+    w = np.array([memo.setdefault(int(s), _expected_evals_oracle(leaf, int(s), True)) for s in hist])
+    per = [w[cuts[r]:cuts[r + 1]].sum() for r in range(world)]
+    ideal = w.sum() / world
+    assert max(abs(x - ideal) for x in per) <= w.max() + 1e-6 * ideal
