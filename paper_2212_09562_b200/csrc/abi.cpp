@@ -98,6 +98,12 @@ int emit(const rs::BuildOutput& o, recsplit_bytes* out) {
     return RECSPLIT_OK;
 }
 
+#define CK_RT(x)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (x);                                                                      \
+        if (e_ != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, cudaGetErrorString(e_));           \
+    } while (0)
+
 int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, const recsplit_options* opt,
                     recsplit_bytes* out, recsplit_stats* stats, rs::BuildOutput* keep, bool want_values) {
     if (!out) return fail(RECSPLIT_E_INVALID, "out is NULL");
@@ -118,20 +124,43 @@ int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, c
             cudaStream_t s;
             ~StreamGuard() { cudaStreamDestroy(s); }
         } sg{st};
+        int dev = 0;
+        cudaGetDevice(&dev);
         uint64_t* d_keys = nullptr;
-        cudaError_t e = cudaMallocAsync(&d_keys, n * 8, st);
+        cudaError_t e = cudaMallocFromPoolAsync((void**)&d_keys, n * 8, rs::device_pool(dev), st);
         if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_NOMEM, "device allocation of keys failed");
         struct KeyGuard {
             uint64_t* p;
             cudaStream_t s;
             ~KeyGuard() { cudaFreeAsync(p, s); }
         } kg{d_keys, st};
+        // pinned host keys of an unsharded build are streamed in chunks overlapped with the
+        // hash kernel; pageable ones are copied in one piece first
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, keys) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        const bool stream_keys = pinned && p.shards <= 1;
+        cudaStream_t cs = nullptr;
+        if (stream_keys && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+            throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
+        struct CopyStreamGuard {
+            cudaStream_t s;
+            ~CopyStreamGuard() {
+                if (s) cudaStreamDestroy(s);
+            }
+        } csg{cs};
         cudaEvent_t a, z;
         cudaEventCreate(&a);
         cudaEventCreate(&z);
         cudaEventRecord(a, st);
-        e = cudaMemcpyAsync(d_keys, keys, n * 8, cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, cudaGetErrorString(e));
+        if (stream_keys) {
+            p.h_keys = keys;
+            p.copy_stream = cs;
+            CK_RT(cudaStreamWaitEvent(cs, a, 0));  // the key buffer's allocation is ordered on st
+        } else {
+            e = cudaMemcpyAsync(d_keys, keys, n * 8, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, cudaGetErrorString(e));
+        }
         cudaEventRecord(z, st);
         rs::BuildOutput local;
         rs::BuildOutput& o = keep ? *keep : local;

@@ -67,8 +67,12 @@ struct PhaseLaunch {
     u32 iters;      // 32-seed iterations per window
     int help;
     int sm_count;
+    int fuse_reorder = 0;   // split phases: may redistribute the keys in the search kernel (A7)
+    u64* lo_w = nullptr;    // ... into these arrays (the phase's key arrays)
+    u8* ab_w = nullptr;
 };
-void launch_search(const PhaseLaunch& P, cudaStream_t st);
+// returns true if the phase's key redistribution was fused into the search (no launch_reorder)
+bool launch_search(const PhaseLaunch& P, cudaStream_t st);
 u32 search_active_slots(int sm_count);
 
 // key redistribution after a split phase (A7), in place for the phase's nodes

@@ -34,7 +34,7 @@ namespace {
 // that, the driver returns the excess to the OS at the next synchronization.
 constexpr uint64_t kPoolKeepBytes = 8ull << 30;
 
-cudaMemPool_t device_pool(int dev) {
+cudaMemPool_t device_pool_impl(int dev) {
     static std::mutex mu;
     static std::map<int, cudaMemPool_t> pools;
     std::lock_guard<std::mutex> g(mu);
@@ -62,7 +62,7 @@ struct Arena {
     explicit Arena(cudaStream_t s) : st(s) {
         int dev = 0;
         CK(cudaGetDevice(&dev));
-        pool = device_pool(dev);
+        pool = device_pool_impl(dev);
     }
     template <typename T>
     T* alloc(size_t count) {
@@ -83,7 +83,7 @@ struct Arena {
     }
 };
 
-void init_device(int dev) { (void)device_pool(dev); }
+void init_device(int dev) { (void)device_pool_impl(dev); }
 
 int sm_count(int dev) {
     int v = 0;
@@ -242,6 +242,8 @@ void shard_range(const BuildParams& p, uint64_t B, int rank, int world, uint64_t
     b1 = p.cuts[rank + 1];
 }
 
+cudaMemPool_t device_pool(int dev) { return device_pool_impl(dev); }
+
 Globals compute_globals(const uint64_t* all, int world, int rank) {
     Globals G{};
     uint64_t mn = UINT64_MAX;
@@ -357,9 +359,29 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
         S.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
         return;
     }
-    launch_hash(p.strings ? nullptr : d_keys, p.strings ? d_keys : nullptr, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt,
-                hist, st);
-    CKL();
+    if (p.h_keys && !p.strings) {
+        // A1 overlapped with the host->device copy: chunk c is copied on the copy stream while
+        // the hash kernel works on chunk c - 1 (chunked H2D with hashing)
+        const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
+        std::vector<cudaEvent_t> evs;
+        for (uint64_t off = 0; off < n; off += chunk) {
+            const uint64_t len = std::min(chunk, n - off);
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            evs.push_back(ev);
+            CK(cudaMemcpyAsync(const_cast<uint64_t*>(d_keys) + off, p.h_keys + off, len * 8, cudaMemcpyHostToDevice,
+                               p.copy_stream));
+            CK(cudaEventRecord(ev, p.copy_stream));
+            CK(cudaStreamWaitEvent(st, ev, 0));
+            launch_hash(d_keys + off, nullptr, len, p.g, B, I.b0, I.b1, lo_t + off, ab_t + off, bkt + off, hist, st);
+            CKL();
+        }
+        for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // released once complete
+    } else {
+        launch_hash(p.strings ? nullptr : d_keys, p.strings ? d_keys : nullptr, n, p.g, B, I.b0, I.b1, lo_t, ab_t, bkt,
+                    hist, st);
+        CKL();
+    }
     launch_bucket_stats(hist, Bl, small, size_hist_d, cap, st);
     CKL();
     exscan_u32_to_u64(hist, C, Bl, scan_tmp, st);
@@ -508,11 +530,14 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
         phase_policy(T, kind, typical, P.iters, P.help);
         P.sm_count = sms;
         CK(cudaMemsetAsync(active, 0xff, nslots * 4, st));
+        P.fuse_reorder = kind == SK_UPPER || kind == SK_LOWER;
+        P.lo_w = lo_a;
+        P.ab_w = ab_a;
         const int a = tm.mark();
-        launch_search(P, st);
+        const bool fused = launch_search(P, st);
         CKL();
         const int b = tm.mark();
-        if (kind == SK_UPPER || kind == SK_LOWER) {
+        if ((kind == SK_UPPER || kind == SK_LOWER) && !fused) {
             launch_reorder(nodes + poff[q], (u32)pcount[q], values_d, lo_a, ab_a, leaf, sh.u1, sh.u2, maxs, sms, big_scratch,
                            st);
             CKL();

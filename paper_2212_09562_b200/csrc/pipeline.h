@@ -32,7 +32,14 @@ struct BuildParams {
     bool strings = false;  // keys are precomputed master hash codes of strings (2 u64 each, R16)
     uint64_t n_total = 0;  // keys of the whole build (0 = n): routed shards hold only their own keys
     std::vector<uint64_t> cuts;  // world + 1 bucket cuts (empty = equal bucket counts)
+    // host keys streamed in chunks (pinned memory, single shard): d_keys is the destination
+    // buffer; chunk c is copied on copy_stream while the hash kernel runs on chunk c - 1
+    const uint64_t* h_keys = nullptr;
+    cudaStream_t copy_stream = nullptr;
 };
+
+// the library's stream-ordered memory pool on device dev (kept reserved between builds)
+cudaMemPool_t device_pool(int dev);
 
 // the bucket range [b0, b1) of `rank` (cuts, else equal counts); validates the cuts
 void shard_range(const BuildParams& p, uint64_t B, int rank, int world, uint64_t& b0, uint64_t& b1);

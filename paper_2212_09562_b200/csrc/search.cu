@@ -63,6 +63,9 @@ struct Args {
     u32 cp_wide;   // early rejection in the wide-counter kernel (l >= 19) too (0 = off)
     u32 cp_leaf2;  // leaves: second checkpoint (0 = single stage)
     u32 cp_wide2;  // wide-counter splits: second checkpoint too (0 = single stage)
+    u64* lo_w;     // fused redistribution (batch-mode split phases, nodes <= kFuseMax keys): the
+    u8* ab_w;      // key arrays written in child order right after the node's search; null = off
+    u32 upper_kp;  // upper splits in batch mode: keys-parallel sequential seeds (upper_keys_parallel)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -885,6 +888,92 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, Nod
     return false;
 }
 
+// A7 fused into the batch-mode split search: the warp that found the node's seed still holds
+// its keys (shared memory, natural order, possibly rebased by kW) and writes them in child
+// order -- the stable partition of reorder_node, without a separate pass over the keys.  The
+// node's A/B bytes are read into registers before any write (the node's range is rewritten in
+// place).
+constexpr u32 kFuseMax = 256;
+
+template <int KIND>
+__device__ __forceinline__ void fused_reorder(const Args& A, const u32* G, u32 key_off, const NodeCtx& c, u64 val,
+                                              u32 lane) {
+    constexpr u32 GW = Layout<KIND>::GW;
+    const u32 s = c.s;
+    u8 abv[kFuseMax / 32];
+#pragma unroll
+    for (u32 q = 0; q < kFuseMax / 32; ++q) abv[q] = q * 32 + lane < s ? A.ab[key_off + q * 32 + lane] : 0;
+    __syncwarp();
+    u32 unit = 0, f, c0 = 0;
+    const bool upper = KIND == SK_UPPER;
+    if (upper) {
+        c0 = c.target;
+        f = 2;
+    } else {
+        unit = c.unit;
+        f = c.f;
+    }
+    u32 cnt[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) cnt[p] = 0;
+    const u32 lt = lanemask_lt();
+#pragma unroll
+    for (u32 q = 0; q < kFuseMax / 32; ++q) {
+        const u32 j = q * 32 + lane;
+        if (q * 32 >= s) break;
+        const bool valid = j < s;
+        u64 k = 0;
+        u32 part = 0xff;
+        if (valid) {
+            const u32* g = G + GW * (j >> 2) + (j & 3);
+            k = (((u64)g[4] << 32) | g[0]) - c.kW;  // undo the key rebase
+            const u32 v = __umulhi(remix_hi(k + val), s);
+            part = upper ? (v >= c0) : v / unit;
+        }
+        u32 dst = 0;
+#pragma unroll
+        for (u32 p = 0; p < 16; ++p) {
+            if (p < f) {
+                const u32 bal = __ballot_sync(FULL, part == p);
+                const u32 start = upper ? (p ? c0 : 0) : p * unit;
+                if (part == p) dst = start + cnt[p] + __popc(bal & lt);
+                cnt[p] += __popc(bal);
+            }
+        }
+        if (valid) {
+            A.lo_w[key_off + dst] = k;
+            A.ab_w[key_off + dst] = abv[q];
+        }
+    }
+    __syncwarp();
+}
+
+// Upper split, keys in parallel (batch mode): an upper node needs few trials (about
+// sqrt(pi s / 2) at most; 5-17 for the ~100-200-key nodes of l = 8, b = 100), so a 32-seed
+// window wastes most of its work.  Here the lanes share the node's keys and the seeds
+// sigma = 0, 1, 2, ... are tried one after another: count |{k : h_k < T}| by ballots, the
+// first sigma with count c0 is the minimal seed (R6).
+__device__ __forceinline__ u64 upper_keys_parallel(const Args& A, const u32* G, const NodeCtx& c, u32 lane) {
+    constexpr u32 GW = Layout<SK_UPPER>::GW;
+    const u32 s = c.s;
+    for (u64 sigma = 0; sigma < kSeedCap; ++sigma) {
+        u32 cnt = 0;
+        for (u32 j0 = 0; j0 < s; j0 += 32) {
+            const u32 j = j0 + lane;
+            bool left = false;
+            if (j < s) {
+                const u32* g = G + GW * (j >> 2) + (j & 3);
+                const u64 k = (((u64)g[4] << 32) | g[0]) - c.kW;
+                left = remix_hi(k + sigma) < c.mask;  // remap(h, s) < c0  <=>  h_hi < T
+            }
+            cnt += __popc(__ballot_sync(FULL, left));
+        }
+        if (cnt == c.target) return sigma;
+    }
+    if (lane == 0) atomicOr(A.err, 1u);
+    return kSeedCap;
+}
+
 // ------------------------------------------------------------- scheduling --
 
 __device__ u32 find_help(const Args& A, u32 gw, u32 lane, u32 nn) {
@@ -989,6 +1078,9 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                 if (KIND == SK_UPPER && A.nodes[n].size > kWarpKeyCap) continue;  // k_search_upper_big
                 load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c);
                 u64 val = 0;
+                if (KIND == SK_UPPER && A.upper_kp) {
+                    val = upper_keys_parallel(A, G, c, lane);
+                } else
                 for (u64 wstart = 0;; wstart += ws) {
                     if (wstart >= kSeedCap) {
                         if (lane == 0) atomicOr(A.err, 1u);
@@ -998,6 +1090,8 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                     if (run_window<KIND, VAR>(A, K, c, wstart, lane, &val, QS, QC)) break;
                 }
                 if (lane == 0) A.values[c.slot] = val;
+                if ((KIND == SK_UPPER || KIND == SK_LOWER) && A.lo_w)
+                    fused_reorder<KIND>(A, G, A.nodes[n].key_off, c, val, lane);
                 __syncwarp();
             }
         }
@@ -1096,6 +1190,139 @@ __global__ void __launch_bounds__(1024) k_search_upper_big(const NodeRec* __rest
     }
 }
 
+// ------------------------------------------------------- lane-per-leaf search --
+//
+// Small leaves (m <= kLaneLeafMax, e.g. l = 8 at C2: ~56 base seeds per leaf) spend most of a
+// warp-per-leaf search on window overshoot (a 32-seed window for ~56 seeds), node loading and
+// the cross-lane rotation check.  Here every LANE owns one leaf: its m keys sit in registers
+// and it tries base seeds k = 0, 1, 2, ... in order, for each the rotations r = 0..m-1 in
+// order -- exactly the sequential search, so the first fit is the minimal stored
+// value k*m + r (brute force: the first k with a bijection).  A lane that finishes
+// stores its value and takes the next leaf of the phase (warp-aggregated cursor atomics), so
+// the lanes of a warp stay busy while leaves finish at different times.
+constexpr u32 kLaneLeafMax = 12;
+
+// masks of base value `base` over the m keys held in registers (a: A keys, b: B keys)
+__device__ __forceinline__ void lane_masks(const u64* key, const u32* amask, u32 m, u64 base, u32& a, u32& b) {
+    a = 0;
+    b = 0;
+#pragma unroll
+    for (u32 j = 0; j < kLaneLeafMax; ++j) {
+        if (j < m) {
+            const u32 bit = 1u << __umulhi(remix_hi(key[j] + base), m);
+            a |= bit & amask[j];
+            b |= bit & ~amask[j];
+        }
+    }
+}
+
+// smallest r with rot_m^r(b) filling the holes of a, or -1
+__device__ __forceinline__ int lane_fit(u32 a, u32 b, u32 m, u32 full) {
+    if (__popc(a) + __popc(b) != (int)m) return -1;  // a collision inside A or B
+    const u32 na = ~a & full;
+    const u64 bb = (u64)b | ((u64)b << m);  // rot_m^r(b) = (bb >> (m - r)) & full
+    for (u32 r = 0; r < m; ++r)
+        if (((u32)(bb >> (m - r)) & full) == na) return (int)r;
+    return -1;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256) k_leaf_lane(const NodeRec* __restrict__ nodes, const u32* n_nodes,
+                                                   const u64* __restrict__ lo, const u8* __restrict__ ab,
+                                                   u64* __restrict__ values, u32* cursor, u32* err, const u32* dup) {
+    if (dup[0] || dup[1] > 1) return;
+    const u32 nn = *n_nodes;
+    const u32 lane = threadIdx.x & 31;
+    u64 key[kLaneLeafMax];
+    u32 amask[kLaneLeafMax];  // all-ones for A keys (R7), 0 for B keys
+    u32 m = 0, full = 0, slot = 0;
+    u64 k = 0;
+    bool busy = false, dry = false;  // dry: the phase's cursor is exhausted
+    for (;;) {
+        // lanes without a leaf take the next ones (one atomic per warp)
+        const u32 want = __ballot_sync(FULL, !busy);
+        if (want && !dry) {
+            const int leader = __ffs(want) - 1;
+            u32 first = 0;
+            if ((int)lane == leader) first = atomicAdd(cursor, (u32)__popc(want));
+            first = __shfl_sync(FULL, first, leader);
+            dry = first + __popc(want) > nn;
+            if (!busy) {
+                const u32 idx = first + __popc(want & lanemask_lt());
+                if (idx < nn) {
+                    const NodeRec rec = nodes[idx];
+                    m = rec.size;
+                    slot = rec.slot;
+                    full = (1u << m) - 1u;
+#pragma unroll
+                    for (u32 j = 0; j < kLaneLeafMax; ++j) {
+                        key[j] = j < m ? lo[rec.key_off + j] : 0;
+                        amask[j] = j < m && !(KIND == SK_LEAF_RF && ab[rec.key_off + j]) ? FULL : 0u;
+                    }
+                    k = 0;
+                    busy = true;
+                }
+            }
+        }
+        if (dry) break;  // finish the warp's remaining leaves cooperatively (below)
+        // one base seed of this lane's leaf, tried in (k, r) order
+        const u64 base = KIND == SK_LEAF_RF ? k * m : k;
+        u32 a, b;
+        lane_masks(key, amask, m, base, a, b);
+        int r = -1;
+        if (KIND == SK_LEAF_BF)
+            r = a == full ? 0 : -1;
+        else
+            r = lane_fit(a, b, m, full);
+        if (r >= 0) {
+            values[slot] = base + (u32)r;
+            busy = false;
+        } else if (++k >= kSeedCap) {
+            atomicOr(err, 1u);
+            values[slot] = base;
+            busy = false;
+        }
+    }
+    // Tail: the leaves still open in this warp, one after another with all 32 lanes trying
+    // consecutive base seeds from the owner's next untried k (all smaller ones failed); the
+    // lowest lane with a fit and its smallest r is the minimal value.
+    u32 open = __ballot_sync(FULL, busy);
+    while (open) {
+        const int L = __ffs(open) - 1;
+        open &= open - 1;
+        const u32 mL = __shfl_sync(FULL, m, L), fL = (1u << mL) - 1u, sL = __shfl_sync(FULL, slot, L);
+        u64 kL = shfl64(k, L);
+        u64 kk[kLaneLeafMax];
+        u32 am[kLaneLeafMax];
+#pragma unroll
+        for (u32 j = 0; j < kLaneLeafMax; ++j) {
+            kk[j] = shfl64(key[j], L);
+            am[j] = __shfl_sync(FULL, amask[j], L);
+        }
+        for (;; kL += 32) {
+            const u64 kx = kL + lane;
+            const u64 base = KIND == SK_LEAF_RF ? kx * mL : kx;
+            u32 a, b;
+            lane_masks(kk, am, mL, base, a, b);
+            const int r = KIND == SK_LEAF_BF ? (a == fL ? 0 : -1) : lane_fit(a, b, mL, fL);
+            const u32 bal = __ballot_sync(FULL, r >= 0);
+            if (bal) {
+                const int w = __ffs(bal) - 1;
+                const u64 v = shfl64(base + (u32)(r < 0 ? 0 : r), w);
+                if ((int)lane == L) values[sL] = v;
+                break;
+            }
+            if (kL + 32 >= kSeedCap) {
+                if ((int)lane == L) {
+                    atomicOr(err, 1u);
+                    values[sL] = KIND == SK_LEAF_RF ? kL * mL : kL;
+                }
+                break;
+            }
+        }
+    }
+}
+
 template <int KIND, int VAR = V_PLAIN>
 void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 grid, cudaStream_t st) {
     cudaFuncSetAttribute(k_search<KIND, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -1106,8 +1333,8 @@ void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 
 
 u32 search_active_slots(int sm_count) { return (u32)sm_count * 16u * kWarpsPerBlockMax; }
 
-void launch_search(const PhaseLaunch& P, cudaStream_t st) {
-    if (P.n_nodes_host == 0) return;
+bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
+    if (P.n_nodes_host == 0) return false;
     Args A;
     A.nodes = P.nodes;
     A.n_nodes = P.n_nodes;
@@ -1152,6 +1379,18 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
         static const int cpw2 = getenv("RS_CPW2") ? atoi(getenv("RS_CPW2")) : 1;
         A.cp_wide2 = cpw2 ? 1u : 0u;
     }
+    static const int lane_leaf_max = getenv("RS_LANE_LEAF") ? atoi(getenv("RS_LANE_LEAF")) : 8;
+    if ((P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) && P.max_size <= (u32)lane_leaf_max &&
+        P.max_size <= kLaneLeafMax) {
+        // lane-per-leaf search (small leaves); the phase's batch cursor is zeroed
+        const u32 blocks = std::max<u32>(1, std::min<u32>((P.n_nodes_host + 255) / 256, (u32)P.sm_count * 8));
+        if (P.kind == SK_LEAF_RF)
+            k_leaf_lane<SK_LEAF_RF><<<blocks, 256, 0, st>>>(P.nodes, P.n_nodes, P.lo, P.ab, P.values, P.cursor, P.err, P.dup);
+        else
+            k_leaf_lane<SK_LEAF_BF><<<blocks, 256, 0, st>>>(P.nodes, P.n_nodes, P.lo, P.ab, P.values, P.cursor, P.err, P.dup);
+        g_launches++;
+        return false;
+    }
     if (P.kind == SK_UPPER && P.max_size > kWarpKeyCap) {  // oversized upper nodes first
         const u32 grid_big = std::min<u32>(P.n_nodes_host, (u32)P.sm_count * 2);
         k_search_upper_big<<<grid_big, 1024, 0, st>>>(P.nodes, P.n_nodes_host, P.lo, P.values, P.u2, P.err, P.dup);
@@ -1191,6 +1430,15 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
     }
     if (grid == 0) grid = 1;
     A.n_warps = grid * wpb;
+    // fused redistribution (A7) for batch-mode split phases of small nodes: every node is
+    // finished by the one warp that holds its keys
+    static const int fuse = getenv("RS_FUSE_REORDER") ? atoi(getenv("RS_FUSE_REORDER")) : 1;
+    const bool fused = fuse && P.fuse_reorder && (P.kind == SK_UPPER || P.kind == SK_LOWER) && !P.help &&
+                       A.tail == 0 && P.max_size <= kFuseMax;
+    static const int ukp = getenv("RS_UPPER_KP") ? atoi(getenv("RS_UPPER_KP")) : 1;
+    A.upper_kp = ukp && P.kind == SK_UPPER && !P.help && A.tail == 0 ? 1u : 0u;
+    A.lo_w = fused ? P.lo_w : nullptr;
+    A.ab_w = fused ? P.ab_w : nullptr;
     switch (P.kind) {
         case SK_UPPER: launch_kind<SK_UPPER>(P, A, wpb, smem, grid, st); break;
         case SK_LOWER: {
@@ -1220,6 +1468,7 @@ void launch_search(const PhaseLaunch& P, cudaStream_t st) {
             break;
     }
     g_launches++;
+    return fused;
 }
 
 // ------------------------------------------------------------------ reorder --

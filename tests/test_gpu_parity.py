@@ -38,13 +38,18 @@ def _mhc_np(keys, g=0):
 
 # ------------------------------------------------------------------ kernel level --
 
-@pytest.mark.parametrize("rf", [True, False])
-def test_leaf_search_parity(rf):
-    rng = np.random.default_rng(11 + rf)
+@pytest.mark.parametrize("rf,mmax", [(True, 16), (False, 12), (True, 8), (False, 8), (True, 3)])
+def test_leaf_search_parity(rf, mmax):
+    """Leaf searches against the oracle's (rotation fitting P:245-263 / brute force P:125-128).
+    mmax <= 8: the phase runs the lane-per-leaf kernel (k_leaf_lane, incl. its cooperative
+    tail), else the warp-per-leaf engine."""
+    rng = np.random.default_rng(11 + rf + mmax)
     sizes = []
-    for m in range(1, 17):
+    for m in range(1, mmax + 1):
         sizes += [m] * (400 if m <= 12 else 60)
-    if not rf:
+    if mmax <= 8:
+        sizes = sizes * 4  # several leaves per lane
+    if not rf and mmax > 11:
         sizes = [m for m in sizes if m <= 11] + [12] * 10
     rng.shuffle(sizes)
     off = np.zeros(len(sizes) + 1, dtype=np.uint32)
