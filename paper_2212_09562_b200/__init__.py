@@ -179,8 +179,9 @@ def build(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
 
 
 def build_device(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
-                 global_seed: int = 0, stream=None, stats: bool = False):
-    """Build from a CUDA tensor of keys (int64/uint64 bit patterns) resident in HBM."""
+                 global_seed: int = 0, stream=None, stats: bool = False, virtual_shards: int = 0):
+    """Build from a CUDA tensor of keys (int64/uint64 bit patterns) resident in HBM
+    (virtual_shards > 1: the bucket-range sharded path on this one device)."""
     import torch
 
     if not keys_tensor.is_cuda or not keys_tensor.is_contiguous() or keys_tensor.element_size() != 8:
@@ -189,7 +190,7 @@ def build_device(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting
         stream = torch.cuda.current_stream(keys_tensor.device)
     b = Bytes()
     st = Stats()
-    o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, 0)
+    o = _opts(rotation_fitting, global_seed, keys_tensor.device.index, virtual_shards)
     _check(lib().recsplit_build_device(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), leaf_size,
                                        bucket_size, C.byref(o), C.c_void_p(stream.cuda_stream), C.byref(b),
                                        C.byref(st)))

@@ -90,8 +90,15 @@ void select_device(int dev) {
     }
 }
 
-int emit(const rs::BuildOutput& o, recsplit_bytes* out) {
-    out->data = (uint8_t*)malloc(o.bytes.size());
+int emit(rs::BuildOutput& o, recsplit_bytes* out) {
+    if (o.raw) {  // hand over the malloc'ed result (no copy)
+        out->data = o.raw;
+        out->size = o.raw_size;
+        o.raw = nullptr;
+        o.raw_size = 0;
+        return RECSPLIT_OK;
+    }
+    out->data = (uint8_t*)malloc(std::max<size_t>(o.bytes.size(), 1));
     if (!out->data) return fail(RECSPLIT_E_NOMEM, "host allocation failed");
     memcpy(out->data, o.bytes.data(), o.bytes.size());
     out->size = o.bytes.size();

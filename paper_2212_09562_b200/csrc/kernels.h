@@ -41,11 +41,14 @@ void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cur
                     u8* ab2, cudaStream_t st);
 
 // ---- tree (encode.cu): node counts per bucket, node expansion into phase lists.
+// per-phase node counts pcnt[q] (device) from the scanned count matrix
+void launch_phase_counts(const u64* Ms, u64 B, u32 NP, u32* pcnt, cudaStream_t st);
+// (S: largest size the tables cover; larger buckets are skipped and flagged in *ovf)
 void launch_bucket_counts(const u64* C, u64 B, const u32* N, const u32* phase_cnt, u32 NP,
-                          u64* M /*[(NP+1)*(B+1)]*/, cudaStream_t st);
+                          u64* M /*[(NP+1)*(B+1)]*/, cudaStream_t st, u32 S, u32* ovf);
 void launch_expand(const u64* C, u64 B, const u64* Mscan, u32 NP, const u32* tstart,
                    const rsd::TNodeD* tnodes, const u64* phase_off /*[NP]*/, rsd::NodeRec* nodes,
-                   cudaStream_t st);
+                   cudaStream_t st, u32 S);
 
 // ---- search (search.cu): the hot path, steps A4-A9.
 enum SearchKind { SK_UPPER = 0, SK_LOWER = 1, SK_LEAF_RF = 2, SK_LEAF_BF = 3 };
@@ -78,18 +81,37 @@ u32 search_active_slots(int sm_count);
 // key redistribution after a split phase (A7), in place for the phase's nodes
 // (big_scratch: kReorderBigWarps * 2 * max_size u64 when max_size > 8192, else unused)
 constexpr u32 kReorderBigWarps = 64;
+// (n_nodes_dev non-null: the phase's node count on the device; n_nodes is then an estimate
+// for the grid size only)
 void launch_reorder(const rsd::NodeRec* nodes, u32 n_nodes, const u64* values, u64* lo, u8* ab, u32 leaf,
-                    u32 u1, u32 u2, u32 max_size, int sm_count, u64* big_scratch, cudaStream_t st);
+                    u32 u1, u32 u2, u32 max_size, int sm_count, u64* big_scratch, cudaStream_t st,
+                    const u32* n_nodes_dev = nullptr);
 
 // ---- encode (encode.cu), steps A10-A11.
 // bucket bit lengths: F(s) + N(s) + sum (x >> tau); also algorithmic-evals statistics
 void launch_bucket_bits(const u64* C, u64 B, const u64* nodebase, const u32* tstart,
                         const rsd::TNodeD* tnodes, const u64* F, const u64* values, u32 leaf,
                         u32 u1, u32 u2, int rf, u64* len, unsigned long long* evals /*[4]*/,
-                        cudaStream_t st);
+                        cudaStream_t st, u32 S);
+// Device-side globals and layout of a single-shard build (one-enqueue path).
+struct SingleDev {
+    u64 n, D, dC, beta;
+    long long dR;
+    u32 LC, LP;
+    u64 lowC, upC, lowP, upP;                        // bit lengths of the EF vectors
+    u64 off_lowC, off_upC, off_lowP, off_upP, off_data;  // 64-bit word offsets in the output
+    u64 total_words;
+    u32 overflow, pad;
+};
+// sd non-null: words = the output buffer, data written at sd->off_data (skipped on overflow)
 void launch_write_data(const u64* C, u64 B, const u64* nodebase, const u32* tstart,
                        const rsd::TNodeD* tnodes, const u64* F, const u64* values, const u64* P,
-                       unsigned long long* words, cudaStream_t st);
+                       unsigned long long* words, cudaStream_t st, u32 S, const SingleDev* sd);
+// globals (n, D, delta_C, beta), delta_R, EF parameters, offsets and header words into sd / out
+void launch_single_index(const u64* C, const u64* P, u64 B, const u32* small, SingleDev* sd, u64 hdr0, u64 hdr1, u64 g,
+                         u64 cap_words, unsigned long long* out, cudaStream_t st);
+// both EF sequences of all B + 1 entries into out at sd's offsets
+void launch_single_ef(const u64* C, const u64* P, u64 B, const SingleDev* sd, unsigned long long* out, cudaStream_t st);
 // Global view of a shard's bucket range for the index (R13): global bucket i = b0 + l,
 // C_g = key_base + C_l, P_g = bit_base + P_l, R[i] = P_g[i] - floor(beta C_g[i] / 2^20).
 struct IndexView {

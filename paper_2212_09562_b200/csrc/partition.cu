@@ -141,13 +141,15 @@ void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cur
 // dup[0] |= 1 on a repeated value, dup[1] += keys with lo == 0 (> 1 is a duplicate).
 template <bool BIG>
 __global__ void __launch_bounds__(256) k_dedupe(const u64* __restrict__ lo, const u64* __restrict__ C, u64 nb,
-                                                u32 dup_cap, u32* dup, unsigned long long* gtab) {
+                                                u32 dup_cap, u32* dup, unsigned long long* gtab, u32 smax) {
     extern __shared__ unsigned long long stab[];
     unsigned long long* tab = BIG ? gtab + (size_t)blockIdx.x * 2 * dup_cap : stab;
     for (u64 b = blockIdx.x; b < nb; b += gridDim.x) {
         const u64 c0 = C[b], s = C[b + 1] - c0;
         __syncthreads();
-        if (s < 2 || (BIG ? s <= kSmallBucketKeys : s > kSmallBucketKeys)) continue;
+        // (s > smax: a bucket above the caller's size bound, flagged elsewhere; never read past
+        // the table)
+        if (s < 2 || s > smax || (BIG ? s <= kSmallBucketKeys : s > kSmallBucketKeys)) continue;
         u32 ts = 64;
         while (ts < 2 * s) ts <<= 1;
         for (u32 i = threadIdx.x; i < ts; i += blockDim.x) tab[i] = 0;
@@ -181,13 +183,13 @@ void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, u64*
     cudaFuncSetAttribute(k_dedupe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const u32 threads = smax <= 128 ? 128 : 256;
     unsigned grid = nb < 148ull * 64 ? (unsigned)nb : 148u * 64;
-    k_dedupe<false><<<grid, threads, smem, st>>>(lo, C, nb, 0, dup, nullptr);
+    k_dedupe<false><<<grid, threads, smem, st>>>(lo, C, nb, 0, dup, nullptr, smax);
     g_launches++;
     if (smax > kSmallBucketKeys) {
         u32 tb = 64;
         while (tb < 2 * smax) tb <<= 1;  // per-block table of tb entries (dup_cap = tb / 2)
         const unsigned g2 = nb < kDedupeBigBlocks ? (unsigned)nb : kDedupeBigBlocks;
-        k_dedupe<true><<<g2, 256, 0, st>>>(lo, C, nb, tb / 2, dup, (unsigned long long*)big_scratch);
+        k_dedupe<true><<<g2, 256, 0, st>>>(lo, C, nb, tb / 2, dup, (unsigned long long*)big_scratch, smax);
         g_launches++;
     }
 }

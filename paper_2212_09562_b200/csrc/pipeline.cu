@@ -4,10 +4,12 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <tuple>
 
 #include "kernels.h"
 #include "pipeline.h"
@@ -442,7 +444,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     u64* M = A.alloc<u64>(rows);
     u64* Ms = A.alloc<u64>(rows + 1);
     void* scan_tmp2 = A.alloc<u8>(scan_temp_bytes(rows) + 64);
-    launch_bucket_counts(C, Bl, DT.N, DT.phase_cnt, NP, M, st);
+    launch_bucket_counts(C, Bl, DT.N, DT.phase_cnt, NP, M, st, smax, small + 5);
     CKL();
     exscan_u64(M, Ms, rows, scan_tmp2, st);
     CKL();
@@ -473,7 +475,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     std::vector<u32> pc32(NP);
     for (uint32_t q = 0; q < NP; ++q) pc32[q] = (u32)pcount[q];
     CK(cudaMemcpyAsync(pcnt_d, pc32.data(), NP * 4, cudaMemcpyHostToDevice, st));
-    launch_expand(C, Bl, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st);
+    launch_expand(C, Bl, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st, smax);
     CKL();
     const int e2 = tm.mark();
 
@@ -555,7 +557,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     CK(cudaMemsetAsync(evals, 0, 32, st));
     u64* nodebase = Ms;  // row 0 of the scanned count matrix
     launch_bucket_bits(C, Bl, nodebase, DT.tstart, DT.tnodes, DT.F, values_d, leaf, sh.u1, sh.u2, p.rf ? 1 : 0, len,
-                       evals, st);
+                       evals, st, smax);
     CKL();
     exscan_u64(len, Pbits, Bl, scan_tmp, st);
     CKL();
@@ -577,7 +579,7 @@ Shard::Shard(const uint64_t* d_keys, const BuildParams& p, int rank, int world, 
     I.d_data = data;
     CK(cudaMemsetAsync(data, 0, (nwords + 1) * 8, st));
     if (!summary[SUM_DUP] && !summary[SUM_ERR]) {
-        launch_write_data(C, Bl, nodebase, DT.tstart, DT.tnodes, DT.F, values_d, Pbits, data, st);
+        launch_write_data(C, Bl, nodebase, DT.tstart, DT.tnodes, DT.F, values_d, Pbits, data, st, smax, nullptr);
         CKL();
     }
     if (want_values) {
@@ -732,7 +734,7 @@ struct PinnedStage {
 };
 static PinnedStage g_stage;
 
-void Shard::finish_blob(long long dR, std::vector<uint8_t>& blob) {
+void Shard::finish_blob(long long dR, uint8_t*& blob, size_t& blob_size) {
     Impl& I = *impl_;
     if (I.world != 1) throw Error(RECSPLIT_E_INVALID, "finish_blob needs a single shard");
     auto t0 = std::chrono::steady_clock::now();
@@ -783,7 +785,10 @@ void Shard::finish_blob(long long dR, std::vector<uint8_t>& blob) {
     at += nb;
     if (at != size) throw Error(RECSPLIT_E_INVALID, "internal: serialized size mismatch");
     CK(cudaStreamSynchronize(I.st));
-    blob.assign(buf, buf + size);
+    blob = (uint8_t*)malloc(size);
+    if (!blob) throw Error(RECSPLIT_E_NOMEM, "host allocation failed");
+    memcpy(blob, buf, size);
+    blob_size = size;
     stats.t_d2h += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -865,10 +870,323 @@ void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::ve
     if (!vec[0].empty()) memcpy(blob.data() + at, vec[0].data(), 8 * vec[0].size());
 }
 
+// ============================================================ one enqueue ==
+//
+// Single-shard builds without a host round trip before the end ("size the node
+// table on the device with worst-case allocation, so the build is one enqueue").  The
+// synchronized path reads the bucket-size histogram back to size the node table and the
+// phases; here the tables cover every bucket size up to a bound S (far beyond the Poisson
+// tail: n/B + 8 sqrt(n/B) + 32), each phase's node array is sized by max_s ceil(cnt_q(s) n / s)
+// -- an exact upper bound, since sum_i cnt_q(s_i) <= max_s (cnt_q(s)/s) sum_i s_i -- the phase
+// counts stay on the device, the globals (n, D, delta_C, beta, delta_R, R13) and the EF layout
+// are computed by kernels and the serialized MPHF is assembled in one device buffer.  One D2H
+// and one synchronization at the end.  A bucket above S (flagged by the kernels) makes the
+// call return false and the caller rebuilds on the synchronized path.
+namespace {
+
+struct PinnedReport {
+    std::mutex mu;
+    uint8_t* p = nullptr;
+    uint8_t* get() {
+        if (!p) CK(cudaMallocHost(&p, 4096));
+        return p;
+    }
+};
+PinnedReport g_report;
+
+std::mutex g_est_mu;
+std::map<std::tuple<uint64_t, uint32_t, uint32_t, bool, uint64_t>, uint64_t> g_est_words;  // last blob size
+
+}  // namespace
+
+bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out) {
+    auto t_start = std::chrono::steady_clock::now();
+    const uint64_t n = p.n;
+    const uint32_t leaf = p.leaf;
+    const uint64_t B = (n + p.bucket - 1) / p.bucket;  // R12
+    const double avg = (double)n / (double)B;
+    const uint32_t S = (uint32_t)std::min<uint64_t>(n, (uint64_t)(avg + 8.0 * std::sqrt(avg) + 32.0));
+    if (S > kSmallBucketKeys || B >= (1ull << 31)) return false;
+    g_launches = 0;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    init_device(dev);
+    const int sms = sm_count(dev);
+    const Shape sh = make_shape(leaf);
+    recsplit_stats& Sst = out.stats;
+    memset(&Sst, 0, sizeof Sst);
+    Arena A(st);
+    Timer tm(st);
+    const int e0 = tm.mark();
+
+    // ---- A1/A2 ----------------------------------------------------------------
+    u64* lo_t = A.alloc<u64>(n);
+    u8* ab_t = A.alloc<u8>(n);
+    u32* bkt = A.alloc<u32>(n);
+    u32* hist = A.alloc<u32>(B + 1);
+    u64* C = A.alloc<u64>(B + 2);
+    u64* cursor = A.alloc<u64>(B + 1);
+    u32* small = A.alloc<u32>(8);  // [0] max, [1] min bucket size, [2] dup, [3] lo == 0, [4] seed cap, [5] size > S
+    u32* size_hist_d = A.alloc<u32>(S + 1);
+    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(B + 1) + 64);
+    CK(cudaMemsetAsync(hist, 0, (B + 1) * 4, st));
+    CK(cudaMemsetAsync(size_hist_d, 0, (S + 1) * 4, st));
+    const uint32_t small_init[8] = {0, 0xffffffffu, 0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(small, small_init, sizeof small_init, cudaMemcpyHostToDevice, st));
+    if (p.h_keys && !p.strings) {  // A1 overlapped with the chunked host->device copy
+        const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
+        std::vector<cudaEvent_t> evs;
+        for (uint64_t off = 0; off < n; off += chunk) {
+            const uint64_t len = std::min(chunk, n - off);
+            cudaEvent_t ev;
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            evs.push_back(ev);
+            CK(cudaMemcpyAsync(const_cast<uint64_t*>(d_keys) + off, p.h_keys + off, len * 8, cudaMemcpyHostToDevice,
+                               p.copy_stream));
+            CK(cudaEventRecord(ev, p.copy_stream));
+            CK(cudaStreamWaitEvent(st, ev, 0));
+            launch_hash(d_keys + off, nullptr, len, p.g, B, 0, B, lo_t + off, ab_t + off, bkt + off, hist, st);
+            CKL();
+        }
+        for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+    } else {
+        launch_hash(p.strings ? nullptr : d_keys, p.strings ? d_keys : nullptr, n, p.g, B, 0, B, lo_t, ab_t, bkt, hist, st);
+        CKL();
+    }
+    launch_bucket_stats(hist, B, small, size_hist_d, S, st);
+    CKL();
+    exscan_u32_to_u64(hist, C, B, scan_tmp, st);
+    CKL();
+    CK(cudaMemcpyAsync(cursor, C, (B + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    u64* lo_a = A.alloc<u64>(n);
+    u8* ab_a = A.alloc<u8>(n);
+    launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
+    CKL();
+    launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
+    CKL();
+    A.release(lo_t);
+    A.release(ab_t);
+    A.release(bkt);
+    const int e1 = tm.mark();
+
+    // ---- A3: node table for all sizes <= S --------------------------------------
+    std::vector<uint8_t> present(S + 1, 1);
+    present[0] = 0;
+    const DevTables& DT = device_tables(dev, leaf, p.rf, S, present, st);
+    const Tables& T = *DT.T;
+    const uint32_t NP = T.NP;
+    const uint64_t rows = (uint64_t)(NP + 1) * (B + 1);
+    u64* M = A.alloc<u64>(rows);
+    u64* Ms = A.alloc<u64>(rows + 1);
+    void* scan_tmp2 = A.alloc<u8>(scan_temp_bytes(rows) + 64);
+    launch_bucket_counts(C, B, DT.N, DT.phase_cnt, NP, M, st, S, small + 5);
+    CKL();
+    exscan_u64(M, Ms, rows, scan_tmp2, st);
+    CKL();
+    // exact upper bounds of the phase lists and of the node count, and the counts expected
+    // for a typical bucket (launch sizing only)
+    std::vector<uint64_t> bound(NP, 0), poff(NP, 0), est(NP, 0);
+    uint64_t nbound = 0;
+    const uint32_t typ = (uint32_t)std::max<double>(1.0, std::min<double>(S, std::round(avg)));
+    for (uint32_t x = 1; x <= S; ++x) {
+        const Tables::Tmpl& tp = T.tmpl(x);
+        for (uint32_t q = 0; q < NP; ++q)
+            bound[q] = std::max<uint64_t>(bound[q], ((uint64_t)tp.phase_cnt[q] * n + x - 1) / x);
+        nbound = std::max<uint64_t>(nbound, ((uint64_t)T.N[x] * n + x - 1) / x);
+    }
+    uint64_t acc = 0;
+    for (uint32_t q = 0; q < NP; ++q) {
+        poff[q] = acc;
+        acc += bound[q];
+        est[q] = std::max<uint64_t>(bound[q] ? 1 : 0, B * (uint64_t)T.tmpl(typ).phase_cnt[q]);
+    }
+    rsd::NodeRec* nodes = A.alloc<rsd::NodeRec>(acc);
+    u64* values_d = A.alloc<u64>(nbound);
+    u32* next_win = A.alloc<u32>(nbound);
+    u32* pcnt_d = A.alloc<u32>(NP + 32);
+    const u32 nslots = search_active_slots(sms);
+    int* active = A.alloc<int>(nslots);
+    u32* cursors = A.alloc<u32>(2 * NP + 2);
+    CK(cudaMemsetAsync(values_d, 0xff, nbound * 8, st));
+    CK(cudaMemsetAsync(next_win, 0, nbound * 4, st));
+    CK(cudaMemsetAsync(cursors, 0, (2 * NP + 2) * 4, st));
+    launch_phase_counts(Ms, B, NP, pcnt_d, st);
+    CKL();
+    launch_expand(C, B, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st, S);
+    CKL();
+    const int e2 = tm.mark();
+
+    // ---- A4-A9 -----------------------------------------------------------------
+    struct PhaseEv {
+        uint32_t cls;
+        int a, b, c;
+    };
+    std::vector<PhaseEv> pev;
+    for (uint32_t q = 0; q < NP; ++q) {
+        if (bound[q] == 0) continue;
+        SearchKind kind;
+        uint32_t maxs, typical, cls;
+        if (q < T.n_upper) {
+            kind = SK_UPPER;
+            maxs = S;
+            typical = std::min<uint32_t>(S, 2 * sh.u2);
+            cls = 0;
+        } else if (q == T.phase_L2()) {
+            kind = SK_LOWER;
+            maxs = sh.u2;
+            typical = sh.u2;
+            cls = 1;
+        } else if (q == T.phase_L1()) {
+            kind = SK_LOWER;
+            maxs = sh.u1;
+            typical = sh.u1;
+            cls = 2;
+        } else {
+            kind = p.rf ? SK_LEAF_RF : SK_LEAF_BF;
+            maxs = leaf;
+            typical = leaf;
+            cls = 3;
+        }
+        PhaseLaunch P{};
+        P.kind = kind;
+        P.nodes = nodes + poff[q];
+        P.n_nodes = pcnt_d + q;
+        P.n_nodes_host = (u32)std::min<uint64_t>(est[q], 0xffffffffu);
+        P.lo = lo_a;
+        P.ab = ab_a;
+        P.values = values_d;
+        P.next_win = next_win;
+        P.cursor = cursors + 2 * q;
+        P.active = active;
+        P.err = small + 4;
+        P.dup = small + 2;
+        P.leaf = leaf;
+        P.u1 = sh.u1;
+        P.u2 = sh.u2;
+        P.max_size = maxs;
+        phase_policy(T, kind, typical, P.iters, P.help);
+        P.sm_count = sms;
+        P.fuse_reorder = kind == SK_UPPER || kind == SK_LOWER;
+        P.lo_w = lo_a;
+        P.ab_w = ab_a;
+        CK(cudaMemsetAsync(active, 0xff, nslots * 4, st));
+        const int a = tm.mark();
+        const bool fused = launch_search(P, st);
+        CKL();
+        const int b = tm.mark();
+        if ((kind == SK_UPPER || kind == SK_LOWER) && !fused) {
+            launch_reorder(nodes + poff[q], P.n_nodes_host, values_d, lo_a, ab_a, leaf, sh.u1, sh.u2, maxs, sms, nullptr,
+                           st, pcnt_d + q);
+            CKL();
+        }
+        const int c = tm.mark();
+        pev.push_back({cls, a, b, c});
+    }
+    const int e3 = tm.mark();
+
+    // ---- A10-A12: lengths, globals, EF, data, header in one output buffer ----------
+    u64* len = A.alloc<u64>(B + 1);
+    u64* Pbits = A.alloc<u64>(B + 2);
+    unsigned long long* evals = A.alloc<unsigned long long>(4);
+    CK(cudaMemsetAsync(evals, 0, 32, st));
+    launch_bucket_bits(C, B, Ms, DT.tstart, DT.tnodes, DT.F, values_d, leaf, sh.u1, sh.u2, p.rf ? 1 : 0, len, evals, st,
+                       S);
+    CKL();
+    exscan_u64(len, Pbits, B, scan_tmp, st);
+    CKL();
+    SingleDev* sd = A.alloc<SingleDev>(1);
+    CK(cudaMemsetAsync(sd, 0, sizeof(SingleDev), st));
+    const uint64_t k = B + 1;
+    const uint64_t cap_words = 9 + 2 * (3 + k + (3 * k) / 64 + 2) + (8 * n + 4096) / 64 + 16;
+    unsigned long long* outw = A.alloc<unsigned long long>(cap_words);
+    CK(cudaMemsetAsync(outw, 0, cap_words * 8, st));
+    const uint64_t flags = (p.rf ? 1u : 0u) | (p.strings ? 2u : 0u);
+    const uint64_t hdr0 = (uint64_t)'R' | ((uint64_t)'S' << 8) | ((uint64_t)'R' << 16) | ((uint64_t)'F' << 24) |
+                          (1ull << 32) | ((uint64_t)leaf << 48) | (flags << 56);
+    const uint64_t hdr1 = p.bucket;
+    launch_single_index(C, Pbits, B, small, sd, hdr0, hdr1, p.g, cap_words, outw, st);
+    CKL();
+    launch_write_data(C, B, Ms, DT.tstart, DT.tnodes, DT.F, values_d, Pbits, outw, st, S, sd);
+    CKL();
+    launch_single_ef(C, Pbits, B, sd, outw, st);
+    CKL();
+    const int e4 = tm.mark();
+
+    // ---- one D2H of the report and (most likely all of) the serialized MPHF -----
+    const auto key = std::make_tuple(n, leaf, p.bucket, p.rf, p.g);
+    uint64_t est_words;
+    {
+        std::lock_guard<std::mutex> g(g_est_mu);
+        auto it = g_est_words.find(key);
+        // first build of a configuration: about 2.5 bits per key plus the index
+        est_words = it == g_est_words.end() ? std::min<uint64_t>(cap_words, 64 + (5 * n / 2 + 24 * k) / 64)
+                                            : std::min<uint64_t>(cap_words, it->second + it->second / 64 + 64);
+    }
+    std::lock_guard<std::mutex> lk_rep(g_report.mu);
+    uint8_t* rep = g_report.get();
+    CK(cudaMemcpyAsync(rep, small, 32, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rep + 32, sd, sizeof(SingleDev), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rep + 32 + sizeof(SingleDev), evals, 32, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rep + 64 + sizeof(SingleDev), pcnt_d, NP * 4, cudaMemcpyDeviceToHost, st));
+    std::lock_guard<std::mutex> lk_stage(g_stage.mu);
+    uint8_t* buf = g_stage.get(cap_words * 8);
+    CK(cudaMemcpyAsync(buf, outw, est_words * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint32_t fl[8];
+    memcpy(fl, rep, 32);
+    SingleDev sdh;
+    memcpy(&sdh, rep + 32, sizeof sdh);
+    unsigned long long ev_h[4];
+    memcpy(ev_h, rep + 32 + sizeof(SingleDev), 32);
+    std::vector<uint32_t> pc(NP);
+    memcpy(pc.data(), rep + 64 + sizeof(SingleDev), NP * 4);
+    if (fl[2] || fl[3] > 1) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
+    if (fl[4]) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
+    if (fl[5] || fl[0] > S || sdh.overflow) return false;  // rebuild on the synchronized path
+    if (sdh.total_words > est_words) {
+        CK(cudaMemcpyAsync(buf + est_words * 8, outw + est_words, (sdh.total_words - est_words) * 8,
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    {
+        std::lock_guard<std::mutex> g(g_est_mu);
+        g_est_words[key] = sdh.total_words;
+    }
+    const size_t size = sdh.total_words * 8;
+    out.raw = (uint8_t*)malloc(size);
+    if (!out.raw) throw Error(RECSPLIT_E_NOMEM, "host allocation failed");
+    memcpy(out.raw, buf, size);
+    out.raw_size = size;
+    // statistics
+    Sst.t_partition = tm.secs(e0, e1);
+    Sst.t_tree = tm.secs(e1, e2);
+    for (const PhaseEv& x : pev) {
+        Sst.t_search[x.cls] += tm.secs(x.a, x.b);
+        Sst.t_reorder += tm.secs(x.b, x.c);
+    }
+    (void)e3;
+    Sst.t_encode = tm.secs(e3, e4);
+    for (uint32_t q = 0; q < NP; ++q) {
+        const int cls = q < T.n_upper ? 0 : q == T.phase_L2() ? 1 : q == T.phase_L1() ? 2 : 3;
+        Sst.nodes[cls] += pc[q];
+    }
+    for (int c = 0; c < 4; ++c) Sst.algo_evals[c] = ev_h[c];
+    Sst.data_bits = sdh.D;
+    Sst.index_bits = sdh.lowC + sdh.upC + sdh.lowP + sdh.upP;
+    Sst.max_bucket = fl[0];
+    Sst.kernel_launches = g_launches;
+    Sst.t_d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count() - tm.secs(e0, e4);
+    if (Sst.t_d2h < 0) Sst.t_d2h = 0;
+    Sst.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    return true;
+}
+
 void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, bool want_values,
                      BuildOutput& out) {
     auto t_start = std::chrono::steady_clock::now();
     const int world = (int)std::max<uint32_t>(1, p.shards);
+    static const int fast = getenv("RS_ONE_ENQUEUE") ? atoi(getenv("RS_ONE_ENQUEUE")) : 1;
+    if (fast && world == 1 && !want_values && p.cuts.empty() && build_single_fast(d_keys, p, st, out)) return;
     std::vector<std::unique_ptr<Shard>> shards;
     std::vector<uint64_t> all(8 * world);
     for (int r = 0; r < world; ++r) {  // virtual shards run one after the other
@@ -879,7 +1197,7 @@ void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t 
     for (auto& s : shards) dR = std::min(dR, s->min_step(all.data()));
     if (dR == LLONG_MAX) dR = 0;
     if (world == 1) {
-        shards[0]->finish_blob(dR, out.bytes);
+        shards[0]->finish_blob(dR, out.raw, out.raw_size);
     } else {
         std::vector<std::vector<uint8_t>> parts(world);
         std::vector<std::pair<const uint8_t*, size_t>> views;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -46,6 +47,16 @@ void shard_range(const BuildParams& p, uint64_t B, int rank, int world, uint64_t
 
 struct BuildOutput {
     std::vector<uint8_t> bytes;
+    // single-shard builds: the serialized MPHF in a malloc'ed buffer (handed to the caller
+    // without another copy); bytes stays empty then
+    uint8_t* raw = nullptr;
+    size_t raw_size = 0;
+    BuildOutput() = default;
+    BuildOutput(const BuildOutput&) = delete;
+    BuildOutput& operator=(const BuildOutput&) = delete;
+    ~BuildOutput() { free(raw); }
+    const uint8_t* data() const { return raw ? raw : bytes.data(); }
+    size_t size() const { return raw ? raw_size : bytes.size(); }
     std::vector<uint64_t> values;  // only when requested
     recsplit_stats stats{};
 };
@@ -74,8 +85,8 @@ class Shard {
     long long min_step(const uint64_t* all_summaries);
     // phase 3: EF and data slices at their global bit positions -> serialized part
     void finish(long long dR, std::vector<uint8_t>& part);
-    // phase 3 for a single shard (world 1): the serialized MPHF directly
-    void finish_blob(long long dR, std::vector<uint8_t>& blob);
+    // phase 3 for a single shard (world 1): the serialized MPHF directly (malloc'ed)
+    void finish_blob(long long dR, uint8_t*& blob, size_t& size);
     const Globals& globals() const;
     struct Impl;
     std::vector<uint64_t> values;  // node values of the shard (want_values)

@@ -33,8 +33,7 @@ namespace {
 
 constexpr u32 kWarpsPerBlockMax = 4;
 constexpr u64 kSeedCap = 1ull << 40;  // diagnostic trial cap per node (R11)
-constexpr u32 kQWords = 384;
-constexpr u32 kWarpKeyCap = 8192;     // largest node the warp engine holds in shared memory          // per-warp early-rejection queues: two stages x 3 x 64 words
+constexpr u32 kWarpKeyCap = 8192;     // largest node the warp engine holds in shared memory
 
 struct Args {
     const NodeRec* nodes;
@@ -66,6 +65,7 @@ struct Args {
     u64* lo_w;     // fused redistribution (batch-mode split phases, nodes <= kFuseMax keys): the
     u8* ab_w;      // key arrays written in child order right after the node's search; null = off
     u32 upper_kp;  // upper splits in batch mode: keys-parallel sequential seeds (upper_keys_parallel)
+    u32 qwords;    // early-rejection queue words per warp (0 for the plain variants)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -94,6 +94,7 @@ struct KeysView {
     const u32* __restrict__ G;  // groups
     u32 tbase;                  // shared-space byte address of the shift table
     u32 H;                      // carry path: high word of every value of the window
+    u32 fbase;                  // shared-space byte address of s_full_tab (64-byte aligned)
 };
 
 template <u32 GW>
@@ -139,7 +140,7 @@ enum { V_PLAIN = 0, V_CP = 1, V_WIDE = 2 };
 // Block-wide shift tables of the FULL lower-level nodes of a phase (all share f and w):
 // index 0 = lower level 1 (f1 parts of l), 1 = lower level 2 (f2 parts of u1).  Static
 // shared arrays have link-time addresses, so the lookup is LDS [part + imm].
-__shared__ __align__(16) u8 s_full_tab[2][32];
+__shared__ __align__(64) u8 s_full_tab[2][32];
 // early-rejection constants of the two full classes (run_window_cp): {me, ke, ce, mo, ko, co}
 // for the "some field > unit" test, then {Me, Mo, tope | topo << 8 | w << 16, thr} for the
 // last-part test (sum of fields 0..f-2 < thr = keys so far - unit; thr = 0: off), then thr of
@@ -147,8 +148,25 @@ __shared__ __align__(16) u8 s_full_tab[2][32];
 __shared__ u32 s_cp_masks[2][11];
 
 // increment 1 << s_full_tab[c][remap(h, f)]
+#ifndef RS_TAB_OR
+#define RS_TAB_OR 0
+#endif
 template <int CL>
-__device__ __forceinline__ u32 inc_full(u32 h, u32 f) { return bit_clamp(s_full_tab[CL][__umulhi(h, f)]); }
+__device__ __forceinline__ u32 inc_full(u32 h, u32 f, u32 fbase) {
+#if RS_TAB_OR
+    // row CL of the 64-byte aligned table is 32-byte aligned and part < 32, so OR = ADD; an OR
+    // keeps ptxas from folding the base into IMAD.HI's 64-bit addend (which costs two
+    // IMAD.MOV per four keys on the FMA-heavy pipe to rebuild the {0, base} pair)
+    u32 sh;
+    asm("{\n\t.reg .u32 p, ad;\n\tmul.hi.u32 p, %1, %2;\n\tor.b32 ad, p, %3;\n\tld.shared.u8 %0, [ad];\n\t}"
+        : "=r"(sh)
+        : "r"(h), "r"(f), "r"(fbase + 32u * CL));
+    return bit_clamp(sh);
+#else
+    (void)fbase;
+    return bit_clamp(s_full_tab[CL][__umulhi(h, f)]);
+#endif
+}
 
 
 // increment 1 << table[remap(h, r)]: the byte address comes straight out of mad.hi
@@ -176,8 +194,8 @@ __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, 
         u32 h[4];
         hash4<MODE>(g, sigma, h, K.H);
         if (CL < 2) {
-            c0 += inc_full<CL>(h[0], r) + inc_full<CL>(h[1], r);
-            c1 += inc_full<CL>(h[2], r) + inc_full<CL>(h[3], r);
+            c0 += inc_full<CL>(h[0], r, K.fbase) + inc_full<CL>(h[1], r, K.fbase);
+            c1 += inc_full<CL>(h[2], r, K.fbase) + inc_full<CL>(h[3], r, K.fbase);
         } else {
             c0 += inc_of(h[0], r, K.tbase) + inc_of(h[1], r, K.tbase);
             c1 += inc_of(h[2], r, K.tbase) + inc_of(h[3], r, K.tbase);
@@ -186,7 +204,7 @@ __device__ __forceinline__ u32 count_lower(const KeysView& K, u32 s, u32 sigma, 
     if (TAIL)
         for (u32 j = (s >> 2) << 2; j < s; ++j) {
             const u32 h = hash1<MODE, 12>(K, j, sigma);
-            c0 += CL < 2 ? inc_full<(CL < 2 ? CL : 0)>(h, r) : inc_of(h, r, K.tbase);
+            c0 += CL < 2 ? inc_full<(CL < 2 ? CL : 0)>(h, r, K.fbase) : inc_of(h, r, K.tbase);
         }
     return c0 + c1;
 }
@@ -1006,11 +1024,11 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     const u32 cap = A.warp_cap;                    // keys (multiple of 4)
     const u32 gwords = GW * (cap / 4 + 1);         // key groups
     const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
-    u32* G = smem32 + (size_t)wib * (gwords + twords + kQWords);
+    u32* G = smem32 + (size_t)wib * (gwords + twords + A.qwords);
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
-    u32* QS = G + gwords + twords;  // early-rejection queues, kQWords per warp (64 entries each):
+    u32* QS = G + gwords + twords;  // early-rejection queues, A.qwords per warp (64 entries each):
     u32* QC = QS + 64;              // seeds + partial counters / masks, for up to two stages
-    const KeysView K{G, (u32)__cvta_generic_to_shared(T8)};
+    const KeysView K{G, (u32)__cvta_generic_to_shared(T8), 0u, (u32)__cvta_generic_to_shared(&s_full_tab[0][0])};
     if (KIND == SK_LOWER) {  // shift tables of full nodes: part p -> p*w (p < f-1), 32 for the last
         for (u32 t = threadIdx.x; t < 64; t += blockDim.x) {
             const u32 cl = t >> 5, p = t & 31;
@@ -1396,21 +1414,52 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
         k_search_upper_big<<<grid_big, 1024, 0, st>>>(P.nodes, P.n_nodes_host, P.lo, P.values, P.u2, P.err, P.dup);
         g_launches++;
     }
-    // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table
+    // kernel variant of the phase (its register count and queue needs set the occupancy)
+    int var = V_PLAIN;
+    if (P.kind == SK_LOWER) {
+        // the phase holds one level: lower level 2 iff its largest node exceeds u1
+        const bool l2 = P.max_size > P.u1;
+        const u32 unit = l2 ? P.u1 : P.leaf, f = l2 ? P.u2 / P.u1 : P.u1 / P.leaf;
+        const u32 w = 32 - __builtin_clz(unit + 1);
+        var = (f - 1) * w > 32 ? V_WIDE : (A.cp_l1 | A.cp_l2) ? V_CP : V_PLAIN;
+    } else if ((P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) && A.cp_leaf && P.max_size >= 10) {
+        var = V_CP;
+    }
+    const void* kfn = nullptr;
+    switch (P.kind) {
+        case SK_UPPER: kfn = (const void*)k_search<SK_UPPER>; break;
+        case SK_LOWER:
+            kfn = var == V_WIDE ? (const void*)k_search<SK_LOWER, V_WIDE>
+                  : var == V_CP ? (const void*)k_search<SK_LOWER, V_CP>
+                                : (const void*)k_search<SK_LOWER>;
+            break;
+        case SK_LEAF_RF:
+            kfn = var == V_CP ? (const void*)k_search<SK_LEAF_RF, V_CP> : (const void*)k_search<SK_LEAF_RF>;
+            break;
+        case SK_LEAF_BF:
+            kfn = var == V_CP ? (const void*)k_search<SK_LEAF_BF, V_CP> : (const void*)k_search<SK_LEAF_BF>;
+            break;
+    }
+    // early-rejection queues per warp (64 entries per array): splits keep (seed, counter) per
+    // stage (the wide variant seed + two counter words), leaves (seed, a, b) per stage
+    u32 qwords = 0;
+    if (var != V_PLAIN) {
+        const bool two = P.kind == SK_LOWER ? (P.max_size > P.u1 ? A.cp_l2b : A.cp_l1b) != 0 : A.cp_leaf2 != 0;
+        const u32 per_stage = (P.kind == SK_LOWER && var == V_CP) ? 128 : 192;
+        qwords = per_stage * (two ? 2 : 1);
+    }
+    A.qwords = qwords;
+    // warp-private buffer: key groups (12 or 20 words per 4 keys) + byte shift table + queues
     u32 cap = (std::min(P.max_size, kWarpKeyCap) + 3) & ~3u;
     if (cap < 32) cap = 32;
     A.warp_cap = cap;
     const u32 GW = (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) ? 20 : 12;
-    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + kQWords) * sizeof(u32);
+    const size_t per_warp = ((size_t)GW * (cap / 4 + 1) + (cap + 32 + 15) / 16 * 4 + qwords) * sizeof(u32);
     u32 wpb = kWarpsPerBlockMax;
     while (wpb > 1 && per_warp * wpb > 200 * 1024) --wpb;
     const size_t smem = per_warp * wpb;
-    // resident blocks per SM (occupancy), persistent grid
+    // resident blocks per SM (occupancy of the variant launched), persistent grid
     int occ = 1;
-    auto kfn = P.kind == SK_UPPER ? (const void*)k_search<SK_UPPER>
-               : P.kind == SK_LOWER ? (const void*)k_search<SK_LOWER>
-               : P.kind == SK_LEAF_RF ? (const void*)k_search<SK_LEAF_RF>
-                                      : (const void*)k_search<SK_LEAF_BF>;
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, (int)(wpb * 32), smem);
     if (occ < 1) occ = 1;
@@ -1441,27 +1490,22 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.ab_w = fused ? P.ab_w : nullptr;
     switch (P.kind) {
         case SK_UPPER: launch_kind<SK_UPPER>(P, A, wpb, smem, grid, st); break;
-        case SK_LOWER: {
-            // the phase holds one level: lower level 2 iff its largest node exceeds u1
-            const bool l2 = P.max_size > P.u1;
-            const u32 unit = l2 ? P.u1 : P.leaf, f = l2 ? P.u2 / P.u1 : P.u1 / P.leaf;
-            const u32 w = 32 - __builtin_clz(unit + 1);
-            if ((f - 1) * w > 32)
+        case SK_LOWER:
+            if (var == V_WIDE)
                 launch_kind<SK_LOWER, V_WIDE>(P, A, wpb, smem, grid, st);
-            else if (A.cp_l1 | A.cp_l2)
+            else if (var == V_CP)
                 launch_kind<SK_LOWER, V_CP>(P, A, wpb, smem, grid, st);
             else
                 launch_kind<SK_LOWER>(P, A, wpb, smem, grid, st);
             break;
-        }
         case SK_LEAF_RF:
-            if (A.cp_leaf && P.max_size >= 10)
+            if (var == V_CP)
                 launch_kind<SK_LEAF_RF, V_CP>(P, A, wpb, smem, grid, st);
             else
                 launch_kind<SK_LEAF_RF>(P, A, wpb, smem, grid, st);
             break;
         case SK_LEAF_BF:
-            if (A.cp_leaf && P.max_size >= 10)
+            if (var == V_CP)
                 launch_kind<SK_LEAF_BF, V_CP>(P, A, wpb, smem, grid, st);
             else
                 launch_kind<SK_LEAF_BF>(P, A, wpb, smem, grid, st);
@@ -1533,8 +1577,10 @@ __device__ __forceinline__ void reorder_node(const NodeRec r, u64 sigma, u64* __
 }
 
 __global__ void k_reorder(const NodeRec* __restrict__ nodes, u32 n_nodes, const u64* __restrict__ values,
-                          u64* __restrict__ lo, u8* __restrict__ ab, u32 leaf, u32 u1, u32 u2, u32 cap) {
+                          u64* __restrict__ lo, u8* __restrict__ ab, u32 leaf, u32 u1, u32 u2, u32 cap,
+                          const u32* n_nodes_dev) {
     extern __shared__ __align__(16) unsigned char rsm[];
+    if (n_nodes_dev) n_nodes = *n_nodes_dev;
     const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     u64* slo = reinterpret_cast<u64*>(rsm + (size_t)wib * cap * 9);
     u8* sab = reinterpret_cast<u8*>(slo + cap);
@@ -1564,7 +1610,7 @@ __global__ void k_reorder_big(const NodeRec* __restrict__ nodes, u32 n_nodes, co
 }
 
 void launch_reorder(const NodeRec* nodes, u32 n_nodes, const u64* values, u64* lo, u8* ab, u32 leaf, u32 u1, u32 u2,
-                    u32 max_size, int sm_count, u64* big_scratch, cudaStream_t st) {
+                    u32 max_size, int sm_count, u64* big_scratch, cudaStream_t st, const u32* n_nodes_dev) {
     if (n_nodes == 0) return;
     const u32 cap = (std::min(max_size, kReorderSmemCap) + 15) & ~15u;
     const size_t per_warp = (size_t)cap * 9;
@@ -1576,7 +1622,7 @@ void launch_reorder(const NodeRec* nodes, u32 n_nodes, const u64* values, u64* l
     if (occ < 1) occ = 1;
     u32 blocks = (n_nodes + wpb - 1) / wpb;
     blocks = std::min<u32>(blocks, (u32)(occ * sm_count));
-    k_reorder<<<blocks, wpb * 32, per_warp * wpb, st>>>(nodes, n_nodes, values, lo, ab, leaf, u1, u2, cap);
+    k_reorder<<<blocks, wpb * 32, per_warp * wpb, st>>>(nodes, n_nodes, values, lo, ab, leaf, u1, u2, cap, n_nodes_dev);
     g_launches++;
     if (max_size > kReorderSmemCap) {
         // big_scratch holds kReorderBigWarps slices of 2 * max_size words

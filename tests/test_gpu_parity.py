@@ -214,8 +214,8 @@ def test_duplicate_keys_rejected():
     assert e.value.code == rs.E_DUPLICATE
 
 
-@pytest.mark.parametrize("leaf,b,n", [(8, 20_000, 30_000), (16, 12_000, 40_000), (5, 9_000, 60_000),
-                                      (24, 10_000, 25_000), (3, 8_500, 17_500)])
+@pytest.mark.parametrize("leaf,b,n", [(8, 20_000, 30_000), (16, 12_000, 30_000), (5, 9_000, 60_000),
+                                      (12, 10_000, 25_000), (3, 8_500, 17_500)])
 def test_oversized_buckets_full_parity(leaf, b, n):
     """any bucket_size >= 1.  Buckets above the warp engine's 8192-key
     shared-memory capacity run their upper splits, redistribution and duplicate check
@@ -241,6 +241,26 @@ def test_bucket_cap_enforced():
     with pytest.raises(rs.RecSplitError) as e:
         rs.build(keys, 8, 70_000)
     assert e.value.code == rs.E_INVALID
+
+
+def test_one_enqueue_fallback_on_oversized_bucket():
+    """The one-enqueue single-shard path sizes its tables for buckets up to n/B + 8 sqrt(n/B)
+    + 32 keys; a bucket beyond that (here 400 keys at b = 100, chosen through the oracle's
+    master hash) is flagged on the device and the build reruns on the synchronized path --
+    the bytes still equal the oracle's."""
+    rng = np.random.default_rng(77)
+    n, b = 4000, 100
+    B = (n + b - 1) // b
+    cand = rng.integers(0, M64, size=200_000, dtype=np.uint64, endpoint=True)
+    hi, _ = _mhc_np(cand)
+    bucket = ((hi >> np.uint64(32)) * np.uint64(B)) >> np.uint64(32)
+    in0 = np.unique(cand[bucket == 0])[:400]
+    rest = np.unique(cand[bucket != 0])[:n - 400]
+    keys = np.concatenate([in0, rest])
+    assert len(np.unique(keys)) == n
+    got, st = rs.build(keys, 8, b, stats=True)
+    assert st["max_bucket"] == 400
+    assert got == oracle.build(keys, 8, b, threads=os.cpu_count())
 
 
 def test_device_entry_matches_host_entry():
