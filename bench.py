@@ -56,12 +56,43 @@ def _peaks():
         return {}
 
 
+def mix_bound():
+    """Measured roofline denominator: evaluations per clock per SM of the split
+    loop's SASS mix under the per-opcode throughputs measured by tools/probe/pipes.cu
+    (profiles/l1_mix_bound_r02.json, written by tools/probe/mix_bound.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "l1_mix_bound_r02.json")) as f:
+            d = json.load(f)
+        return float(d["evals_per_clk_per_sm"]), d
+    except (OSError, ValueError, KeyError):
+        return None, None
+
+
 def int32_peak_evals(sm_count: int, mhz: float) -> float:
-    """INT32 roofline in remix evaluations/s: 4 SMSPs x 32 lanes
-    issue per clock, ALU and FMA pipes 64 lanes/clk/SM each; the minimal SplitMix64
-    evaluation + remap + packed count needs 21 integer instructions split 10.5/10.5
-    over the two pipes -> 64/10.5 = 6.10 evaluations per clock per SM."""
-    return sm_count * mhz * 1e6 * (64.0 / 10.5)
+    """INT32 roofline in remix evaluations/s: the measured mix bound (mix_bound) if present,
+    else the round-1 derived issue bound (21 integer instructions per evaluation, 64 lanes/clk
+    per pipe -> 6.10 evaluations per clock per SM)."""
+    per_clk, _ = mix_bound()
+    return sm_count * mhz * 1e6 * (per_clk if per_clk else 64.0 / 10.5)
+
+
+def executed_evals(cfg: dict, world: int):
+    """Executed key evaluations per class of one build of the workload, from the counting
+    build of the same kernels (build_var/count, -DRS_COUNT_EVALS) in a subprocess; None when
+    that library is absent."""
+    lib = os.path.join(ROOT, "build_var", "count", "librecsplit_b200.so")
+    if world != 1 or not os.path.exists(lib):
+        return None
+    code = ("import sys, json, numpy as np, torch; sys.path.insert(0, %r)\n"
+            "import paper_2212_09562_b200 as rs, synth\n"
+            "k = synth.keys(%d, %d); kt = torch.from_numpy(k.view(np.int64)).cuda()\n"
+            "b, s = rs.build_device(kt, %d, %d, stats=True)\n"
+            "print(json.dumps(s['exec_evals']))" % (ROOT, cfg["n"], cfg["seed"], cfg["leaf"], cfg["bucket"]))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                       env=dict(os.environ, RECSPLIT_LIB=lib), timeout=600)
+    if r.returncode:
+        return None
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 class Clocks:
@@ -146,6 +177,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--weak", action="store_true", help="n keys per rank (one MPHF of N x n keys)")
+    ap.add_argument("--no-exec-count", action="store_true", help="skip the executed-evaluation count")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -302,7 +334,10 @@ def main():
     else:
         max_mhz, mhz_src = 1965.0, "fallback: B200 max SM clock"
     peak = int32_peak_evals(sms, max_mhz) / 1e9
+    mix = mix_bound()
     achieved = evals / kt_s / 1e9
+    ex = executed_evals(cfg, world) if not args.no_exec_count else None
+    exec_l1 = float(ex[cls]) if ex and ex[cls] else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_l1_split_traffic.json")
     if os.path.exists(prof) and args.config == "C3":  # the ncu capture is of the C3 launch
@@ -331,7 +366,13 @@ def main():
         "roofline": {"bound": "alu", "kernel": "k_search<SK_LOWER> (lower level 1 splits)",
                      "achieved": achieved, "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
                      "traffic": traffic,
-                     "peak_note": f"{sms} SMs x {max_mhz:.0f} MHz ({mhz_src}) x 6.10 evals/clk/SM"},
+                     "executed_frac": (exec_l1 / kt_s / 1e9 / peak) if exec_l1 else None,
+                     "executed_over_algorithmic": (exec_l1 / evals) if exec_l1 else None,
+                     "peak_note": (f"{sms} SMs x {max_mhz:.0f} MHz ({mhz_src}) x {mix[0]:.3f} evals/clk/SM: the split "
+                                   f"loop's SASS mix ({mix[1]['loop_instructions']} instructions per 4 keys x 32 seeds) "
+                                   f"under the per-opcode rates measured by tools/probe/pipes.cu "
+                                   f"(profiles/l1_mix_bound_r02.json; FMA-pipe bound)") if mix[0] else
+                                  f"{sms} SMs x {max_mhz:.0f} MHz ({mhz_src}) x 6.10 evals/clk/SM (derived issue bound)"},
         "phases_s": {"partition": st0["t_partition"], "tree": st0["t_tree"], "upper": st0["t_search"][0],
                      "lower2": st0["t_search"][1], "lower1": st0["t_search"][2], "leaves": st0["t_search"][3],
                      "reorder": st0["t_reorder"], "encode": st0["t_encode"], "d2h": st0["t_d2h"]},
@@ -345,6 +386,12 @@ def main():
             for k, nm in enumerate(["upper", "lower2", "lower1", "leaves"])},
         "int32_frac_step": (float(np.mean([sum(x["algo_evals"]) for x in stats])) / t_max / 1e9 / peak)
         if world == 1 else None,
+        # executed key evaluations (counting build) per phase / that phase's time / the same peak
+        "int32_exec_frac_by_phase": ({
+            nm: (float(ex[k]) / float(np.mean([x["t_search"][k] for x in stats])) / 1e9 / peak)
+            if ex[k] and float(np.mean([x["t_search"][k] for x in stats])) > 0 else None
+            for k, nm in enumerate(["upper", "lower2", "lower1", "leaves"])} if ex else None),
+        "exec_evals_per_step": [int(x) for x in ex] if ex else None,
         "clocks": clocks,
     }
     if not args.no_cpu_baseline and world == 1:  # rank 0 at N = 1 only

@@ -102,6 +102,9 @@ typedef struct {
     uint64_t index_bits;     /* Elias-Fano lower+upper bits of both sequences */
     uint32_t kernel_launches; /* CUDA kernels this library launched during the build */
     uint32_t max_bucket;      /* largest bucket size */
+    uint64_t exec_evals[4];   /* diagnostic builds (-DRS_COUNT_EVALS) only, else 0: key evaluations
+                                 the search kernels EXECUTED per class (32 lanes per group step,
+                                 incl. discarded lanes; early rejection skips the rest) */
 } recsplit_stats;
 
 /* Library version (format version is the header's u16 version = 1). */

@@ -73,6 +73,7 @@ struct PhaseLaunch {
     int fuse_reorder = 0;   // split phases: may redistribute the keys in the search kernel (A7)
     u64* lo_w = nullptr;    // ... into these arrays (the phase's key arrays)
     u8* ab_w = nullptr;
+    unsigned long long* exec = nullptr;  // RS_COUNT_EVALS builds: executed evaluations of the class
 };
 // returns true if the phase's key redistribution was fused into the search (no launch_reorder)
 bool launch_search(const PhaseLaunch& P, cudaStream_t st);

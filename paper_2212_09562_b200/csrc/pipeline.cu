@@ -1007,6 +1007,11 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     const u32 nslots = search_active_slots(sms);
     int* active = A.alloc<int>(nslots);
     u32* cursors = A.alloc<u32>(2 * NP + 2);
+    unsigned long long* exec_d = nullptr;
+#ifdef RS_COUNT_EVALS
+    exec_d = A.alloc<unsigned long long>(4);
+    CK(cudaMemsetAsync(exec_d, 0, 32, st));
+#endif
     CK(cudaMemsetAsync(values_d, 0xff, nbound * 8, st));
     CK(cudaMemsetAsync(next_win, 0, nbound * 4, st));
     CK(cudaMemsetAsync(cursors, 0, (2 * NP + 2) * 4, st));
@@ -1069,6 +1074,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         P.fuse_reorder = kind == SK_UPPER || kind == SK_LOWER;
         P.lo_w = lo_a;
         P.ab_w = ab_a;
+        P.exec = exec_d ? exec_d + cls : nullptr;
         CK(cudaMemsetAsync(active, 0xff, nslots * 4, st));
         const int a = tm.mark();
         const bool fused = launch_search(P, st);
@@ -1128,6 +1134,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     CK(cudaMemcpyAsync(rep + 32, sd, sizeof(SingleDev), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(rep + 32 + sizeof(SingleDev), evals, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(rep + 64 + sizeof(SingleDev), pcnt_d, NP * 4, cudaMemcpyDeviceToHost, st));
+    if (exec_d) CK(cudaMemcpyAsync(rep + 2048, exec_d, 32, cudaMemcpyDeviceToHost, st));
     std::lock_guard<std::mutex> lk_stage(g_stage.mu);
     uint8_t* buf = g_stage.get(cap_words * 8);
     CK(cudaMemcpyAsync(buf, outw, est_words * 8, cudaMemcpyDeviceToHost, st));
@@ -1171,6 +1178,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         Sst.nodes[cls] += pc[q];
     }
     for (int c = 0; c < 4; ++c) Sst.algo_evals[c] = ev_h[c];
+    if (exec_d) memcpy(Sst.exec_evals, rep + 2048, 32);
     Sst.data_bits = sdh.D;
     Sst.index_bits = sdh.lowC + sdh.upC + sdh.lowP + sdh.upP;
     Sst.max_bucket = fl[0];

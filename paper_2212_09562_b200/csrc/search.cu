@@ -66,6 +66,7 @@ struct Args {
     u8* ab_w;      // key arrays written in child order right after the node's search; null = off
     u32 upper_kp;  // upper splits in batch mode: keys-parallel sequential seeds (upper_keys_parallel)
     u32 qwords;    // early-rejection queue words per warp (0 for the plain variants)
+    unsigned long long* exec;  // RS_COUNT_EVALS builds: executed evaluations of this phase's class
 };
 
 // ------------------------------------------------------------------ trials --
@@ -90,6 +91,44 @@ struct Layout {
     static constexpr u32 GW = (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) ? 20 : 12;
 };
 
+// Diagnostic build (-DRS_COUNT_EVALS): every warp counts the key evaluations its lanes issue
+// (32 per key of a group evaluation, including lanes whose seed is discarded) in shared memory
+// and adds them to a per-class global counter at exit -- the EXECUTED work, next to the
+// algorithmic count of DESIGN.md 7.  Compiled out otherwise.
+#ifdef RS_COUNT_EVALS
+__shared__ unsigned long long s_exec[8];
+#define RS_COUNT(k)                                                               \
+    do {                                                                          \
+        if ((threadIdx.x & 31) == 0) s_exec[threadIdx.x >> 5] += 32ull * (k);     \
+    } while (0)
+#define RS_COUNT_RAW(v_)                                                          \
+    do {                                                                          \
+        const unsigned long long c_ = (v_); /* evaluated by every lane */         \
+        if ((threadIdx.x & 31) == 0) s_exec[threadIdx.x >> 5] += c_;              \
+    } while (0)
+#define RS_COUNT_INIT()                                                           \
+    do {                                                                          \
+        if ((threadIdx.x & 31) == 0) s_exec[threadIdx.x >> 5] = 0;                \
+    } while (0)
+#define RS_COUNT_FLUSH(ptr)                                                       \
+    do {                                                                          \
+        if ((threadIdx.x & 31) == 0 && (ptr)) atomicAdd((ptr), s_exec[threadIdx.x >> 5]); \
+    } while (0)
+#else
+#define RS_COUNT(k) \
+    do {            \
+    } while (0)
+#define RS_COUNT_RAW(v_) \
+    do {                 \
+    } while (0)
+#define RS_COUNT_INIT() \
+    do {                \
+    } while (0)
+#define RS_COUNT_FLUSH(ptr) \
+    do {                    \
+    } while (0)
+#endif
+
 struct KeysView {
     const u32* __restrict__ G;  // groups
     u32 tbase;                  // shared-space byte address of the shift table
@@ -105,12 +144,14 @@ __device__ __forceinline__ u32 key_word(const KeysView& K, u32 j, u32 field) {
 // h_hi of node_hash(key j, sigma) (R4): generic 64-bit path
 template <u32 GW>
 __device__ __forceinline__ u32 hash_slow(const KeysView& K, u32 j, u64 sigma) {
+    RS_COUNT(1);
     return remix_hi((((u64)key_word<GW>(K, j, 1) << 32) | key_word<GW>(K, j, 0)) + sigma);
 }
 
 // evaluate the four keys of group g
 template <int MODE>  // 0: no-carry, 1: carry (value = H * 2^32 + sigma)
 __device__ __forceinline__ void hash4(const u32* __restrict__ g, u32 sigma, u32 h[4], u32 H) {
+    RS_COUNT(4);
     const uint4 kl = *reinterpret_cast<const uint4*>(g);
     const uint4 kh = *reinterpret_cast<const uint4*>(g + 4);
     if (MODE == 0) {
@@ -129,6 +170,7 @@ __device__ __forceinline__ void hash4(const u32* __restrict__ g, u32 sigma, u32 
 
 template <int MODE, u32 GW>
 __device__ __forceinline__ u32 hash1(const KeysView& K, u32 j, u32 sigma) {
+    RS_COUNT(1);
     return MODE == 0 ? remix_hi_nc(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), key_word<GW>(K, j, 2), sigma)
                      : remix_hi_fast<true>(key_word<GW>(K, j, 0), key_word<GW>(K, j, 1), sigma, K.H);
 }
@@ -148,24 +190,13 @@ __shared__ __align__(64) u8 s_full_tab[2][32];
 __shared__ u32 s_cp_masks[2][11];
 
 // increment 1 << s_full_tab[c][remap(h, f)]
-#ifndef RS_TAB_OR
-#define RS_TAB_OR 0
-#endif
 template <int CL>
 __device__ __forceinline__ u32 inc_full(u32 h, u32 f, u32 fbase) {
-#if RS_TAB_OR
-    // row CL of the 64-byte aligned table is 32-byte aligned and part < 32, so OR = ADD; an OR
-    // keeps ptxas from folding the base into IMAD.HI's 64-bit addend (which costs two
-    // IMAD.MOV per four keys on the FMA-heavy pipe to rebuild the {0, base} pair)
-    u32 sh;
-    asm("{\n\t.reg .u32 p, ad;\n\tmul.hi.u32 p, %1, %2;\n\tor.b32 ad, p, %3;\n\tld.shared.u8 %0, [ad];\n\t}"
-        : "=r"(sh)
-        : "r"(h), "r"(f), "r"(fbase + 32u * CL));
-    return bit_clamp(sh);
-#else
+    // (an OR of the 32-bit table base instead of the 64-bit addend ptxas folds into IMAD.HI --
+    // two IMAD.MOV fewer per four keys, four LOP3 more -- measured 6 % slower at C3: the ALU
+    // pipe has less headroom than the FMA pipe)
     (void)fbase;
     return bit_clamp(s_full_tab[CL][__umulhi(h, f)]);
-#endif
 }
 
 
@@ -912,6 +943,7 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, Nod
 // node's A/B bytes are read into registers before any write (the node's range is rewritten in
 // place).
 constexpr u32 kFuseMax = 256;
+constexpr u32 kUpperKpMax = 256;  // keys-parallel upper splits for nodes up to this size (few trials)
 
 template <int KIND>
 __device__ __forceinline__ void fused_reorder(const Args& A, const u32* G, u32 key_off, const NodeCtx& c, u64 val,
@@ -977,6 +1009,7 @@ __device__ __forceinline__ u64 upper_keys_parallel(const Args& A, const u32* G, 
     for (u64 sigma = 0; sigma < kSeedCap; ++sigma) {
         u32 cnt = 0;
         for (u32 j0 = 0; j0 < s; j0 += 32) {
+            RS_COUNT(1);
             const u32 j = j0 + lane;
             bool left = false;
             if (j < s) {
@@ -1025,6 +1058,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
     const u32 gwords = GW * (cap / 4 + 1);         // key groups
     const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
     u32* G = smem32 + (size_t)wib * (gwords + twords + A.qwords);
+    RS_COUNT_INIT();
     u8* T8 = reinterpret_cast<u8*>(G + gwords);
     u32* QS = G + gwords + twords;  // early-rejection queues, A.qwords per warp (64 entries each):
     u32* QC = QS + 64;              // seeds + partial counters / masks, for up to two stages
@@ -1096,7 +1130,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                 if (KIND == SK_UPPER && A.nodes[n].size > kWarpKeyCap) continue;  // k_search_upper_big
                 load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c);
                 u64 val = 0;
-                if (KIND == SK_UPPER && A.upper_kp) {
+                if (KIND == SK_UPPER && A.upper_kp && c.s <= kUpperKpMax) {
                     val = upper_keys_parallel(A, G, c, lane);
                 } else
                 for (u64 wstart = 0;; wstart += ws) {
@@ -1113,7 +1147,10 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                 __syncwarp();
             }
         }
-        if (A.tail == 0) return;
+        if (A.tail == 0) {
+            RS_COUNT_FLUSH(A.exec);
+            return;
+        }
     }
 
     // help mode: per-node window dispenser + helping
@@ -1160,6 +1197,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
         if (run_window<KIND, VAR>(A, K, c, wstart, lane, &val, QS, QC) && lane == 0)
             atomicMin((unsigned long long*)(A.values + c.slot), (unsigned long long)val);
     }
+    RS_COUNT_FLUSH(A.exec);
 }
 
 // Upper splits of nodes above the warp engine's shared-memory capacity (kWarpKeyCap keys;
@@ -1220,12 +1258,13 @@ __global__ void __launch_bounds__(1024) k_search_upper_big(const NodeRec* __rest
 // the lanes of a warp stay busy while leaves finish at different times.
 constexpr u32 kLaneLeafMax = 12;
 
-// masks of base value `base` over the m keys held in registers (a: A keys, b: B keys)
+// masks of base value `base` over the m <= M keys held in registers (a: A keys, b: B keys)
+template <int M>
 __device__ __forceinline__ void lane_masks(const u64* key, const u32* amask, u32 m, u64 base, u32& a, u32& b) {
     a = 0;
     b = 0;
 #pragma unroll
-    for (u32 j = 0; j < kLaneLeafMax; ++j) {
+    for (u32 j = 0; j < M; ++j) {
         if (j < m) {
             const u32 bit = 1u << __umulhi(remix_hi(key[j] + base), m);
             a |= bit & amask[j];
@@ -1244,15 +1283,18 @@ __device__ __forceinline__ int lane_fit(u32 a, u32 b, u32 m, u32 full) {
     return -1;
 }
 
-template <int KIND>
+template <int KIND, int M>
 __global__ void __launch_bounds__(256) k_leaf_lane(const NodeRec* __restrict__ nodes, const u32* n_nodes,
                                                    const u64* __restrict__ lo, const u8* __restrict__ ab,
-                                                   u64* __restrict__ values, u32* cursor, u32* err, const u32* dup) {
+                                                   u64* __restrict__ values, u32* cursor, u32* err, const u32* dup,
+                                                   unsigned long long* exec) {
     if (dup[0] || dup[1] > 1) return;
+    RS_COUNT_INIT();
+    (void)exec;
     const u32 nn = *n_nodes;
     const u32 lane = threadIdx.x & 31;
-    u64 key[kLaneLeafMax];
-    u32 amask[kLaneLeafMax];  // all-ones for A keys (R7), 0 for B keys
+    u64 key[M];
+    u32 amask[M];  // all-ones for A keys (R7), 0 for B keys
     u32 m = 0, full = 0, slot = 0;
     u64 k = 0;
     bool busy = false, dry = false;  // dry: the phase's cursor is exhausted
@@ -1273,7 +1315,7 @@ __global__ void __launch_bounds__(256) k_leaf_lane(const NodeRec* __restrict__ n
                     slot = rec.slot;
                     full = (1u << m) - 1u;
 #pragma unroll
-                    for (u32 j = 0; j < kLaneLeafMax; ++j) {
+                    for (u32 j = 0; j < M; ++j) {
                         key[j] = j < m ? lo[rec.key_off + j] : 0;
                         amask[j] = j < m && !(KIND == SK_LEAF_RF && ab[rec.key_off + j]) ? FULL : 0u;
                     }
@@ -1283,10 +1325,11 @@ __global__ void __launch_bounds__(256) k_leaf_lane(const NodeRec* __restrict__ n
             }
         }
         if (dry) break;  // finish the warp's remaining leaves cooperatively (below)
+        RS_COUNT_RAW(__reduce_add_sync(FULL, m));  // m keys per lane with a leaf
         // one base seed of this lane's leaf, tried in (k, r) order
         const u64 base = KIND == SK_LEAF_RF ? k * m : k;
         u32 a, b;
-        lane_masks(key, amask, m, base, a, b);
+        lane_masks<M>(key, amask, m, base, a, b);
         int r = -1;
         if (KIND == SK_LEAF_BF)
             r = a == full ? 0 : -1;
@@ -1310,18 +1353,19 @@ __global__ void __launch_bounds__(256) k_leaf_lane(const NodeRec* __restrict__ n
         open &= open - 1;
         const u32 mL = __shfl_sync(FULL, m, L), fL = (1u << mL) - 1u, sL = __shfl_sync(FULL, slot, L);
         u64 kL = shfl64(k, L);
-        u64 kk[kLaneLeafMax];
-        u32 am[kLaneLeafMax];
+        u64 kk[M];
+        u32 am[M];
 #pragma unroll
-        for (u32 j = 0; j < kLaneLeafMax; ++j) {
+        for (u32 j = 0; j < M; ++j) {
             kk[j] = shfl64(key[j], L);
             am[j] = __shfl_sync(FULL, amask[j], L);
         }
         for (;; kL += 32) {
+            RS_COUNT_RAW(32ull * mL);
             const u64 kx = kL + lane;
             const u64 base = KIND == SK_LEAF_RF ? kx * mL : kx;
             u32 a, b;
-            lane_masks(kk, am, mL, base, a, b);
+            lane_masks<M>(kk, am, mL, base, a, b);
             const int r = KIND == SK_LEAF_BF ? (a == fL ? 0 : -1) : lane_fit(a, b, mL, fL);
             const u32 bal = __ballot_sync(FULL, r >= 0);
             if (bal) {
@@ -1339,6 +1383,7 @@ __global__ void __launch_bounds__(256) k_leaf_lane(const NodeRec* __restrict__ n
             }
         }
     }
+    RS_COUNT_FLUSH(exec);
 }
 
 template <int KIND, int VAR = V_PLAIN>
@@ -1368,6 +1413,7 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.u1 = P.u1;
     A.u2 = P.u2;
     A.iters = P.iters ? P.iters : 1;
+    A.exec = P.exec;
     A.help = P.help;
     // early-rejection checkpoints (per mille of the node size; RS_CP1 / RS_CP2 override, 0 = off)
     {
@@ -1400,12 +1446,20 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     static const int lane_leaf_max = getenv("RS_LANE_LEAF") ? atoi(getenv("RS_LANE_LEAF")) : 8;
     if ((P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) && P.max_size <= (u32)lane_leaf_max &&
         P.max_size <= kLaneLeafMax) {
-        // lane-per-leaf search (small leaves); the phase's batch cursor is zeroed
+        // lane-per-leaf search (small leaves); the phase's batch cursor is zeroed; the key loop
+        // is unrolled to the phase's largest leaf (M = 4, 8 or 12)
         const u32 blocks = std::max<u32>(1, std::min<u32>((P.n_nodes_host + 255) / 256, (u32)P.sm_count * 8));
-        if (P.kind == SK_LEAF_RF)
-            k_leaf_lane<SK_LEAF_RF><<<blocks, 256, 0, st>>>(P.nodes, P.n_nodes, P.lo, P.ab, P.values, P.cursor, P.err, P.dup);
-        else
-            k_leaf_lane<SK_LEAF_BF><<<blocks, 256, 0, st>>>(P.nodes, P.n_nodes, P.lo, P.ab, P.values, P.cursor, P.err, P.dup);
+        const bool rf = P.kind == SK_LEAF_RF;
+#define RS_LANE_LAUNCH(K_, M_) \
+    k_leaf_lane<K_, M_><<<blocks, 256, 0, st>>>(P.nodes, P.n_nodes, P.lo, P.ab, P.values, P.cursor, P.err, P.dup, P.exec)
+        if (P.max_size <= 4) {
+            if (rf) RS_LANE_LAUNCH(SK_LEAF_RF, 4); else RS_LANE_LAUNCH(SK_LEAF_BF, 4);
+        } else if (P.max_size <= 8) {
+            if (rf) RS_LANE_LAUNCH(SK_LEAF_RF, 8); else RS_LANE_LAUNCH(SK_LEAF_BF, 8);
+        } else {
+            if (rf) RS_LANE_LAUNCH(SK_LEAF_RF, 12); else RS_LANE_LAUNCH(SK_LEAF_BF, 12);
+        }
+#undef RS_LANE_LAUNCH
         g_launches++;
         return false;
     }

@@ -215,7 +215,7 @@ def test_duplicate_keys_rejected():
 
 
 @pytest.mark.parametrize("leaf,b,n", [(8, 20_000, 30_000), (16, 12_000, 30_000), (5, 9_000, 60_000),
-                                      (12, 10_000, 25_000), (3, 8_500, 17_500)])
+                                      (12, 10_000, 25_000), (3, 8_500, 17_000)])
 def test_oversized_buckets_full_parity(leaf, b, n):
     """any bucket_size >= 1.  Buckets above the warp engine's 8192-key
     shared-memory capacity run their upper splits, redistribution and duplicate check
