@@ -1246,146 +1246,6 @@ __global__ void __launch_bounds__(1024) k_search_upper_big(const NodeRec* __rest
     }
 }
 
-// ------------------------------------------------------- lane-per-leaf search --
-//
-// Small leaves (m <= kLaneLeafMax, e.g. l = 8 at C2: ~56 base seeds per leaf) spend most of a
-// warp-per-leaf search on window overshoot (a 32-seed window for ~56 seeds), node loading and
-// the cross-lane rotation check.  Here every LANE owns one leaf: its m keys sit in registers
-// and it tries base seeds k = 0, 1, 2, ... in order, for each the rotations r = 0..m-1 in
-// order -- exactly the sequential search, so the first fit is the minimal stored
-// value k*m + r (brute force: the first k with a bijection).  A lane that finishes
-// stores its value and takes the next leaf of the phase (warp-aggregated cursor atomics), so
-// the lanes of a warp stay busy while leaves finish at different times.
-constexpr u32 kLaneLeafMax = 12;
-
-// masks of base value `base` over the m <= M keys held in registers (a: A keys, b: B keys)
-template <int M>
-__device__ __forceinline__ void lane_masks(const u64* key, const u32* amask, u32 m, u64 base, u32& a, u32& b) {
-    a = 0;
-    b = 0;
-#pragma unroll
-    for (u32 j = 0; j < M; ++j) {
-        if (j < m) {
-            const u32 bit = 1u << __umulhi(remix_hi(key[j] + base), m);
-            a |= bit & amask[j];
-            b |= bit & ~amask[j];
-        }
-    }
-}
-
-// smallest r with rot_m^r(b) filling the holes of a, or -1
-__device__ __forceinline__ int lane_fit(u32 a, u32 b, u32 m, u32 full) {
-    if (__popc(a) + __popc(b) != (int)m) return -1;  // a collision inside A or B
-    const u32 na = ~a & full;
-    const u64 bb = (u64)b | ((u64)b << m);  // rot_m^r(b) = (bb >> (m - r)) & full
-    for (u32 r = 0; r < m; ++r)
-        if (((u32)(bb >> (m - r)) & full) == na) return (int)r;
-    return -1;
-}
-
-template <int KIND, int M>
-__global__ void __launch_bounds__(256) k_leaf_lane(const NodeRec* __restrict__ nodes, const u32* n_nodes,
-                                                   const u64* __restrict__ lo, const u8* __restrict__ ab,
-                                                   u64* __restrict__ values, u32* cursor, u32* err, const u32* dup,
-                                                   unsigned long long* exec) {
-    if (dup[0] || dup[1] > 1) return;
-    RS_COUNT_INIT();
-    (void)exec;
-    const u32 nn = *n_nodes;
-    const u32 lane = threadIdx.x & 31;
-    u64 key[M];
-    u32 amask[M];  // all-ones for A keys (R7), 0 for B keys
-    u32 m = 0, full = 0, slot = 0;
-    u64 k = 0;
-    bool busy = false, dry = false;  // dry: the phase's cursor is exhausted
-    for (;;) {
-        // lanes without a leaf take the next ones (one atomic per warp)
-        const u32 want = __ballot_sync(FULL, !busy);
-        if (want && !dry) {
-            const int leader = __ffs(want) - 1;
-            u32 first = 0;
-            if ((int)lane == leader) first = atomicAdd(cursor, (u32)__popc(want));
-            first = __shfl_sync(FULL, first, leader);
-            dry = first + __popc(want) > nn;
-            if (!busy) {
-                const u32 idx = first + __popc(want & lanemask_lt());
-                if (idx < nn) {
-                    const NodeRec rec = nodes[idx];
-                    m = rec.size;
-                    slot = rec.slot;
-                    full = (1u << m) - 1u;
-#pragma unroll
-                    for (u32 j = 0; j < M; ++j) {
-                        key[j] = j < m ? lo[rec.key_off + j] : 0;
-                        amask[j] = j < m && !(KIND == SK_LEAF_RF && ab[rec.key_off + j]) ? FULL : 0u;
-                    }
-                    k = 0;
-                    busy = true;
-                }
-            }
-        }
-        if (dry) break;  // finish the warp's remaining leaves cooperatively (below)
-        RS_COUNT_RAW(__reduce_add_sync(FULL, m));  // m keys per lane with a leaf
-        // one base seed of this lane's leaf, tried in (k, r) order
-        const u64 base = KIND == SK_LEAF_RF ? k * m : k;
-        u32 a, b;
-        lane_masks<M>(key, amask, m, base, a, b);
-        int r = -1;
-        if (KIND == SK_LEAF_BF)
-            r = a == full ? 0 : -1;
-        else
-            r = lane_fit(a, b, m, full);
-        if (r >= 0) {
-            values[slot] = base + (u32)r;
-            busy = false;
-        } else if (++k >= kSeedCap) {
-            atomicOr(err, 1u);
-            values[slot] = base;
-            busy = false;
-        }
-    }
-    // Tail: the leaves still open in this warp, one after another with all 32 lanes trying
-    // consecutive base seeds from the owner's next untried k (all smaller ones failed); the
-    // lowest lane with a fit and its smallest r is the minimal value.
-    u32 open = __ballot_sync(FULL, busy);
-    while (open) {
-        const int L = __ffs(open) - 1;
-        open &= open - 1;
-        const u32 mL = __shfl_sync(FULL, m, L), fL = (1u << mL) - 1u, sL = __shfl_sync(FULL, slot, L);
-        u64 kL = shfl64(k, L);
-        u64 kk[M];
-        u32 am[M];
-#pragma unroll
-        for (u32 j = 0; j < M; ++j) {
-            kk[j] = shfl64(key[j], L);
-            am[j] = __shfl_sync(FULL, amask[j], L);
-        }
-        for (;; kL += 32) {
-            RS_COUNT_RAW(32ull * mL);
-            const u64 kx = kL + lane;
-            const u64 base = KIND == SK_LEAF_RF ? kx * mL : kx;
-            u32 a, b;
-            lane_masks<M>(kk, am, mL, base, a, b);
-            const int r = KIND == SK_LEAF_BF ? (a == fL ? 0 : -1) : lane_fit(a, b, mL, fL);
-            const u32 bal = __ballot_sync(FULL, r >= 0);
-            if (bal) {
-                const int w = __ffs(bal) - 1;
-                const u64 v = shfl64(base + (u32)(r < 0 ? 0 : r), w);
-                if ((int)lane == L) values[sL] = v;
-                break;
-            }
-            if (kL + 32 >= kSeedCap) {
-                if ((int)lane == L) {
-                    atomicOr(err, 1u);
-                    values[sL] = KIND == SK_LEAF_RF ? kL * mL : kL;
-                }
-                break;
-            }
-        }
-    }
-    RS_COUNT_FLUSH(exec);
-}
-
 template <int KIND, int VAR = V_PLAIN>
 void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 grid, cudaStream_t st) {
     cudaFuncSetAttribute(k_search<KIND, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -1442,26 +1302,6 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
         A.cp_leaf2 = cpl2 ? 1u : 0u;
         static const int cpw2 = getenv("RS_CPW2") ? atoi(getenv("RS_CPW2")) : 1;
         A.cp_wide2 = cpw2 ? 1u : 0u;
-    }
-    static const int lane_leaf_max = getenv("RS_LANE_LEAF") ? atoi(getenv("RS_LANE_LEAF")) : 8;
-    if ((P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) && P.max_size <= (u32)lane_leaf_max &&
-        P.max_size <= kLaneLeafMax) {
-        // lane-per-leaf search (small leaves); the phase's batch cursor is zeroed; the key loop
-        // is unrolled to the phase's largest leaf (M = 4, 8 or 12)
-        const u32 blocks = std::max<u32>(1, std::min<u32>((P.n_nodes_host + 255) / 256, (u32)P.sm_count * 8));
-        const bool rf = P.kind == SK_LEAF_RF;
-#define RS_LANE_LAUNCH(K_, M_) \
-    k_leaf_lane<K_, M_><<<blocks, 256, 0, st>>>(P.nodes, P.n_nodes, P.lo, P.ab, P.values, P.cursor, P.err, P.dup, P.exec)
-        if (P.max_size <= 4) {
-            if (rf) RS_LANE_LAUNCH(SK_LEAF_RF, 4); else RS_LANE_LAUNCH(SK_LEAF_BF, 4);
-        } else if (P.max_size <= 8) {
-            if (rf) RS_LANE_LAUNCH(SK_LEAF_RF, 8); else RS_LANE_LAUNCH(SK_LEAF_BF, 8);
-        } else {
-            if (rf) RS_LANE_LAUNCH(SK_LEAF_RF, 12); else RS_LANE_LAUNCH(SK_LEAF_BF, 12);
-        }
-#undef RS_LANE_LAUNCH
-        g_launches++;
-        return false;
     }
     if (P.kind == SK_UPPER && P.max_size > kWarpKeyCap) {  // oversized upper nodes first
         const u32 grid_big = std::min<u32>(P.n_nodes_host, (u32)P.sm_count * 2);

@@ -43,6 +43,28 @@ def keys_device(n: int, seed: int):
         out = torch.cat([u, extra])
 
 
+def keys_device_counter(n: int, seed: int):
+    """n DISTINCT uniform-looking 64-bit keys on the current CUDA device for any n (torch.unique
+    is limited to 2^31 elements): key i = mix(seed * 2^40 + i) with mix a bijection of 64-bit
+    words (xor-shift 32 / multiply by the odd constant 0xD6E8FEB86659FD93, twice) -- distinct
+    inputs give distinct keys.  Not SplitMix64 nor MurmurHash3 (the method's own mixers, R1,
+    R16).  Returns an int64 CUDA tensor (bit patterns)."""
+    import torch
+
+    M = 0xD6E8FEB86659FD93 - (1 << 64)  # as int64 (two's-complement multiply wraps mod 2^64)
+    out = torch.empty(n, dtype=torch.int64, device="cuda")
+    step = 1 << 28
+    for a in range(0, n, step):
+        b = min(n, a + step)
+        x = torch.arange(a, b, dtype=torch.int64, device="cuda") + (seed << 40)
+        for _ in range(2):
+            x = x ^ ((x >> 32) & 0xFFFFFFFF)
+            x = x * M
+        x = x ^ ((x >> 32) & 0xFFFFFFFF)
+        out[a:b] = x
+    return out
+
+
 def strings(n: int, seed: int, min_len: int = 10, max_len: int = 50):
     """n distinct random byte strings, lengths uniform in [min_len, max_len], bytes in
     1..255 (the paper's competitor workload: "strings of uniform random length in [10, 50]

@@ -40,9 +40,8 @@ def _mhc_np(keys, g=0):
 
 @pytest.mark.parametrize("rf,mmax", [(True, 16), (False, 12), (True, 8), (False, 8), (True, 3)])
 def test_leaf_search_parity(rf, mmax):
-    """Leaf searches against the oracle's (rotation fitting P:245-263 / brute force P:125-128).
-    mmax <= 8: the phase runs the lane-per-leaf kernel (k_leaf_lane, incl. its cooperative
-    tail), else the warp-per-leaf engine."""
+    """Leaf searches against the oracle's (rotation fitting P:245-263 / brute force P:125-128),
+    phases of mixed leaf sizes up to mmax (small-leaf phases are the batch-mode case)."""
     rng = np.random.default_rng(11 + rf + mmax)
     sizes = []
     for m in range(1, mmax + 1):

@@ -80,7 +80,7 @@ def main():
         del pinned, pk, blob
     if not a.skip_2g:
         n = (1 << 31) + 12345
-        kt = synth.keys_device(n, 11)
+        kt = synth.keys_device_counter(n, 11)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         blob = rs.build_device(kt, 8, 100, virtual_shards=8)
