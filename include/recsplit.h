@@ -21,9 +21,10 @@
  * Conventions
  *  - All functions return RECSPLIT_OK (0) or a negative error code; on error
  *    recsplit_last_error() returns a thread-local message describing the failure.
- *  - Output buffers (recsplit_bytes) are allocated by the library with malloc and
- *    owned by the caller, who releases them with recsplit_free().  On any error
- *    *out = {NULL, 0} and nothing leaks.
+ *  - Output buffers (recsplit_bytes) are allocated by the library (malloc, or pinned
+ *    host memory from a small reuse pool for single-GPU build results, so the result is
+ *    copied from the device only once) and owned by the caller, who releases them with
+ *    recsplit_free() -- never free().  On any error *out = {NULL, 0} and nothing leaks.
  *  - Input pointers are borrowed for the duration of the call and never retained.
  *  - The output bytes are a pure function of (key set, leaf_size, bucket_size,
  *    rotation_fitting, global_seed): independent of key order, device, shard

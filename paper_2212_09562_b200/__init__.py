@@ -164,10 +164,23 @@ def _take(b: Bytes) -> bytes:
     return out
 
 
+def _view(b: Bytes) -> np.ndarray:
+    """The library's result buffer as a read-only uint8 array (no copy); released with
+    recsplit_free when the array is garbage collected."""
+    import weakref
+
+    holder = Bytes(b.data, b.size)
+    arr = np.ctypeslib.as_array(b.data, shape=(b.size,)) if b.size else np.zeros(0, np.uint8)
+    arr.flags.writeable = False
+    weakref.finalize(arr, lib().recsplit_free, C.byref(holder))
+    return arr
+
+
 def build(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool = True, global_seed: int = 0,
-          device: int = -1, virtual_shards: int = 0, stats: bool = False, cuts=None):
+          device: int = -1, virtual_shards: int = 0, stats: bool = False, cuts=None, copy: bool = True):
     """Build from host keys (uint64 array).  Returns bytes (and a stats dict).  With
-    virtual_shards > 1, `cuts` (virtual_shards + 1 bucket indices) sets the shard ranges."""
+    virtual_shards > 1, `cuts` (virtual_shards + 1 bucket indices) sets the shard ranges.
+    copy=False: a read-only uint8 numpy view of the library's result buffer instead of bytes."""
     keys = np.ascontiguousarray(keys, dtype=np.uint64)
     b = Bytes()
     st = Stats()
@@ -175,14 +188,17 @@ def build(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
     o = _opts(rotation_fitting, global_seed, device, virtual_shards, cuts=cuts)
     _check(lib().recsplit_build_ex(_p64(keys), len(keys), leaf_size, bucket_size, C.byref(o), C.byref(b),
                                    C.byref(st)))
-    blob = _take(b)
+    blob = _take(b) if copy else _view(b)
     return (blob, st.as_dict()) if stats else blob
 
 
 def build_device(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting: bool = True,
-                 global_seed: int = 0, stream=None, stats: bool = False, virtual_shards: int = 0):
+                 global_seed: int = 0, stream=None, stats: bool = False, virtual_shards: int = 0,
+                 copy: bool = True):
     """Build from a CUDA tensor of keys (int64/uint64 bit patterns) resident in HBM
-    (virtual_shards > 1: the bucket-range sharded path on this one device)."""
+    (virtual_shards > 1: the bucket-range sharded path on this one device).  copy=False returns
+    the serialized MPHF as a read-only uint8 numpy array over the library's buffer (no host
+    copy) instead of bytes."""
     import torch
 
     if not keys_tensor.is_cuda or not keys_tensor.is_contiguous() or keys_tensor.element_size() != 8:
@@ -195,7 +211,7 @@ def build_device(keys_tensor, leaf_size: int, bucket_size: int, rotation_fitting
     _check(lib().recsplit_build_device(C.c_void_p(keys_tensor.data_ptr()), keys_tensor.numel(), leaf_size,
                                        bucket_size, C.byref(o), C.c_void_p(stream.cuda_stream), C.byref(b),
                                        C.byref(st)))
-    blob = _take(b)
+    blob = _take(b) if copy else _view(b)
     return (blob, st.as_dict()) if stats else blob
 
 

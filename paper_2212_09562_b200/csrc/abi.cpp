@@ -726,7 +726,7 @@ int recsplit_shard_globals(const uint64_t* summaries, int32_t world, int32_t ran
 
 void recsplit_free(recsplit_bytes* b) {
     if (!b) return;
-    free(b->data);
+    if (!rs::pinned_release(b->data)) free(b->data);
     b->data = nullptr;
     b->size = 0;
 }

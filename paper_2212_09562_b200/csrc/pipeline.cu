@@ -246,6 +246,57 @@ void shard_range(const BuildParams& p, uint64_t B, int rank, int world, uint64_t
 
 cudaMemPool_t device_pool(int dev) { return device_pool_impl(dev); }
 
+namespace {
+struct PinnedPool {
+    std::mutex mu;
+    std::map<void*, size_t> live;               // handed out: pointer -> capacity
+    std::multimap<size_t, void*> idle;          // returned, by capacity
+    size_t idle_bytes = 0;
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool;  // never destroyed (buffers may be freed at exit)
+    return *p;
+}
+constexpr size_t kPinnedIdleMax = 256u << 20;  // idle bytes kept for reuse
+}  // namespace
+
+uint8_t* pinned_get(size_t bytes) {
+    PinnedPool& P = pinned_pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    auto it = P.idle.lower_bound(bytes);
+    if (it != P.idle.end() && it->first <= 2 * bytes + (1u << 20)) {  // reuse a close fit
+        void* p = it->second;
+        P.live[p] = it->first;
+        P.idle_bytes -= it->first;
+        P.idle.erase(it);
+        return (uint8_t*)p;
+    }
+    const size_t cap = std::max<size_t>(bytes + bytes / 8, 1u << 16);
+    void* p = nullptr;
+    CK(cudaMallocHost(&p, cap));
+    P.live[p] = cap;
+    return (uint8_t*)p;
+}
+
+bool pinned_release(void* p) {
+    if (!p) return false;
+    PinnedPool& P = pinned_pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    auto it = P.live.find(p);
+    if (it == P.live.end()) return false;
+    const size_t cap = it->second;
+    P.live.erase(it);
+    P.idle.emplace(cap, p);
+    P.idle_bytes += cap;
+    while (P.idle_bytes > kPinnedIdleMax && !P.idle.empty()) {  // trim the largest idle buffers
+        auto last = std::prev(P.idle.end());
+        P.idle_bytes -= last->first;
+        cudaFreeHost(last->second);
+        P.idle.erase(last);
+    }
+    return true;
+}
+
 Globals compute_globals(const uint64_t* all, int world, int rank) {
     Globals G{};
     uint64_t mn = UINT64_MAX;
@@ -1135,8 +1186,14 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     CK(cudaMemcpyAsync(rep + 32 + sizeof(SingleDev), evals, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(rep + 64 + sizeof(SingleDev), pcnt_d, NP * 4, cudaMemcpyDeviceToHost, st));
     if (exec_d) CK(cudaMemcpyAsync(rep + 2048, exec_d, 32, cudaMemcpyDeviceToHost, st));
-    std::lock_guard<std::mutex> lk_stage(g_stage.mu);
-    uint8_t* buf = g_stage.get(cap_words * 8);
+    // the serialized MPHF goes straight into the caller's (pinned) result buffer
+    uint8_t* buf = pinned_get(est_words * 8);
+    struct BufGuard {
+        uint8_t*& b;
+        ~BufGuard() {
+            if (b) pinned_release(b);
+        }
+    } bg{buf};
     CK(cudaMemcpyAsync(buf, outw, est_words * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     uint32_t fl[8];
@@ -1150,7 +1207,11 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     if (fl[2] || fl[3] > 1) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
     if (fl[4]) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
     if (fl[5] || fl[0] > S || sdh.overflow) return false;  // rebuild on the synchronized path
-    if (sdh.total_words > est_words) {
+    if (sdh.total_words > est_words) {  // the estimate was short: a larger buffer, copy the rest
+        uint8_t* big = pinned_get(sdh.total_words * 8);
+        memcpy(big, buf, est_words * 8);
+        pinned_release(buf);
+        buf = big;
         CK(cudaMemcpyAsync(buf + est_words * 8, outw + est_words, (sdh.total_words - est_words) * 8,
                            cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -1159,11 +1220,9 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         std::lock_guard<std::mutex> g(g_est_mu);
         g_est_words[key] = sdh.total_words;
     }
-    const size_t size = sdh.total_words * 8;
-    out.raw = (uint8_t*)malloc(size);
-    if (!out.raw) throw Error(RECSPLIT_E_NOMEM, "host allocation failed");
-    memcpy(out.raw, buf, size);
-    out.raw_size = size;
+    out.raw = buf;
+    out.raw_size = sdh.total_words * 8;
+    buf = nullptr;  // owned by out now
     // statistics
     Sst.t_partition = tm.secs(e0, e1);
     Sst.t_tree = tm.secs(e1, e2);

@@ -42,6 +42,12 @@ struct BuildParams {
 // the library's stream-ordered memory pool on device dev (kept reserved between builds)
 cudaMemPool_t device_pool(int dev);
 
+// Pinned host result buffers (single-GPU builds D2H straight into the caller's result):
+// pinned_get returns a buffer of >= bytes (reused when possible), pinned_release takes back
+// one of them and returns false for any other pointer.
+uint8_t* pinned_get(size_t bytes);
+bool pinned_release(void* p);
+
 // the bucket range [b0, b1) of `rank` (cuts, else equal counts); validates the cuts
 void shard_range(const BuildParams& p, uint64_t B, int rank, int world, uint64_t& b0, uint64_t& b1);
 
@@ -54,7 +60,9 @@ struct BuildOutput {
     BuildOutput() = default;
     BuildOutput(const BuildOutput&) = delete;
     BuildOutput& operator=(const BuildOutput&) = delete;
-    ~BuildOutput() { free(raw); }
+    ~BuildOutput() {
+        if (!pinned_release(raw)) free(raw);
+    }
     const uint8_t* data() const { return raw ? raw : bytes.data(); }
     size_t size() const { return raw ? raw_size : bytes.size(); }
     std::vector<uint64_t> values;  // only when requested

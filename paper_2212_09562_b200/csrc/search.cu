@@ -67,6 +67,7 @@ struct Args {
     u32 upper_kp;  // upper splits in batch mode: keys-parallel sequential seeds (upper_keys_parallel)
     u32 qwords;    // early-rejection queue words per warp (0 for the plain variants)
     unsigned long long* exec;  // RS_COUNT_EVALS builds: executed evaluations of this phase's class
+    u32 lane_fit;  // leaves up to this size check rotations lane by lane (fit_rotation_lane)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -354,6 +355,29 @@ __device__ __forceinline__ bool fit_rotation_warp(u32 a, u32 b, u32 m, u32 full,
     return false;
 }
 
+// The same test lane by lane: every lane whose masks pass the popcount pruning tries its m
+// rotations in order; the caller's ballot takes the lowest lane with a fit (its smallest r is
+// the first one found), the minimal value as in fit_rotation_warp.  For small leaves (m <= 10:
+// ~17 % of the lanes pass at m = 8) m predicated steps per lane are cheaper than the warp's
+// serial loop over the passing lanes with two shuffles and a ballot each.
+__device__ __forceinline__ bool fit_rotation_lane(u32 a, u32 b, u32 m, u32 full, int& r) {
+    r = -1;
+    if (__popc(a) + __popc(b) == (int)m) {
+        const u32 na = ~a & full;
+        const u64 bb = (u64)b | ((u64)b << m);  // rot_m^r(b) = (bb >> (m - r)) & full
+        for (u32 q = 0; q < m; ++q)
+            if (((u32)(bb >> (m - q)) & full) == na) {
+                r = (int)q;
+                break;
+            }
+    }
+    return r >= 0;
+}
+
+__device__ __forceinline__ bool fit_rotation(u32 a, u32 b, u32 m, u32 full, u32 lane, int& r, u32 lane_fit_max) {
+    return m <= lane_fit_max ? fit_rotation_lane(a, b, m, full, r) : fit_rotation_warp(a, b, m, full, lane, r);
+}
+
 // Per-node search state (registers).
 struct NodeCtx {
     u32 s, slot;
@@ -363,6 +387,7 @@ struct NodeCtx {
     u32 cp;  // early rejection (full lower nodes): checkpoint in key groups, 0 = off
     u32 cp2; // second checkpoint (key groups), 0 = single stage
     u64 kW;  // key rebase: the buffered keys are lo + kW (values are tried relative to kW)
+    u32 lane_fit;  // leaves: lane-by-lane rotation check up to this m (fit_rotation)
 };
 
 
@@ -374,7 +399,7 @@ __device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, 
         u32 a, b;
         leaf_masks<MODE>(K, (c.s + 3) >> 2, c.s, base, a, b);
         if (KIND == SK_LEAF_BF) return a == c.full;
-        return fit_rotation_warp(a, b, c.s, c.full, lane, r);
+        return fit_rotation(a, b, c.s, c.full, lane, r, c.lane_fit);
     } else if (KIND == SK_UPPER) {
         return count_left<MODE>(K, c.s, sig, c.mask) == c.target;
     } else {
@@ -405,7 +430,7 @@ __device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, 
             b |= bit & key_word<GW>(K, j, 4);
         }
         if (KIND == SK_LEAF_BF) return a == c.full;
-        return fit_rotation_warp(a, b, s, c.full, lane, r);
+        return fit_rotation(a, b, s, c.full, lane, r, c.lane_fit);
     } else if (KIND == SK_UPPER) {
         u32 cnt = 0;
         for (u32 j = 0; j < s; ++j) cnt += hash_slow<GW>(K, j, idx) < c.mask;
@@ -429,10 +454,18 @@ __device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, 
 }
 
 // Load node n's keys into the warp's buffer and derive its constants.
+// Leaf data fetched ahead (batch mode): the node record and this lane's key / A-B byte.
+struct LeafPrefetch {
+    NodeRec rec;
+    u64 k;
+    u8 ab;
+};
+
 template <int KIND, bool WIDE = false>
-__device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G, u8* T8, NodeCtx& c) {
+__device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G, u8* T8, NodeCtx& c,
+                                          const LeafPrefetch* pf = nullptr) {
     constexpr u32 GW = Layout<KIND>::GW;
-    const NodeRec rec = A.nodes[n];
+    const NodeRec rec = pf ? pf->rec : A.nodes[n];
     c.s = rec.size;
     c.slot = rec.slot;
     const u32 s = c.s;
@@ -444,8 +477,8 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
         // natural key order; A/B select masks (global 1-bit hash); padding keys to
         // the next multiple of four get zero masks
         const bool valid = lane < s;
-        const u64 k = valid ? A.lo[rec.key_off + lane] : 0;
-        const bool isb = KIND == SK_LEAF_RF && valid && A.ab[rec.key_off + lane];
+        const u64 k = valid ? (pf ? pf->k : A.lo[rec.key_off + lane]) : 0;
+        const bool isb = KIND == SK_LEAF_RF && valid && (pf ? pf->ab : A.ab[rec.key_off + lane]);
         if (lane < ((s + 3) & ~3u)) {
             const u32 gp = GW * (lane >> 2), q = lane & 3;
             const u32 kh = (u32)(k >> 32);
@@ -465,6 +498,7 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
         // m = 20..24; a single stage is better below m = 14)
         c.cp2 = c.cp && A.cp_leaf2 && s >= 14 ? c.cp + 1 : 0u;
         c.kW = 0;
+        c.lane_fit = A.lane_fit;
     } else {
         for (u32 j = lane; j < s; j += 32) {
             const u64 k = A.lo[rec.key_off + j];
@@ -724,7 +758,7 @@ __device__ __forceinline__ bool run_window_leaf_cp(const Args& A, const KeysView
         leaf_masks<0>(K, ng, c.s, base_of(sig), a, b, gf, a, b);
         if (!have) a = b = 0;  // no entry: cannot fit (m >= 10 keys)
         int r = 0;
-        const bool ok = KIND == SK_LEAF_BF ? a == c.full : fit_rotation_warp(a, b, c.s, c.full, lane, r);
+        const bool ok = KIND == SK_LEAF_BF ? a == c.full : fit_rotation(a, b, c.s, c.full, lane, r, c.lane_fit);
         const u32 bal = __ballot_sync(FULL, ok);
         if (bal) {
             const int win = __ffs(bal) - 1;
@@ -1126,9 +1160,26 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
             n0 = __shfl_sync(FULL, n0, 0);
             if (n0 >= hbase) break;
             const u32 n1 = min(n0 + A.batch, hbase);
+            // leaves: the next node's record and keys are loaded while this node is searched
+            // (two-stage: keys of n + 1 from its record fetched one node earlier, record of n + 2)
+            constexpr bool kLeafPf = KIND == SK_LEAF_RF || KIND == SK_LEAF_BF;
+            LeafPrefetch pf{}, pf_next{};
+            NodeRec rec2{};
+            if (kLeafPf) {
+                pf.rec = A.nodes[n0];
+                if (n0 + 1 < n1) rec2 = A.nodes[n0 + 1];
+                pf.k = lane < pf.rec.size ? A.lo[pf.rec.key_off + lane] : 0;
+                pf.ab = KIND == SK_LEAF_RF && lane < pf.rec.size ? A.ab[pf.rec.key_off + lane] : 0;
+            }
             for (u32 n = n0; n < n1; ++n) {
                 if (KIND == SK_UPPER && A.nodes[n].size > kWarpKeyCap) continue;  // k_search_upper_big
-                load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c);
+                load_node<KIND, VAR == V_WIDE>(A, n, lane, G, T8, c, kLeafPf ? &pf : nullptr);
+                if (kLeafPf && n + 1 < n1) {
+                    pf_next.rec = rec2;
+                    pf_next.k = lane < rec2.size ? A.lo[rec2.key_off + lane] : 0;
+                    pf_next.ab = KIND == SK_LEAF_RF && lane < rec2.size ? A.ab[rec2.key_off + lane] : 0;
+                    if (n + 2 < n1) rec2 = A.nodes[n + 2];
+                }
                 u64 val = 0;
                 if (KIND == SK_UPPER && A.upper_kp && c.s <= kUpperKpMax) {
                     val = upper_keys_parallel(A, G, c, lane);
@@ -1145,6 +1196,7 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
                 if ((KIND == SK_UPPER || KIND == SK_LOWER) && A.lo_w)
                     fused_reorder<KIND>(A, G, A.nodes[n].key_off, c, val, lane);
                 __syncwarp();
+                if (kLeafPf) pf = pf_next;
             }
         }
         if (A.tail == 0) {
@@ -1274,6 +1326,8 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.u2 = P.u2;
     A.iters = P.iters ? P.iters : 1;
     A.exec = P.exec;
+    static const int lane_fit = getenv("RS_LANE_FIT") ? atoi(getenv("RS_LANE_FIT")) : 10;
+    A.lane_fit = (u32)std::max(0, lane_fit);
     A.help = P.help;
     // early-rejection checkpoints (per mille of the node size; RS_CP1 / RS_CP2 override, 0 = off)
     {

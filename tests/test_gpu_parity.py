@@ -263,10 +263,21 @@ def test_one_enqueue_fallback_on_oversized_bucket():
 
 
 def test_device_entry_matches_host_entry():
+    """Device-pointer and host-pointer entries give the same bytes; the no-copy result views
+    (pinned result buffers released with recsplit_free when collected) hold the same bytes."""
+    import gc
+
     import torch
     keys = synth.keys(50000, 21)
     kt = torch.from_numpy(keys.view(np.int64)).cuda()
-    assert rs.build_device(kt, 12, 500) == rs.build(keys, 12, 500)
+    ref = rs.build(keys, 12, 500)
+    assert rs.build_device(kt, 12, 500) == ref
+    for _ in range(3):  # buffers are recycled through the pinned pool
+        v = rs.build_device(kt, 12, 500, copy=False)
+        w = rs.build(keys, 12, 500, copy=False)
+        assert v.tobytes() == ref and w.tobytes() == ref and not v.flags.writeable
+        del v, w
+        gc.collect()
 
 
 @pytest.mark.slow
