@@ -324,8 +324,13 @@ def main():
         blob1, st1 = rs.build_device(kt, cfg["leaf"], cfg["bucket"], stream=stream, stats=True)
         stats = [st1]
     cls = 2
-    evals = float(np.mean([s["algo_evals"][cls] for s in stats]))
-    kt_s = float(np.mean([s["t_search"][cls] for s in stats]))
+    tree = float(np.mean([s.get("t_search_tree", 0.0) for s in stats])) > 0
+    if tree:  # small configurations: one whole-bucket kernel searches every node class
+        evals = float(np.mean([sum(s["algo_evals"]) for s in stats]))
+        kt_s = float(np.mean([s["t_search_tree"] for s in stats]))
+    else:
+        evals = float(np.mean([s["algo_evals"][cls] for s in stats]))
+        kt_s = float(np.mean([s["t_search"][cls] for s in stats]))
     peaks = _peaks()
     if "sm_max_mhz" in peaks:
         max_mhz, mhz_src = float(peaks["sm_max_mhz"]), "MEASURED_PEAKS sm_max_mhz"
@@ -337,7 +342,7 @@ def main():
     mix = mix_bound()
     achieved = evals / kt_s / 1e9
     ex = executed_evals(cfg, world) if not args.no_exec_count else None
-    exec_l1 = float(ex[cls]) if ex and ex[cls] else None
+    exec_l1 = (float(sum(ex)) if tree else float(ex[cls])) if ex and (sum(ex) if tree else ex[cls]) else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_l1_split_traffic.json")
     if os.path.exists(prof) and args.config == "C3":  # the ncu capture is of the C3 launch
@@ -363,7 +368,8 @@ def main():
         "e2e": {"value": e2e_value, "unit": "keys/s", "h2d_bytes_per_step": int(n_total * 8),  # whole job
                 "d2h_bytes_per_step": len(blob)},
         "gpu_launches": int(sum(s["kernel_launches"] for s in stats)) * (args.steps if world > 1 else 1),
-        "roofline": {"bound": "alu", "kernel": "k_search<SK_LOWER> (lower level 1 splits)",
+        "roofline": {"bound": "alu", "kernel": ("k_bucket_tree (whole buckets per warp, every node class)" if tree
+                                                else "k_search<SK_LOWER> (lower level 1 splits)"),
                      "achieved": achieved, "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
                      "traffic": traffic,
                      "executed_frac": (exec_l1 / kt_s / 1e9 / peak) if exec_l1 else None,
@@ -373,7 +379,8 @@ def main():
                                    f"under the per-opcode rates measured by tools/probe/pipes.cu "
                                    f"(profiles/l1_mix_bound_r02.json; FMA-pipe bound)") if mix[0] else
                                   f"{sms} SMs x {max_mhz:.0f} MHz ({mhz_src}) x 6.10 evals/clk/SM (derived issue bound)"},
-        "phases_s": {"partition": st0["t_partition"], "tree": st0["t_tree"], "upper": st0["t_search"][0],
+        "phases_s": {"partition": st0["t_partition"], "tree": st0["t_tree"],
+                     "search_bucket_tree": st0.get("t_search_tree", 0.0), "upper": st0["t_search"][0],
                      "lower2": st0["t_search"][1], "lower1": st0["t_search"][2], "leaves": st0["t_search"][3],
                      "reorder": st0["t_reorder"], "encode": st0["t_encode"], "d2h": st0["t_d2h"]},
         "algo_evals_per_step": [int(x) for x in st0["algo_evals"]],

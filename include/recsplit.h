@@ -106,6 +106,9 @@ typedef struct {
     uint64_t exec_evals[4];   /* diagnostic builds (-DRS_COUNT_EVALS) only, else 0: key evaluations
                                  the search kernels EXECUTED per class (32 lanes per group step,
                                  incl. discarded lanes; early rejection skips the rest) */
+    double t_search_tree;     /* small configurations: the whole-bucket search kernel (all classes
+                                 in one launch; t_search is then 0 and exec_evals[0] holds the
+                                 executed total), else 0 */
 } recsplit_stats;
 
 /* Library version (format version is the header's u16 version = 1). */

@@ -53,7 +53,8 @@ class Stats(C.Structure):
                 ("t_tree", C.c_double), ("t_search", C.c_double * 4), ("t_reorder", C.c_double),
                 ("t_encode", C.c_double), ("t_d2h", C.c_double), ("algo_evals", C.c_uint64 * 4),
                 ("nodes", C.c_uint64 * 4), ("data_bits", C.c_uint64), ("index_bits", C.c_uint64),
-                ("kernel_launches", C.c_uint32), ("max_bucket", C.c_uint32), ("exec_evals", C.c_uint64 * 4)]
+                ("kernel_launches", C.c_uint32), ("max_bucket", C.c_uint32), ("exec_evals", C.c_uint64 * 4),
+                ("t_search_tree", C.c_double)]
 
     def as_dict(self) -> dict:
         return {
@@ -62,7 +63,7 @@ class Stats(C.Structure):
             "t_encode": self.t_encode, "t_d2h": self.t_d2h, "algo_evals": list(self.algo_evals),
             "nodes": list(self.nodes), "data_bits": self.data_bits, "index_bits": self.index_bits,
             "kernel_launches": self.kernel_launches, "max_bucket": self.max_bucket,
-            "exec_evals": list(self.exec_evals),
+            "exec_evals": list(self.exec_evals), "t_search_tree": self.t_search_tree,
         }
 
 

@@ -143,8 +143,13 @@ int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, c
         } kg{d_keys, st};
         // pinned host keys of an unsharded build are streamed in chunks overlapped with the
         // hash kernel; pageable ones are copied in one piece first
+        // (memory pinned by another CUDA runtime in the process -- e.g. PyTorch's -- is page-locked
+        // at the driver level; cudaHostGetFlags answers for it where the pointer attributes of
+        // this statically linked runtime may not)
         cudaPointerAttributes pa{};
-        const bool pinned = cudaPointerGetAttributes(&pa, keys) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        unsigned host_flags = 0;
+        const bool pinned = (cudaPointerGetAttributes(&pa, keys) == cudaSuccess && pa.type == cudaMemoryTypeHost) ||
+                            cudaHostGetFlags(&host_flags, const_cast<uint64_t*>(keys)) == cudaSuccess;
         cudaGetLastError();
         const bool stream_keys = pinned && p.shards <= 1;
         cudaStream_t cs = nullptr;
@@ -176,7 +181,7 @@ int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, c
         cudaEventElapsedTime(&ms, a, z);
         cudaEventDestroy(a);
         cudaEventDestroy(z);
-        o.stats.t_h2d = ms * 1e-3;
+        if (!stream_keys) o.stats.t_h2d = ms * 1e-3;  // streamed: the copy stream's span, set by the build
         o.stats.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (stats) *stats = o.stats;
         return emit(o, out);

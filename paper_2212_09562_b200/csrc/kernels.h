@@ -79,6 +79,31 @@ struct PhaseLaunch {
 bool launch_search(const PhaseLaunch& P, cudaStream_t st);
 u32 search_active_slots(int sm_count);
 
+// Whole buckets per warp for small configurations (k_bucket_tree): every node of a bucket
+// searched in preorder on the bucket's keys in shared memory.  Eligible when the leaf size is
+// at most 9 and the table bound S at most kBucketTreeMax (and all classes are batch mode).
+constexpr u32 kBucketTreeMax = 512;
+struct TreeLaunch {
+    const u64* lo;
+    const u8* ab;
+    const u64* C;
+    u64 B;
+    const u64* nodebase;
+    const u32* tstart;
+    const rsd::TNodeD* tn;
+    u32 S;
+    u32* bcursor;  // zeroed
+    u64* values;
+    u32* err;
+    const u32* dup;
+    u32 leaf, u1, u2;
+    bool rf;
+    int sm_count;
+    unsigned long long* exec = nullptr;
+};
+bool bucket_tree_eligible(u32 leaf, u32 S);
+void launch_bucket_tree(const TreeLaunch& L, cudaStream_t st);
+
 // key redistribution after a split phase (A7), in place for the phase's nodes
 // (big_scratch: kReorderBigWarps * 2 * max_size u64 when max_size > 8192, else unused)
 constexpr u32 kReorderBigWarps = 64;

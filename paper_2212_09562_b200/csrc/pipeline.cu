@@ -969,6 +969,17 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     Arena A(st);
     Timer tm(st);
     const int e0 = tm.mark();
+    cudaEvent_t h2d_ev[2];  // streamed host keys: the copy stream's span (stats.t_h2d)
+    bool h2d_timed = false;
+    CK(cudaEventCreate(&h2d_ev[0]));
+    CK(cudaEventCreate(&h2d_ev[1]));
+    struct EvGuard {
+        cudaEvent_t* e;
+        ~EvGuard() {
+            cudaEventDestroy(e[0]);
+            cudaEventDestroy(e[1]);
+        }
+    } evg{h2d_ev};
 
     // ---- A1/A2 ----------------------------------------------------------------
     u64* lo_t = A.alloc<u64>(n);
@@ -987,6 +998,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     if (p.h_keys && !p.strings) {  // A1 overlapped with the chunked host->device copy
         const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
         std::vector<cudaEvent_t> evs;
+        CK(cudaEventRecord(h2d_ev[0], p.copy_stream));
         for (uint64_t off = 0; off < n; off += chunk) {
             const uint64_t len = std::min(chunk, n - off);
             cudaEvent_t ev;
@@ -999,6 +1011,8 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
             launch_hash(d_keys + off, nullptr, len, p.g, B, 0, B, lo_t + off, ab_t + off, bkt + off, hist, st);
             CKL();
         }
+        CK(cudaEventRecord(h2d_ev[1], p.copy_stream));
+        h2d_timed = true;
         for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
     } else {
         launch_hash(p.strings ? nullptr : d_keys, p.strings ? d_keys : nullptr, n, p.g, B, 0, B, lo_t, ab_t, bkt, hist, st);
@@ -1036,6 +1050,21 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     CKL();
     // exact upper bounds of the phase lists and of the node count, and the counts expected
     // for a typical bucket (launch sizing only)
+    // small configurations: whole buckets per warp (k_bucket_tree), no node table
+    static const int tree_env = getenv("RS_BUCKET_TREE") ? atoi(getenv("RS_BUCKET_TREE")) : 1;
+    bool tree = tree_env && bucket_tree_eligible(leaf, S);
+    if (tree) {
+        uint32_t it;
+        int help;
+        phase_policy(T, SK_UPPER, std::min<uint32_t>(S, 2 * sh.u2), it, help);
+        tree = tree && (S <= sh.u2 || !help);
+        phase_policy(T, SK_LOWER, sh.u2, it, help);
+        tree = tree && !help;
+        phase_policy(T, SK_LOWER, sh.u1, it, help);
+        tree = tree && !help;
+        phase_policy(T, p.rf ? SK_LEAF_RF : SK_LEAF_BF, leaf, it, help);
+        tree = tree && !help;
+    }
     std::vector<uint64_t> bound(NP, 0), poff(NP, 0), est(NP, 0);
     uint64_t nbound = 0;
     const uint32_t typ = (uint32_t)std::max<double>(1.0, std::min<double>(S, std::round(avg)));
@@ -1051,7 +1080,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         acc += bound[q];
         est[q] = std::max<uint64_t>(bound[q] ? 1 : 0, B * (uint64_t)T.tmpl(typ).phase_cnt[q]);
     }
-    rsd::NodeRec* nodes = A.alloc<rsd::NodeRec>(acc);
+    rsd::NodeRec* nodes = tree ? nullptr : A.alloc<rsd::NodeRec>(acc);
     u64* values_d = A.alloc<u64>(nbound);
     u32* next_win = A.alloc<u32>(nbound);
     u32* pcnt_d = A.alloc<u32>(NP + 32);
@@ -1068,8 +1097,10 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     CK(cudaMemsetAsync(cursors, 0, (2 * NP + 2) * 4, st));
     launch_phase_counts(Ms, B, NP, pcnt_d, st);
     CKL();
-    launch_expand(C, B, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st, S);
-    CKL();
+    if (!tree) {
+        launch_expand(C, B, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st, S);
+        CKL();
+    }
     const int e2 = tm.mark();
 
     // ---- A4-A9 -----------------------------------------------------------------
@@ -1078,7 +1109,33 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         int a, b, c;
     };
     std::vector<PhaseEv> pev;
-    for (uint32_t q = 0; q < NP; ++q) {
+    int et0 = -1, et1 = -1;
+    if (tree) {
+        TreeLaunch L{};
+        L.lo = lo_a;
+        L.ab = ab_a;
+        L.C = C;
+        L.B = B;
+        L.nodebase = Ms;
+        L.tstart = DT.tstart;
+        L.tn = DT.tnodes;
+        L.S = S;
+        L.bcursor = cursors;  // zeroed above
+        L.values = values_d;
+        L.err = small + 4;
+        L.dup = small + 2;
+        L.leaf = leaf;
+        L.u1 = sh.u1;
+        L.u2 = sh.u2;
+        L.rf = p.rf;
+        L.sm_count = sms;
+        L.exec = exec_d;
+        et0 = tm.mark();
+        launch_bucket_tree(L, st);
+        CKL();
+        et1 = tm.mark();
+    }
+    for (uint32_t q = 0; q < NP && !tree; ++q) {
         if (bound[q] == 0) continue;
         SearchKind kind;
         uint32_t maxs, typical, cls;
@@ -1232,6 +1289,12 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     }
     (void)e3;
     Sst.t_encode = tm.secs(e3, e4);
+    if (tree) Sst.t_search_tree = tm.secs(et0, et1);
+    if (h2d_timed) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, h2d_ev[0], h2d_ev[1]));
+        Sst.t_h2d = ms * 1e-3;  // the chunked copy (overlapped with hashing, inside t_partition)
+    }
     for (uint32_t q = 0; q < NP; ++q) {
         const int cls = q < T.n_upper ? 0 : q == T.phase_L2() ? 1 : q == T.phase_L1() ? 2 : 3;
         Sst.nodes[cls] += pc[q];

@@ -70,6 +70,18 @@ struct Args {
     u32 lane_fit;  // leaves up to this size check rotations lane by lane (fit_rotation_lane)
 };
 
+// Bucket-tree kernel (k_bucket_tree): buckets, their per-size preorder templates, slots.
+struct TreeArgs {
+    const u64* C;         // bucket key offsets (B + 1)
+    u64 B;
+    const u64* nodebase;  // exclusive node prefix per bucket (slot base)
+    const u32* tstart;    // template start per size
+    const TNodeD* tn;     // template nodes
+    u32 S;                // largest bucket size the tables cover
+    u32* bcursor;         // zeroed bucket cursor
+    u32 bbatch;           // buckets per cursor atomic
+};
+
 // ------------------------------------------------------------------ trials --
 //
 // Warp-private shared memory holds the node's keys in groups of four:
@@ -461,11 +473,16 @@ struct LeafPrefetch {
     u8 ab;
 };
 
+// (rec_ov / lo_src / ab_src: the node record and key arrays when they are not the phase's --
+// the bucket-tree kernel passes its shared-memory copy of the bucket)
 template <int KIND, bool WIDE = false>
 __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G, u8* T8, NodeCtx& c,
-                                          const LeafPrefetch* pf = nullptr) {
+                                          const LeafPrefetch* pf = nullptr, const NodeRec* rec_ov = nullptr,
+                                          const u64* lo_src = nullptr, const u8* ab_src = nullptr) {
     constexpr u32 GW = Layout<KIND>::GW;
-    const NodeRec rec = pf ? pf->rec : A.nodes[n];
+    const u64* const src_lo = lo_src ? lo_src : A.lo;
+    const u8* const src_ab = ab_src ? ab_src : A.ab;
+    const NodeRec rec = rec_ov ? *rec_ov : pf ? pf->rec : A.nodes[n];
     c.s = rec.size;
     c.slot = rec.slot;
     const u32 s = c.s;
@@ -477,8 +494,8 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
         // natural key order; A/B select masks (global 1-bit hash); padding keys to
         // the next multiple of four get zero masks
         const bool valid = lane < s;
-        const u64 k = valid ? (pf ? pf->k : A.lo[rec.key_off + lane]) : 0;
-        const bool isb = KIND == SK_LEAF_RF && valid && (pf ? pf->ab : A.ab[rec.key_off + lane]);
+        const u64 k = valid ? (pf ? pf->k : src_lo[rec.key_off + lane]) : 0;
+        const bool isb = KIND == SK_LEAF_RF && valid && (pf ? pf->ab : src_ab[rec.key_off + lane]);
         if (lane < ((s + 3) & ~3u)) {
             const u32 gp = GW * (lane >> 2), q = lane & 3;
             const u32 kh = (u32)(k >> 32);
@@ -501,7 +518,7 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
         c.lane_fit = A.lane_fit;
     } else {
         for (u32 j = lane; j < s; j += 32) {
-            const u64 k = A.lo[rec.key_off + j];
+            const u64 k = src_lo[rec.key_off + j];
             const u32 gp = GW * (j >> 2), q = j & 3;
             const u32 kh = (u32)(k >> 32);
             G[gp + q] = (u32)k;
@@ -1079,25 +1096,9 @@ __device__ u32 find_help(const Args& A, u32 gw, u32 lane, u32 nn) {
     return NONE;
 }
 
-#ifndef RS_MIN_BLOCKS
-#define RS_MIN_BLOCKS 1
-#endif
-template <int KIND, int VAR = V_PLAIN>
-__global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 : RS_MIN_BLOCKS) k_search(const Args A) {
-    constexpr u32 GW = Layout<KIND>::GW;
-    extern __shared__ __align__(16) u32 smem32[];
-    const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const u32 gw = blockIdx.x * (blockDim.x >> 5) + wib;
-    const u32 cap = A.warp_cap;                    // keys (multiple of 4)
-    const u32 gwords = GW * (cap / 4 + 1);         // key groups
-    const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
-    u32* G = smem32 + (size_t)wib * (gwords + twords + A.qwords);
-    RS_COUNT_INIT();
-    u8* T8 = reinterpret_cast<u8*>(G + gwords);
-    u32* QS = G + gwords + twords;  // early-rejection queues, A.qwords per warp (64 entries each):
-    u32* QC = QS + 64;              // seeds + partial counters / masks, for up to two stages
-    const KeysView K{G, (u32)__cvta_generic_to_shared(T8), 0u, (u32)__cvta_generic_to_shared(&s_full_tab[0][0])};
-    if (KIND == SK_LOWER) {  // shift tables of full nodes: part p -> p*w (p < f-1), 32 for the last
+// Block-wide shift tables and early-rejection constants of the two full lower-level classes
+// (s_full_tab, s_cp_masks); every block of a kernel that searches lower-level nodes runs it.
+__device__ __forceinline__ void init_lower_tables(const Args& A) {
         for (u32 t = threadIdx.x; t < 64; t += blockDim.x) {
             const u32 cl = t >> 5, p = t & 31;
             const u32 unit = cl ? A.u1 : A.leaf, f = cl ? A.u2 / A.u1 : A.u1 / A.leaf;
@@ -1143,6 +1144,26 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
         }
         __syncthreads();
     }
+
+#ifndef RS_MIN_BLOCKS
+#define RS_MIN_BLOCKS 1
+#endif
+template <int KIND, int VAR = V_PLAIN>
+__global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 : RS_MIN_BLOCKS) k_search(const Args A) {
+    constexpr u32 GW = Layout<KIND>::GW;
+    extern __shared__ __align__(16) u32 smem32[];
+    const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const u32 gw = blockIdx.x * (blockDim.x >> 5) + wib;
+    const u32 cap = A.warp_cap;                    // keys (multiple of 4)
+    const u32 gwords = GW * (cap / 4 + 1);         // key groups
+    const u32 twords = (cap + 32 + 15) / 16 * 4;   // byte table of >= cap + 32 entries
+    u32* G = smem32 + (size_t)wib * (gwords + twords + A.qwords);
+    RS_COUNT_INIT();
+    u8* T8 = reinterpret_cast<u8*>(G + gwords);
+    u32* QS = G + gwords + twords;  // early-rejection queues, A.qwords per warp (64 entries each):
+    u32* QC = QS + 64;              // seeds + partial counters / masks, for up to two stages
+    const KeysView K{G, (u32)__cvta_generic_to_shared(T8), 0u, (u32)__cvta_generic_to_shared(&s_full_tab[0][0])};
+    if (KIND == SK_LOWER) init_lower_tables(A);  // shift tables of full nodes, rejection constants
     if (A.dup[0] || A.dup[1] > 1) return;  // duplicate keys: nothing can be found (host reports)
     const u32 nn = *A.n_nodes;
     const u64 ws = 32ull * A.iters;
@@ -1578,6 +1599,134 @@ void launch_reorder(const NodeRec* nodes, u32 n_nodes, const u64* values, u64* l
                                                           big_scratch);
         g_launches++;
     }
+}
+
+// -------------------------------------------------------------- bucket trees --
+//
+// Small configurations (every node class in batch mode, buckets of at most a few hundred keys,
+// e.g. l = 8, b = 100): one warp builds a whole bucket, the paper's per-bucket recursion (P:110-
+// 119) mapped onto a warp.  The bucket's keys are copied into the warp's shared memory
+// once; its nodes are searched in preorder (the template order, so a node's keys are in place
+// when it is reached): each split is searched with the engine's windows (minimal seed, as in
+// batch mode) and its keys are partitioned in shared memory (reorder_node, smem -> smem), each
+// leaf is searched on its sub-range.  No node table, no global key traffic per node, no
+// redistribution passes and one tail for the whole build instead of one per phase.
+
+template <int KIND>
+__device__ __forceinline__ u64 tree_search_node(const Args& A, const NodeRec& rec, u32 lane, u32* G, u8* T8,
+                                                const u64* blo, const u8* bab, u32* QS, u32* QC) {
+    NodeCtx c{};
+    load_node<KIND, false>(A, 0, lane, G, T8, c, nullptr, &rec, blo, bab);
+    if (KIND == SK_UPPER && A.upper_kp && c.s <= kUpperKpMax) return upper_keys_parallel(A, G, c, lane);
+    const KeysView K{G, (u32)__cvta_generic_to_shared(T8), 0u, (u32)__cvta_generic_to_shared(&s_full_tab[0][0])};
+    const u64 ws = 32ull * A.iters;
+    for (u64 wstart = 0;; wstart += ws) {
+        if (wstart >= kSeedCap) {
+            if (lane == 0) atomicOr(A.err, 1u);
+            return KIND == SK_LEAF_RF ? wstart * c.s : wstart;
+        }
+        u64 val;
+        if (run_window<KIND, V_PLAIN>(A, K, c, wstart, lane, &val, QS, QC)) return val;
+    }
+}
+
+template <bool RF>
+__global__ void __launch_bounds__(128, 6) k_bucket_tree(const Args A, const TreeArgs T) {
+    extern __shared__ __align__(16) u32 smem32[];
+    const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const u32 cap = A.warp_cap;  // >= every bucket size searched, multiple of 16
+    const u32 gwords = 12 * (cap / 4 + 1) > 20 * (A.leaf / 4 + 2) ? 12 * (cap / 4 + 1) : 20 * (A.leaf / 4 + 2);
+    const u32 twords = (cap + 32 + 15) / 16 * 4;
+    const u32 per_warp = gwords + twords + 2 * cap + cap / 4 + 2 * cap + cap / 4;
+    u32* G = smem32 + (size_t)wib * per_warp;
+    u8* T8 = reinterpret_cast<u8*>(G + gwords);
+    u64* blo = reinterpret_cast<u64*>(G + gwords + twords);  // the bucket's keys (node order)
+    u8* bab = reinterpret_cast<u8*>(blo + cap);
+    u64* slo = reinterpret_cast<u64*>(bab + cap);            // reorder staging
+    u8* sab = reinterpret_cast<u8*>(slo + cap);
+    init_lower_tables(A);
+    RS_COUNT_INIT();
+    if (A.dup[0] || A.dup[1] > 1) return;
+    const u64 base0 = T.nodebase[0];
+    for (;;) {
+        u32 b0 = 0;
+        if (lane == 0) b0 = atomicAdd(T.bcursor, T.bbatch);
+        b0 = __shfl_sync(FULL, b0, 0);
+        if (b0 >= T.B) break;
+        const u32 b1 = (u32)min((u64)b0 + T.bbatch, T.B);
+        for (u32 b = b0; b < b1; ++b) {
+            const u64 c0 = T.C[b];
+            const u32 s = (u32)(T.C[b + 1] - c0);
+            if (s == 0 || s > T.S) continue;  // (above the tables: flagged, rebuilt by the caller)
+            __syncwarp();
+            for (u32 j = lane; j < s; j += 32) {
+                blo[j] = A.lo[c0 + j];
+                bab[j] = A.ab[c0 + j];
+            }
+            __syncwarp();
+            const u32 t0 = T.tstart[s], t1 = T.tstart[s + 1];
+            const u64 nb = T.nodebase[b] - base0;
+            for (u32 t = t0; t < t1; ++t) {
+                const TNodeD x = T.tn[t];
+                const NodeRec rec{x.rel_off, x.size, (u32)(nb + (t - t0)), 0};
+                u64 val;
+                if (x.size <= A.leaf) {
+                    val = tree_search_node<RF ? SK_LEAF_RF : SK_LEAF_BF>(A, rec, lane, G, T8, blo, bab, nullptr, nullptr);
+                } else {
+                    if (x.size <= A.u2)
+                        val = tree_search_node<SK_LOWER>(A, rec, lane, G, T8, blo, bab, nullptr, nullptr);
+                    else
+                        val = tree_search_node<SK_UPPER>(A, rec, lane, G, T8, blo, bab, nullptr, nullptr);
+                    // children's keys into their sub-ranges (in shared memory)
+                    reorder_node(rec, val, blo, bab, slo, sab, A.leaf, A.u1, A.u2, lane);
+                }
+                if (lane == 0) A.values[rec.slot] = val;
+            }
+        }
+    }
+    RS_COUNT_FLUSH(A.exec);
+}
+
+bool bucket_tree_eligible(u32 leaf, u32 S) { return leaf <= 9 && S <= kBucketTreeMax; }
+
+void launch_bucket_tree(const TreeLaunch& L, cudaStream_t st) {
+    Args A{};
+    A.lo = L.lo;
+    A.ab = L.ab;
+    A.values = L.values;
+    A.err = L.err;
+    A.dup = L.dup;
+    A.leaf = L.leaf;
+    A.u1 = L.u1;
+    A.u2 = L.u2;
+    A.iters = 1;
+    A.exec = L.exec;
+    static const int lane_fit = getenv("RS_LANE_FIT") ? atoi(getenv("RS_LANE_FIT")) : 10;
+    A.lane_fit = (u32)std::max(0, lane_fit);
+    static const int ukp = getenv("RS_UPPER_KP") ? atoi(getenv("RS_UPPER_KP")) : 1;
+    A.upper_kp = ukp ? 1u : 0u;
+    A.qwords = 0;
+    const u32 cap = (L.S + 15) & ~15u;
+    A.warp_cap = cap;
+    TreeArgs T{L.C, L.B, L.nodebase, L.tstart, L.tn, L.S, L.bcursor, 1};
+    const u32 gwords = std::max(12 * (cap / 4 + 1), 20 * (L.leaf / 4 + 2));
+    const size_t per_warp = (size_t)(gwords + (cap + 32 + 15) / 16 * 4 + 2 * cap + cap / 4 + 2 * cap + cap / 4) * 4;
+    const u32 wpb = 4;
+    const size_t smem = per_warp * wpb;
+    const void* fn = L.rf ? (const void*)k_bucket_tree<true> : (const void*)k_bucket_tree<false>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)(wpb * 32), smem);
+    if (occ < 1) occ = 1;
+    u32 grid = (u32)std::min<u64>((u64)occ * L.sm_count, (L.B + wpb - 1) / wpb);
+    // buckets per cursor atomic: a few per warp while many remain, so the last ones finish together
+    T.bbatch = (u32)std::max<u64>(1, std::min<u64>(4, L.B / ((u64)grid * wpb * 16)));
+    if (grid == 0) grid = 1;
+    if (L.rf)
+        k_bucket_tree<true><<<grid, wpb * 32, smem, st>>>(A, T);
+    else
+        k_bucket_tree<false><<<grid, wpb * 32, smem, st>>>(A, T);
+    g_launches++;
 }
 
 }  // namespace rs

@@ -89,7 +89,8 @@ def main():
                           "bijective": ok, "t_keys_host_s": t_keys,
                           "torch_h2d_8gb_s": t_h2d, "device_keys_build_s": t_dev,
                           "device_keys_partition_s": st_d["t_partition"],
-                          "phases_s": {k: st[k] for k in ("t_partition", "t_tree", "t_reorder", "t_encode", "t_d2h")},
+                          "phases_s": {k: st[k] for k in ("t_h2d", "t_partition", "t_tree", "t_reorder", "t_encode", "t_d2h",
+                                                          "t_search_tree")},
                           "t_search": st["t_search"]}), flush=True)
         del pinned, pk, blob
     if not a.skip_2g:
