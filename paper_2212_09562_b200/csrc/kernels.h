@@ -100,6 +100,7 @@ struct TreeLaunch {
     bool rf;
     int sm_count;
     unsigned long long* exec = nullptr;
+    bool dedupe = false;  // each warp checks its bucket for duplicate keys (no k_dedupe pass)
 };
 bool bucket_tree_eligible(u32 leaf, u32 S);
 void launch_bucket_tree(const TreeLaunch& L, cudaStream_t st);

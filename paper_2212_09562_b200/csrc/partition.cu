@@ -75,7 +75,7 @@ __global__ void k_bucket_stats(const u32* __restrict__ hist, u64 B, u32* maxmin,
         u32 s = hist[i];
         mx = s > mx ? s : mx;
         mn = s < mn ? s : mn;
-        atomicAdd(size_hist + (s <= cap ? s : cap), 1u);
+        if (size_hist) atomicAdd(size_hist + (s <= cap ? s : cap), 1u);
     }
     for (int d = 16; d; d >>= 1) {
         mx = max(mx, __shfl_xor_sync(FULL, mx, d));

@@ -981,6 +981,25 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         }
     } evg{h2d_ev};
 
+    // small configurations: whole buckets per warp (k_bucket_tree), no node table; decided
+    // before the partition because the tree kernel also does the duplicate check
+    const std::shared_ptr<const Tables> Tq = get_tables(leaf, p.rf, S);
+    // (off by default: measured 10-27 % slower than the phase kernels -- warps in different
+    // node kinds thrash the instruction cache, ncu "no_instructions" is the top stall)
+    static const int tree_env = getenv("RS_BUCKET_TREE") ? atoi(getenv("RS_BUCKET_TREE")) : 0;
+    bool tree = tree_env && bucket_tree_eligible(leaf, S);
+    if (tree) {
+        uint32_t it;
+        int help;
+        phase_policy(*Tq, SK_UPPER, std::min<uint32_t>(S, 2 * sh.u2), it, help);
+        tree = tree && (S <= sh.u2 || !help);
+        phase_policy(*Tq, SK_LOWER, sh.u2, it, help);
+        tree = tree && !help;
+        phase_policy(*Tq, SK_LOWER, sh.u1, it, help);
+        tree = tree && !help;
+        phase_policy(*Tq, p.rf ? SK_LEAF_RF : SK_LEAF_BF, leaf, it, help);
+        tree = tree && !help;
+    }
     // ---- A1/A2 ----------------------------------------------------------------
     u64* lo_t = A.alloc<u64>(n);
     u8* ab_t = A.alloc<u8>(n);
@@ -989,10 +1008,8 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     u64* C = A.alloc<u64>(B + 2);
     u64* cursor = A.alloc<u64>(B + 1);
     u32* small = A.alloc<u32>(8);  // [0] max, [1] min bucket size, [2] dup, [3] lo == 0, [4] seed cap, [5] size > S
-    u32* size_hist_d = A.alloc<u32>(S + 1);
     void* scan_tmp = A.alloc<u8>(scan_temp_bytes(B + 1) + 64);
     CK(cudaMemsetAsync(hist, 0, (B + 1) * 4, st));
-    CK(cudaMemsetAsync(size_hist_d, 0, (S + 1) * 4, st));
     const uint32_t small_init[8] = {0, 0xffffffffu, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(small, small_init, sizeof small_init, cudaMemcpyHostToDevice, st));
     if (p.h_keys && !p.strings) {  // A1 overlapped with the chunked host->device copy
@@ -1018,7 +1035,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         launch_hash(p.strings ? nullptr : d_keys, p.strings ? d_keys : nullptr, n, p.g, B, 0, B, lo_t, ab_t, bkt, hist, st);
         CKL();
     }
-    launch_bucket_stats(hist, B, small, size_hist_d, S, st);
+    launch_bucket_stats(hist, B, small, nullptr, S, st);  // max / min only (no size histogram needed)
     CKL();
     exscan_u32_to_u64(hist, C, B, scan_tmp, st);
     CKL();
@@ -1027,8 +1044,10 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     u8* ab_a = A.alloc<u8>(n);
     launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
     CKL();
-    launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
-    CKL();
+    if (!tree) {  // (tree: each warp checks its own bucket)
+        launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
+        CKL();
+    }
     A.release(lo_t);
     A.release(ab_t);
     A.release(bkt);
@@ -1050,21 +1069,6 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     CKL();
     // exact upper bounds of the phase lists and of the node count, and the counts expected
     // for a typical bucket (launch sizing only)
-    // small configurations: whole buckets per warp (k_bucket_tree), no node table
-    static const int tree_env = getenv("RS_BUCKET_TREE") ? atoi(getenv("RS_BUCKET_TREE")) : 1;
-    bool tree = tree_env && bucket_tree_eligible(leaf, S);
-    if (tree) {
-        uint32_t it;
-        int help;
-        phase_policy(T, SK_UPPER, std::min<uint32_t>(S, 2 * sh.u2), it, help);
-        tree = tree && (S <= sh.u2 || !help);
-        phase_policy(T, SK_LOWER, sh.u2, it, help);
-        tree = tree && !help;
-        phase_policy(T, SK_LOWER, sh.u1, it, help);
-        tree = tree && !help;
-        phase_policy(T, p.rf ? SK_LEAF_RF : SK_LEAF_BF, leaf, it, help);
-        tree = tree && !help;
-    }
     std::vector<uint64_t> bound(NP, 0), poff(NP, 0), est(NP, 0);
     uint64_t nbound = 0;
     const uint32_t typ = (uint32_t)std::max<double>(1.0, std::min<double>(S, std::round(avg)));
@@ -1092,8 +1096,10 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     exec_d = A.alloc<unsigned long long>(4);
     CK(cudaMemsetAsync(exec_d, 0, 32, st));
 #endif
-    CK(cudaMemsetAsync(values_d, 0xff, nbound * 8, st));
-    CK(cudaMemsetAsync(next_win, 0, nbound * 4, st));
+    if (!tree) {  // (the bucket-tree kernel writes every value once and uses no dispensers)
+        CK(cudaMemsetAsync(values_d, 0xff, nbound * 8, st));
+        CK(cudaMemsetAsync(next_win, 0, nbound * 4, st));
+    }
     CK(cudaMemsetAsync(cursors, 0, (2 * NP + 2) * 4, st));
     launch_phase_counts(Ms, B, NP, pcnt_d, st);
     CKL();
@@ -1130,6 +1136,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         L.rf = p.rf;
         L.sm_count = sms;
         L.exec = exec_d;
+        L.dedupe = true;
         et0 = tm.mark();
         launch_bucket_tree(L, st);
         CKL();

@@ -68,6 +68,7 @@ struct Args {
     u32 qwords;    // early-rejection queue words per warp (0 for the plain variants)
     unsigned long long* exec;  // RS_COUNT_EVALS builds: executed evaluations of this phase's class
     u32 lane_fit;  // leaves up to this size check rotations lane by lane (fit_rotation_lane)
+    u32 guided;    // batch mode: single-node batches near the end of the phase
 };
 
 // Bucket-tree kernel (k_bucket_tree): buckets, their per-size preorder templates, slots.
@@ -80,6 +81,7 @@ struct TreeArgs {
     u32 S;                // largest bucket size the tables cover
     u32* bcursor;         // zeroed bucket cursor
     u32 bbatch;           // buckets per cursor atomic
+    u32 dedupe;           // check each bucket for duplicate keys (instead of k_dedupe)
 };
 
 // ------------------------------------------------------------------ trials --
@@ -1175,12 +1177,18 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 :
         // last A.tail nodes; those then run in help mode so that no warp is left with a
         // straggler batch while the others idle
         hbase = nn > A.tail ? nn - A.tail : 0;
+        // guided batches: once fewer than two full rounds of batches remain, one node per
+        // cursor atomic, so that the last nodes spread over all warps instead of queueing
+        // behind one warp's batch (the phase ends with its slowest warp)
+        u32 bsz = A.batch;
+        const u32 guide = A.guided ? 2 * A.n_warps * A.batch : 0;
         for (;;) {
             u32 n0 = 0;
-            if (lane == 0) n0 = atomicAdd(A.cursor, A.batch);
+            if (lane == 0) n0 = atomicAdd(A.cursor, bsz);
             n0 = __shfl_sync(FULL, n0, 0);
             if (n0 >= hbase) break;
-            const u32 n1 = min(n0 + A.batch, hbase);
+            const u32 n1 = min(n0 + bsz, hbase);
+            if (hbase - n0 < guide) bsz = 1;
             // leaves: the next node's record and keys are loaded while this node is searched
             // (two-stage: keys of n + 1 from its record fetched one node earlier, record of n + 2)
             constexpr bool kLeafPf = KIND == SK_LEAF_RF || KIND == SK_LEAF_BF;
@@ -1349,6 +1357,8 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.exec = P.exec;
     static const int lane_fit = getenv("RS_LANE_FIT") ? atoi(getenv("RS_LANE_FIT")) : 10;
     A.lane_fit = (u32)std::max(0, lane_fit);
+    static const int guided = getenv("RS_GUIDED") ? atoi(getenv("RS_GUIDED")) : 1;
+    A.guided = guided ? 1u : 0u;
     A.help = P.help;
     // early-rejection checkpoints (per mille of the node size; RS_CP1 / RS_CP2 override, 0 = off)
     {
@@ -1630,12 +1640,22 @@ __device__ __forceinline__ u64 tree_search_node(const Args& A, const NodeRec& re
     }
 }
 
+// work-buffer words of a bucket-tree warp: split groups (12 words per 4 keys), leaf groups (20),
+// or the duplicate-check table (2 words per slot, 2 * cap slots)
+__host__ __device__ __forceinline__ u32 tree_gwords(u32 cap, u32 leaf) {
+    u32 g = 12 * (cap / 4 + 1);
+    if (20 * (leaf / 4 + 2) > g) g = 20 * (leaf / 4 + 2);
+    u32 ts = 64;
+    while (ts < 2 * cap) ts <<= 1;
+    return 2 * ts > g ? 2 * ts : g;
+}
+
 template <bool RF>
 __global__ void __launch_bounds__(128, 6) k_bucket_tree(const Args A, const TreeArgs T) {
     extern __shared__ __align__(16) u32 smem32[];
     const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const u32 cap = A.warp_cap;  // >= every bucket size searched, multiple of 16
-    const u32 gwords = 12 * (cap / 4 + 1) > 20 * (A.leaf / 4 + 2) ? 12 * (cap / 4 + 1) : 20 * (A.leaf / 4 + 2);
+    const u32 gwords = tree_gwords(cap, A.leaf);
     const u32 twords = (cap + 32 + 15) / 16 * 4;
     const u32 per_warp = gwords + twords + 2 * cap + cap / 4 + 2 * cap + cap / 4;
     u32* G = smem32 + (size_t)wib * per_warp;
@@ -1662,6 +1682,41 @@ __global__ void __launch_bounds__(128, 6) k_bucket_tree(const Args A, const Tree
             for (u32 j = lane; j < s; j += 32) {
                 blo[j] = A.lo[c0 + j];
                 bab[j] = A.ab[c0 + j];
+            }
+            if (T.dedupe) {
+                // exact duplicate check of the bucket (A2; equal keys <=> equal lo, R2): an
+                // open-addressing set over its lo values in the (still free) work buffer; a
+                // repeated key fails the build, and the bucket is not searched (its leaf search
+                // could never succeed)
+                u32 ts = 64;
+                while (ts < 2 * s) ts <<= 1;
+                unsigned long long* tab = reinterpret_cast<unsigned long long*>(G);
+                for (u32 j = lane; j < ts; j += 32) tab[j] = 0;
+                __syncwarp();
+                bool rep = false;
+                u32 zeros = 0;
+                for (u32 j = lane; j < s; j += 32) {
+                    const u64 v = blo[j];
+                    if (v == 0) {
+                        ++zeros;
+                        continue;
+                    }
+                    u32 slot = (u32)(v ^ (v >> 32)) & (ts - 1);
+                    for (;;) {
+                        const unsigned long long old = atomicCAS(tab + slot, 0ull, (unsigned long long)v);
+                        if (old == 0ull) break;
+                        if (old == v) {
+                            rep = true;
+                            break;
+                        }
+                        slot = (slot + 1) & (ts - 1);
+                    }
+                }
+                zeros = __reduce_add_sync(FULL, zeros);
+                if (__any_sync(FULL, rep) || zeros > 1) {
+                    if (lane == 0) atomicOr(const_cast<u32*>(A.dup), 1u);
+                    continue;
+                }
             }
             __syncwarp();
             const u32 t0 = T.tstart[s], t1 = T.tstart[s + 1];
@@ -1708,8 +1763,8 @@ void launch_bucket_tree(const TreeLaunch& L, cudaStream_t st) {
     A.qwords = 0;
     const u32 cap = (L.S + 15) & ~15u;
     A.warp_cap = cap;
-    TreeArgs T{L.C, L.B, L.nodebase, L.tstart, L.tn, L.S, L.bcursor, 1};
-    const u32 gwords = std::max(12 * (cap / 4 + 1), 20 * (L.leaf / 4 + 2));
+    TreeArgs T{L.C, L.B, L.nodebase, L.tstart, L.tn, L.S, L.bcursor, 1, L.dedupe ? 1u : 0u};
+    const u32 gwords = tree_gwords(cap, L.leaf);
     const size_t per_warp = (size_t)(gwords + (cap + 32 + 15) / 16 * 4 + 2 * cap + cap / 4 + 2 * cap + cap / 4) * 4;
     const u32 wpb = 4;
     const size_t smem = per_warp * wpb;

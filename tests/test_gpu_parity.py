@@ -262,6 +262,34 @@ def test_one_enqueue_fallback_on_oversized_bucket():
     assert got == oracle.build(keys, 8, b, threads=os.cpu_count())
 
 
+def test_bucket_tree_mode_bytes():
+    """The whole-bucket kernel (k_bucket_tree, RS_BUCKET_TREE=1; off by default) in a fresh
+    process: C1 and small configurations (incl. odd leaf sizes, one-key buckets, upper splits,
+    a duplicate) give the oracle's bytes / E_DUPLICATE."""
+    import subprocess
+    import sys
+    code = """
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2212_09562_b200 as rs, oracle, synth
+for leaf, b, n in [(8, 100, 10000), (5, 5, 20000), (7, 200, 30000), (2, 3, 5000), (9, 300, 40000), (8, 100, 1)]:
+    k = synth.keys(n, 40 + leaf)
+    blob, st = rs.build(k, leaf, b, stats=True)
+    assert st["t_search_tree"] > 0, (leaf, b)
+    assert blob == oracle.build(k, leaf, b, threads=4), (leaf, b, n)
+k = synth.keys(5000, 3); k[10] = k[4000]
+try:
+    rs.build(k, 8, 100)
+    raise SystemExit("duplicate not detected")
+except rs.RecSplitError as e:
+    assert e.code == rs.E_DUPLICATE
+print("ok")
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, RS_BUCKET_TREE="1"), capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
 def test_device_entry_matches_host_entry():
     """Device-pointer and host-pointer entries give the same bytes; the no-copy result views
     (pinned result buffers released with recsplit_free when collected) hold the same bytes."""
