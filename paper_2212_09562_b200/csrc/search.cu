@@ -1327,6 +1327,101 @@ __global__ void __launch_bounds__(1024) k_search_upper_big(const NodeRec* __rest
     }
 }
 
+// --------------------------------------------------------- sub-warp leaves --
+//
+// Leaves of at most 8 keys (l <= 8, e.g. C2: ~56 base seeds per leaf): a 32-seed window per leaf
+// overshoots its minimal base seed by ~16 of ~56 seeds and the per-leaf load / ballot work is
+// paid per 1.8 windows.  Here a warp is four 8-lane sub-warps, each owning one leaf: its lanes
+// try 8 consecutive base seeds k .. k+7 per step (lane i: k + i), the keys of the leaf in the
+// sub-warp's shared-memory groups; the lowest lane of the sub-warp with a fit, with its
+// smallest r, gives the minimal value of that step, and every smaller base seed failed in
+// earlier steps, so it is the minimal stored value.  A finished sub-warp takes the
+// next leaf (one cursor atomic per warp for all sub-warps that need one).
+constexpr u32 kSubLeafMax = 8;
+
+template <int KIND>
+__global__ void __launch_bounds__(128) k_leaf_sub(const Args A) {
+    __shared__ __align__(16) u32 sG[4][4][2 * 20];  // [warp][sub-warp][2 groups x 20 words]
+    const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sub = lane >> 3, sl = lane & 7;
+    RS_COUNT_INIT();
+    if (A.dup[0] || A.dup[1] > 1) return;
+    const u32 nn = *A.n_nodes;
+    u32* G = sG[wib][sub];
+    u32 m = 0, full = 0, slot = 0;
+    u64 k = 0;
+    bool busy = false, dry = false;
+    for (;;) {
+        // sub-warps without a leaf take the next ones
+        const u32 want = __ballot_sync(FULL, !busy && !dry && sl == 0);
+        if (want) {
+            const int leader = __ffs(want) - 1;
+            u32 first = 0;
+            if ((int)lane == leader) first = atomicAdd(A.cursor, (u32)__popc(want));
+            first = __shfl_sync(FULL, first, leader);
+            if (!busy && !dry) {
+                const u32 idx = first + __popc(want & ((1u << (sub * 8)) - 1u));  // rank among the wanting
+                if (idx < nn) {
+                    const NodeRec rec = A.nodes[idx];
+                    m = rec.size;
+                    slot = rec.slot;
+                    full = (1u << m) - 1u;
+                    k = 0;
+                    busy = true;
+                    const bool valid = sl < m;
+                    const u64 key = valid ? A.lo[rec.key_off + sl] : 0;
+                    const bool isb = KIND == SK_LEAF_RF && valid && A.ab[rec.key_off + sl];
+                    const u32 g = 20 * (sl >> 2), q = sl & 3, kh = (u32)(key >> 32);
+                    G[g + q] = (u32)key;
+                    G[g + 4 + q] = kh;
+                    G[g + 8 + q] = key_const(kh);
+                    G[g + 12 + q] = valid && !isb ? FULL : 0u;
+                    G[g + 16 + q] = isb ? FULL : 0u;
+                } else {
+                    dry = true;
+                }
+            }
+        }
+        __syncwarp();
+        if (!__any_sync(FULL, busy)) break;
+        // one step: lane sl tries base seed k + sl (64-bit keys + value, generic path)
+        const u64 base = KIND == SK_LEAF_RF ? (k + sl) * m : k + sl;
+        u32 a = 0, b = 0;
+        if (busy) {
+            RS_COUNT_RAW(m);
+#pragma unroll
+            for (u32 j = 0; j < kSubLeafMax; ++j) {
+                const u32* gp = G + 20 * (j >> 2) + (j & 3);
+                const u32 bit = 1u << __umulhi(remix_hi((((u64)gp[4] << 32) | gp[0]) + base), m);
+                a |= bit & gp[12];
+                b |= bit & gp[16];
+            }
+        }
+        int r = -1;
+        const bool ok = busy && (KIND == SK_LEAF_BF ? (a == full && (r = 0) == 0) : fit_rotation_lane(a, b, m, full, r));
+        const u32 bal = __ballot_sync(FULL, ok);
+        const u32 mine = (bal >> (sub * 8)) & 0xffu;
+        const int rw = __shfl_sync(FULL, r, (int)(sub * 8) + (mine ? __ffs(mine) - 1 : 0));
+        if (busy) {
+            if (mine) {
+                const u32 win = __ffs(mine) - 1;
+                if (sl == 0) A.values[slot] = KIND == SK_LEAF_RF ? (k + win) * m + (u32)rw : k + win;
+                busy = false;
+            } else {
+                k += kSubLeafMax;
+                if (k >= kSeedCap) {
+                    if (sl == 0) {
+                        atomicOr(A.err, 1u);
+                        A.values[slot] = KIND == SK_LEAF_RF ? k * m : k;
+                    }
+                    busy = false;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    RS_COUNT_FLUSH(A.exec);
+}
+
 template <int KIND, int VAR = V_PLAIN>
 void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 grid, cudaStream_t st) {
     cudaFuncSetAttribute(k_search<KIND, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -1387,6 +1482,17 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
         A.cp_leaf2 = cpl2 ? 1u : 0u;
         static const int cpw2 = getenv("RS_CPW2") ? atoi(getenv("RS_CPW2")) : 1;
         A.cp_wide2 = cpw2 ? 1u : 0u;
+    }
+    static const int subleaf = getenv("RS_SUB_LEAF") ? atoi(getenv("RS_SUB_LEAF")) : 1;
+    if (subleaf && (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) && P.max_size <= kSubLeafMax) {
+        // leaves of at most 8 keys: four per warp (k_leaf_sub); the phase's batch cursor is zeroed
+        const u32 blocks = std::max<u32>(1, std::min<u32>((P.n_nodes_host + 15) / 16, (u32)P.sm_count * 16));
+        if (P.kind == SK_LEAF_RF)
+            k_leaf_sub<SK_LEAF_RF><<<blocks, 128, 0, st>>>(A);
+        else
+            k_leaf_sub<SK_LEAF_BF><<<blocks, 128, 0, st>>>(A);
+        g_launches++;
+        return false;
     }
     if (P.kind == SK_UPPER && P.max_size > kWarpKeyCap) {  // oversized upper nodes first
         const u32 grid_big = std::min<u32>(P.n_nodes_host, (u32)P.sm_count * 2);
