@@ -174,8 +174,58 @@ __global__ void __launch_bounds__(256) k_dedupe(const u64* __restrict__ lo, cons
     }
 }
 
+// The same check with one WARP per bucket (buckets of at most kDedupeWarpMax keys): no block
+// barriers, several buckets per block in flight; each warp owns a table of ts entries.
+constexpr u32 kDedupeWarpMax = 256;
+
+__global__ void __launch_bounds__(256) k_dedupe_warp(const u64* __restrict__ lo, const u64* __restrict__ C, u64 nb,
+                                                     u32 ts, u32* dup) {
+    extern __shared__ unsigned long long wtab[];
+    const u32 lane = threadIdx.x & 31;
+    unsigned long long* tab = wtab + (size_t)(threadIdx.x >> 5) * ts;
+    const u64 nw = (u64)gridDim.x * (blockDim.x >> 5);
+    for (u64 b = (u64)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += nw) {
+        const u64 c0 = C[b], s = C[b + 1] - c0;
+        if (s < 2 || 2 * s > ts) continue;  // (larger buckets: flagged by the caller's size bound)
+        for (u32 i = lane; i < ts; i += 32) tab[i] = 0;
+        __syncwarp();
+        bool rep = false;
+        u32 zeros = 0;
+        for (u32 i = lane; i < s; i += 32) {
+            const u64 v = lo[c0 + i];
+            if (v == 0) {
+                ++zeros;
+                continue;
+            }
+            u32 slot = (u32)(v ^ (v >> 32)) & (ts - 1);
+            for (;;) {
+                const unsigned long long old = atomicCAS(tab + slot, 0ull, (unsigned long long)v);
+                if (old == 0ull) break;
+                if (old == v) {
+                    rep = true;
+                    break;
+                }
+                slot = (slot + 1) & (ts - 1);
+            }
+        }
+        if (rep) atomicOr(dup, 1u);
+        if (zeros) atomicAdd(dup + 1, zeros);
+        __syncwarp();
+    }
+}
+
 void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, u64* big_scratch, cudaStream_t st) {
     if (nb == 0) return;
+    if (smax <= kDedupeWarpMax) {
+        u32 ts = 64;
+        while (ts < 2 * smax) ts <<= 1;
+        const u32 wpb = 8;
+        const unsigned grid = (unsigned)std::min<u64>((nb + wpb - 1) / wpb, 148ull * 16);
+        cudaFuncSetAttribute(k_dedupe_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        k_dedupe_warp<<<grid, wpb * 32, (size_t)wpb * ts * 8, st>>>(lo, C, nb, ts, dup);
+        g_launches++;
+        return;
+    }
     const u32 sm = std::min(smax, kSmallBucketKeys);
     u32 ts = 64;
     while (ts < 2 * sm) ts <<= 1;

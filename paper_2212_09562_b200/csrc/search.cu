@@ -1347,7 +1347,7 @@ __global__ void __launch_bounds__(128) k_leaf_sub(const Args A) {
     if (A.dup[0] || A.dup[1] > 1) return;
     const u32 nn = *A.n_nodes;
     u32* G = sG[wib][sub];
-    u32 m = 0, full = 0, slot = 0;
+    u32 m = 0, full = 0, slot = 0, margin = 0;
     u64 k = 0;
     bool busy = false, dry = false;
     for (;;) {
@@ -1376,24 +1376,45 @@ __global__ void __launch_bounds__(128) k_leaf_sub(const Args A) {
                     G[g + 8 + q] = key_const(kh);
                     G[g + 12 + q] = valid && !isb ? FULL : 0u;
                     G[g + 16 + q] = isb ? FULL : 0u;
+                    margin = valid ? ~(u32)key : FULL;  // reduced over the sub-warp below
                 } else {
                     dry = true;
                 }
             }
         }
+        // carry margin of each sub-warp's leaf: min over its keys of 2^32 - 1 - k_lo
+        for (int d = 4; d; d >>= 1) margin = min(margin, __shfl_xor_sync(FULL, margin, d));
         __syncwarp();
         if (!__any_sync(FULL, busy)) break;
-        // one step: lane sl tries base seed k + sl (64-bit keys + value, generic path)
+        // one step: lane sl tries base seed k + sl.  No-carry path (remix_hi_nc, the engine's
+        // 4-key groups) while every key's low word + the step's largest value stays below 2^32
+        // (the leaf's carry margin), else the generic 64-bit path.
         const u64 base = KIND == SK_LEAF_RF ? (k + sl) * m : k + sl;
         u32 a = 0, b = 0;
         if (busy) {
-            RS_COUNT_RAW(m);
+            RS_COUNT_RAW(__reduce_add_sync(FULL, m));
+            const u64 top = KIND == SK_LEAF_RF ? (k + kSubLeafMax) * m : k + kSubLeafMax;
+            if (top <= margin) {
 #pragma unroll
-            for (u32 j = 0; j < kSubLeafMax; ++j) {
-                const u32* gp = G + 20 * (j >> 2) + (j & 3);
-                const u32 bit = 1u << __umulhi(remix_hi((((u64)gp[4] << 32) | gp[0]) + base), m);
-                a |= bit & gp[12];
-                b |= bit & gp[16];
+                for (u32 gi = 0; gi < kSubLeafMax / 4; ++gi) {
+                    const u32* g = G + 20 * gi;
+                    u32 h[4];
+                    hash4<0>(g, (u32)base, h, 0u);
+                    const uint4 ma = *reinterpret_cast<const uint4*>(g + 12);
+                    const uint4 mb = *reinterpret_cast<const uint4*>(g + 16);
+                    const u32 t0 = 1u << __umulhi(h[0], m), t1 = 1u << __umulhi(h[1], m);
+                    const u32 t2 = 1u << __umulhi(h[2], m), t3 = 1u << __umulhi(h[3], m);
+                    a |= (t0 & ma.x) | (t1 & ma.y) | (t2 & ma.z) | (t3 & ma.w);
+                    b |= (t0 & mb.x) | (t1 & mb.y) | (t2 & mb.z) | (t3 & mb.w);
+                }
+            } else {
+#pragma unroll
+                for (u32 j = 0; j < kSubLeafMax; ++j) {
+                    const u32* gp = G + 20 * (j >> 2) + (j & 3);
+                    const u32 bit = 1u << __umulhi(remix_hi((((u64)gp[4] << 32) | gp[0]) + base), m);
+                    a |= bit & gp[12];
+                    b |= bit & gp[16];
+                }
             }
         }
         int r = -1;
@@ -1483,7 +1504,8 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
         static const int cpw2 = getenv("RS_CPW2") ? atoi(getenv("RS_CPW2")) : 1;
         A.cp_wide2 = cpw2 ? 1u : 0u;
     }
-    static const int subleaf = getenv("RS_SUB_LEAF") ? atoi(getenv("RS_SUB_LEAF")) : 1;
+    // (off by default: 3-8 % slower than the warp engine at C2, ab_j / ab_i in DESIGN.md 5)
+    static const int subleaf = getenv("RS_SUB_LEAF") ? atoi(getenv("RS_SUB_LEAF")) : 0;
     if (subleaf && (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) && P.max_size <= kSubLeafMax) {
         // leaves of at most 8 keys: four per warp (k_leaf_sub); the phase's batch cursor is zeroed
         const u32 blocks = std::max<u32>(1, std::min<u32>((P.n_nodes_host + 15) / 16, (u32)P.sm_count * 16));
