@@ -1150,8 +1150,16 @@ __device__ __forceinline__ void init_lower_tables(const Args& A) {
 #ifndef RS_MIN_BLOCKS
 #define RS_MIN_BLOCKS 1
 #endif
+#ifndef RS_LEAF_MIN_BLOCKS
+// leaf kernels at 8 blocks x 4 warps per SM (64 registers): measured -8.5 % on the C5 leaf phase,
+// -3 % at C3, neutral at C2 against the unconstrained 78-88 registers (gpurun pass L)
+#define RS_LEAF_MIN_BLOCKS 8
+#endif
 template <int KIND, int VAR = V_PLAIN>
-__global__ void __launch_bounds__(kWarpsPerBlockMax * 32, KIND == SK_LOWER ? 8 : RS_MIN_BLOCKS) k_search(const Args A) {
+__global__ void __launch_bounds__(kWarpsPerBlockMax * 32,
+                                                     KIND == SK_LOWER                             ? 8
+                                                     : (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) ? RS_LEAF_MIN_BLOCKS
+                                                                                                  : RS_MIN_BLOCKS) k_search(const Args A) {
     constexpr u32 GW = Layout<KIND>::GW;
     extern __shared__ __align__(16) u32 smem32[];
     const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
