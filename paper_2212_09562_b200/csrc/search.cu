@@ -68,7 +68,6 @@ struct Args {
     u32 qwords;    // early-rejection queue words per warp (0 for the plain variants)
     unsigned long long* exec;  // RS_COUNT_EVALS builds: executed evaluations of this phase's class
     u32 lane_fit;  // leaves up to this size check rotations lane by lane (fit_rotation_lane)
-    u32 guided;    // batch mode: single-node batches near the end of the phase
 };
 
 // Bucket-tree kernel (k_bucket_tree): buckets, their per-size preorder templates, slots.
@@ -1185,18 +1184,12 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32,
         // last A.tail nodes; those then run in help mode so that no warp is left with a
         // straggler batch while the others idle
         hbase = nn > A.tail ? nn - A.tail : 0;
-        // guided batches: once fewer than two full rounds of batches remain, one node per
-        // cursor atomic, so that the last nodes spread over all warps instead of queueing
-        // behind one warp's batch (the phase ends with its slowest warp)
-        u32 bsz = A.batch;
-        const u32 guide = A.guided ? 2 * A.n_warps * A.batch : 0;
         for (;;) {
             u32 n0 = 0;
-            if (lane == 0) n0 = atomicAdd(A.cursor, bsz);
+            if (lane == 0) n0 = atomicAdd(A.cursor, A.batch);
             n0 = __shfl_sync(FULL, n0, 0);
             if (n0 >= hbase) break;
-            const u32 n1 = min(n0 + bsz, hbase);
-            if (hbase - n0 < guide) bsz = 1;
+            const u32 n1 = min(n0 + A.batch, hbase);
             // leaves: the next node's record and keys are loaded while this node is searched
             // (two-stage: keys of n + 1 from its record fetched one node earlier, record of n + 2)
             constexpr bool kLeafPf = KIND == SK_LEAF_RF || KIND == SK_LEAF_BF;
@@ -1481,8 +1474,6 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     A.exec = P.exec;
     static const int lane_fit = getenv("RS_LANE_FIT") ? atoi(getenv("RS_LANE_FIT")) : 10;
     A.lane_fit = (u32)std::max(0, lane_fit);
-    static const int guided = getenv("RS_GUIDED") ? atoi(getenv("RS_GUIDED")) : 1;
-    A.guided = guided ? 1u : 0u;
     A.help = P.help;
     // early-rejection checkpoints (per mille of the node size; RS_CP1 / RS_CP2 override, 0 = off)
     {
