@@ -95,6 +95,61 @@ def executed_evals(cfg: dict, world: int):
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
+class NvmlClocks:
+    """NVML sampler thread (every 2 ms) running during the timed region: SM clock, max SM
+    clock and the active clock-event reasons -- enough samples even for a 30 ms timed region
+    (C2), where an nvidia-smi process does not get to its first sample."""
+
+    NAMES = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap")]
+
+    def __init__(self, index: int):
+        import threading
+
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        self.rows = []
+        self.stop_ev = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        while not self.rows and self.t.is_alive():  # first sample before the timed region starts
+            time.sleep(0.001)
+
+    def _run(self):
+        nv = self.nv
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs_ = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001 -- a failed query ends sampling
+                return
+            self.rows.append((sm, mx, rs_))
+            if self.stop_ev.wait(0.002):
+                return
+
+    def stop(self) -> dict:
+        self.stop_ev.set()
+        self.t.join()
+        rows = self.rows[1:] or self.rows  # (the first sample was taken before the timed region)
+        reasons = sorted({nm for _, _, r in rows for nm, c in self.NAMES if r & getattr(self.nv, c)})
+        busy = [s for s, _, _ in rows if s > 300] or [s for s, _, _ in rows]
+        return {"sm_mhz": float(np.median(busy)) if busy else None,
+                "sm_max_mhz": float(max(m for _, m, _ in rows)) if rows else None,
+                "reasons": reasons, "samples": len(rows), "source": "nvml"}
+
+
+def clock_sampler(index: int):
+    try:
+        return NvmlClocks(index)
+    except Exception:  # noqa: BLE001 -- no NVML: the nvidia-smi process sampler
+        return Clocks(index)
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
 
@@ -266,7 +321,7 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clk = Clocks(dev)
+    clk = clock_sampler(dev)
     times, stats = [], []
     blob = None
     for _ in range(args.steps):
