@@ -350,7 +350,8 @@ def main():
         kd = pinned.to("cuda", non_blocking=True)
         return rs.build_sharded(kd, cfg["leaf"], cfg["bucket"], stream=stream, distribute=True)
 
-    e2e_once()  # warm
+    for _ in range(max(3, args.warmup)):  # warm (the first builds of a configuration capture its CUDA graph)
+        e2e_once()
     e2e_times = []
     for _ in range(args.steps):
         flush.zero_()

@@ -109,6 +109,10 @@ typedef struct {
     double t_search_tree;     /* small configurations: the whole-bucket search kernel (all classes
                                  in one launch; t_search is then 0 and exec_evals[0] holds the
                                  executed total), else 0 */
+    double t_device;          /* single-GPU builds: device span from the first enqueued operation to
+                                 the end of the result D2H (CUDA events), else 0 */
+    uint32_t graph_replay;    /* 1 if the build replayed a captured CUDA graph of its configuration */
+    uint32_t reserved0;
 } recsplit_stats;
 
 /* Library version (format version is the header's u16 version = 1). */

@@ -54,7 +54,8 @@ class Stats(C.Structure):
                 ("t_encode", C.c_double), ("t_d2h", C.c_double), ("algo_evals", C.c_uint64 * 4),
                 ("nodes", C.c_uint64 * 4), ("data_bits", C.c_uint64), ("index_bits", C.c_uint64),
                 ("kernel_launches", C.c_uint32), ("max_bucket", C.c_uint32), ("exec_evals", C.c_uint64 * 4),
-                ("t_search_tree", C.c_double)]
+                ("t_search_tree", C.c_double), ("t_device", C.c_double), ("graph_replay", C.c_uint32),
+                ("reserved0", C.c_uint32)]
 
     def as_dict(self) -> dict:
         return {
@@ -64,6 +65,7 @@ class Stats(C.Structure):
             "nodes": list(self.nodes), "data_bits": self.data_bits, "index_bits": self.index_bits,
             "kernel_launches": self.kernel_launches, "max_bucket": self.max_bucket,
             "exec_evals": list(self.exec_evals), "t_search_tree": self.t_search_tree,
+            "t_device": self.t_device, "graph_replay": self.graph_replay,
         }
 
 
@@ -165,16 +167,29 @@ def _take(b: Bytes) -> bytes:
     return out
 
 
+class _Owner:
+    """Owns a library result buffer (freed with recsplit_free when collected) and exposes it
+    to numpy through the array interface (a read-only view, no copy)."""
+
+    __slots__ = ("holder", "__array_interface__", "__weakref__")
+
+    def __init__(self, b: Bytes):
+        self.holder = Bytes(b.data, b.size)
+        addr = C.cast(b.data, C.c_void_p).value or 0
+        self.__array_interface__ = {"data": (addr, True), "shape": (b.size,), "typestr": "|u1", "version": 3}
+
+    def __del__(self):
+        if self.holder.data:
+            _lib.recsplit_free(C.byref(self.holder))
+
+
 def _view(b: Bytes) -> np.ndarray:
     """The library's result buffer as a read-only uint8 array (no copy); released with
-    recsplit_free when the array is garbage collected."""
-    import weakref
-
-    holder = Bytes(b.data, b.size)
-    arr = np.ctypeslib.as_array(b.data, shape=(b.size,)) if b.size else np.zeros(0, np.uint8)
-    arr.flags.writeable = False
-    weakref.finalize(arr, lib().recsplit_free, C.byref(holder))
-    return arr
+    recsplit_free when the array is garbage collected (the array keeps its owner alive)."""
+    if not b.size:
+        lib().recsplit_free(C.byref(b))
+        return np.zeros(0, np.uint8)
+    return np.asarray(_Owner(b))
 
 
 def build(keys, leaf_size: int, bucket_size: int, rotation_fitting: bool = True, global_seed: int = 0,

@@ -8,6 +8,7 @@
 #include <cstddef>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -111,6 +112,20 @@ int emit(rs::BuildOutput& o, recsplit_bytes* out) {
         if (e_ != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, cudaGetErrorString(e_));           \
     } while (0)
 
+// one non-blocking stream per device for graph replays of host-key builds (builds are
+// serialized by g_build_mu)
+cudaStream_t replay_stream(int dev) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> st;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = st.find(dev);
+    if (it != st.end()) return it->second;
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
+    st[dev] = s;
+    return s;
+}
+
 int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, const recsplit_options* opt,
                     recsplit_bytes* out, recsplit_stats* stats, rs::BuildOutput* keep, bool want_values) {
     if (!out) return fail(RECSPLIT_E_INVALID, "out is NULL");
@@ -123,24 +138,10 @@ int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, c
         std::lock_guard<std::mutex> g(g_build_mu);
         auto t0 = std::chrono::steady_clock::now();
         rs::BuildParams p = params_of(n, leaf, b, opt);
+        p.want_stats = stats != nullptr;
         select_device(p.device);
-        cudaStream_t st;
-        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
-            throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
-        struct StreamGuard {
-            cudaStream_t s;
-            ~StreamGuard() { cudaStreamDestroy(s); }
-        } sg{st};
         int dev = 0;
         cudaGetDevice(&dev);
-        uint64_t* d_keys = nullptr;
-        cudaError_t e = cudaMallocFromPoolAsync((void**)&d_keys, n * 8, rs::device_pool(dev), st);
-        if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_NOMEM, "device allocation of keys failed");
-        struct KeyGuard {
-            uint64_t* p;
-            cudaStream_t s;
-            ~KeyGuard() { cudaFreeAsync(p, s); }
-        } kg{d_keys, st};
         // pinned host keys of an unsharded build are streamed in chunks overlapped with the
         // hash kernel; pageable ones are copied in one piece first
         // (memory pinned by another CUDA runtime in the process -- e.g. PyTorch's -- is page-locked
@@ -152,6 +153,30 @@ int build_host_keys(const uint64_t* keys, size_t n, uint32_t leaf, uint32_t b, c
                             cudaHostGetFlags(&host_flags, const_cast<uint64_t*>(keys)) == cudaSuccess;
         cudaGetLastError();
         const bool stream_keys = pinned && p.shards <= 1;
+        if (stream_keys && !want_values && !keep) {  // a captured graph of this configuration: one launch
+            cudaStream_t rst = replay_stream(dev);
+            rs::BuildOutput o;
+            if (rs::replay_host_keys(keys, p, rst, o)) {
+                o.stats.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                if (stats) *stats = o.stats;
+                return emit(o, out);
+            }
+        }
+        cudaStream_t st;
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+            throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{st};
+        uint64_t* d_keys = nullptr;
+        cudaError_t e = cudaMallocFromPoolAsync((void**)&d_keys, n * 8, rs::device_pool(dev), st);
+        if (e != cudaSuccess) throw rs::Error(RECSPLIT_E_NOMEM, "device allocation of keys failed");
+        struct KeyGuard {
+            uint64_t* p;
+            cudaStream_t s;
+            ~KeyGuard() { cudaFreeAsync(p, s); }
+        } kg{d_keys, st};
         cudaStream_t cs = nullptr;
         if (stream_keys && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
             throw rs::Error(RECSPLIT_E_CUDA, "stream creation failed");
@@ -348,6 +373,7 @@ int recsplit_build_device(const uint64_t* d_keys, size_t n, uint32_t leaf_size, 
         std::lock_guard<std::mutex> g(g_build_mu);
         auto t0 = std::chrono::steady_clock::now();
         rs::BuildParams p = params_of(n, leaf_size, bucket_size, opt);
+        p.want_stats = stats != nullptr;
         select_device(p.device);
         rs::BuildOutput o;
         rs::build_on_device(d_keys, p, (cudaStream_t)stream, false, o);

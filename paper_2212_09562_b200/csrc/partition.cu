@@ -412,3 +412,186 @@ void route_keys(const u64* d_keys, u64 n, u64 total, u32 bucket, u64 g, u32 worl
 }
 
 }  // namespace rs
+
+namespace rs {
+using namespace rsd;
+
+// ============================================================ two-level sort ==
+//
+// A2 as a two-level counting sort for the one-enqueue build (no per-key global atomics, every
+// write of the second level coalesced).  Buckets are grouped by 2^gl consecutive bucket ids
+// (gl chosen so that a group holds at most kGroupCap keys when every bucket is within the
+// build's size bound S).  Level 0 counts the keys of each group (shared-memory histogram per
+// block); a scan gives each group's start.  Level 1: each block takes a contiguous chunk of
+// keys, counts its keys per group in shared memory, reserves its range inside every group
+// with ONE global atomic per (block, group), and writes (lo, bucket-in-group | A/B << 8) to
+// it.  Level 2: one block per group stages the group's keys in shared memory, counting-sorts
+// them by bucket, writes them out in bucket order (coalesced) together with the bucket
+// offsets C ("sort by bucket index, determine borders") and the max / min bucket size.
+// Keys inside a bucket end up in an arbitrary order: every stored value depends only on the
+// key set of its node.
+namespace {
+
+__device__ __forceinline__ u64 bucket_of(u64 key, u64 g, u64 B) {
+    return ((remix64(key ^ g ^ MHC_SALT_HI) >> 32) * B) >> 32;
+}
+
+__global__ void __launch_bounds__(1024) k_p2_count(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 gl, u32 G,
+                                                   unsigned long long* __restrict__ gcount) {
+    extern __shared__ u32 hc[];
+    for (u32 i = threadIdx.x; i < G; i += blockDim.x) hc[i] = 0;
+    __syncthreads();
+    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+        atomicAdd(hc + (u32)(bucket_of(keys[i], g, B) >> gl), 1u);
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < G; i += blockDim.x)
+        if (hc[i]) atomicAdd(gcount + i, (unsigned long long)hc[i]);
+}
+
+// gcursor: the groups' start offsets (advanced); chunk = keys per block
+__global__ void __launch_bounds__(1024) k_p2_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 gl,
+                                                     u32 G, u64 chunk, unsigned long long* __restrict__ gcursor,
+                                                     u64* __restrict__ lo1, u16* __restrict__ meta1) {
+    extern __shared__ u32 sc[];  // per group: count, then write cursor
+    const u64 k0 = (u64)blockIdx.x * chunk, k1 = min(n, k0 + chunk);
+    for (u32 i = threadIdx.x; i < G; i += blockDim.x) sc[i] = 0;
+    __syncthreads();
+    for (u64 i = k0 + threadIdx.x; i < k1; i += blockDim.x) atomicAdd(sc + (u32)(bucket_of(keys[i], g, B) >> gl), 1u);
+    __syncthreads();
+    for (u32 i = threadIdx.x; i < G; i += blockDim.x) {
+        const u32 c = sc[i];
+        sc[i] = c ? (u32)atomicAdd(gcursor + i, (unsigned long long)c) : 0u;  // (n < 2^32)
+    }
+    __syncthreads();
+    for (u64 i = k0 + threadIdx.x; i < k1; i += blockDim.x) {
+        const u64 k = keys[i] ^ g;
+        const u64 h = remix64(k ^ MHC_SALT_HI);
+        const u64 b = ((h >> 32) * B) >> 32;
+        const u32 pos = atomicAdd(sc + (u32)(b >> gl), 1u);
+        lo1[pos] = remix64(k ^ MHC_SALT_LO);
+        meta1[pos] = (u16)((b & ((1u << gl) - 1u)) | ((h & 1) << 8));
+    }
+}
+
+// one block per group: counting sort by bucket in shared memory, coalesced output, offsets C,
+// max / min bucket size (small[0], small[1]); a group above cap keys (a bucket above the
+// build's bound S) sets small[5] and leaves its buckets empty (the build is redone on the
+// synchronized path)
+__global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ lo1, const u16* __restrict__ meta1,
+                                                  const unsigned long long* __restrict__ gstart, u64 B, u32 gl, u32 G,
+                                                  u32 cap, u64* __restrict__ C, u64* __restrict__ lo_a,
+                                                  u8* __restrict__ ab_a, u32* small) {
+    extern __shared__ __align__(16) unsigned char p2s[];
+    const u32 gb = 1u << gl;
+    u32* cnt = reinterpret_cast<u32*>(p2s);  // gb counts -> exclusive offsets
+    u32* cur = cnt + gb;                     // gb write cursors
+    u64* lo_s = reinterpret_cast<u64*>(p2s + ((8u * gb + 15u) & ~15u));
+    u8* ab_s = reinterpret_cast<u8*>(lo_s + cap);
+    for (u32 grp = blockIdx.x; grp < G; grp += gridDim.x) {
+        const u64 gs = gstart[grp], ge = gstart[grp + 1];
+        const u64 b0 = (u64)grp << gl;
+        const u32 nb = (u32)min((u64)gb, B - b0);
+        const u32 cg = (u32)(ge - gs);
+        if (grp == G - 1 && threadIdx.x == 0) C[B] = ge;
+        __syncthreads();
+        if (cg > cap) {
+            if (threadIdx.x == 0) atomicOr(small + 5, 1u);
+            for (u32 j = threadIdx.x; j < nb; j += blockDim.x) C[b0 + j] = gs;
+            continue;
+        }
+        for (u32 j = threadIdx.x; j < gb; j += blockDim.x) cnt[j] = 0;
+        __syncthreads();
+        for (u32 i = threadIdx.x; i < cg; i += blockDim.x) atomicAdd(cnt + (meta1[gs + i] & 0xffu), 1u);
+        __syncthreads();
+        if (threadIdx.x < 32) {  // exclusive scan of gb <= 256 counts by one warp; sizes' max / min
+            const u32 lane = threadIdx.x;
+            u32 carry = 0, mx = 0, mn = 0xffffffffu;
+            for (u32 base = 0; base < gb; base += 32) {
+                const u32 j = base + lane;
+                const u32 v = j < gb ? cnt[j] : 0;
+                if (j < nb) {
+                    mx = max(mx, v);
+                    mn = min(mn, v);
+                }
+                u32 inc = v;
+                for (int d = 1; d < 32; d <<= 1) {
+                    const u32 t = __shfl_up_sync(FULL, inc, d);
+                    if ((int)lane >= d) inc += t;
+                }
+                if (j < gb) {
+                    cnt[j] = carry + inc - v;
+                    cur[j] = carry + inc - v;
+                }
+                carry += __shfl_sync(FULL, inc, 31);
+            }
+            for (int d = 16; d; d >>= 1) {
+                mx = max(mx, __shfl_xor_sync(FULL, mx, d));
+                mn = min(mn, __shfl_xor_sync(FULL, mn, d));
+            }
+            if (lane == 0 && nb) {
+                atomicMax(small, mx);
+                atomicMin(small + 1, mn);
+            }
+        }
+        __syncthreads();
+        for (u32 j = threadIdx.x; j < nb; j += blockDim.x) C[b0 + j] = gs + cnt[j];
+        for (u32 i = threadIdx.x; i < cg; i += blockDim.x) {
+            const u32 m = meta1[gs + i];
+            const u32 pos = atomicAdd(cur + (m & 0xffu), 1u);
+            lo_s[pos] = lo1[gs + i];
+            ab_s[pos] = (u8)(m >> 8);
+        }
+        __syncthreads();
+        for (u32 i = threadIdx.x; i < cg; i += blockDim.x) {
+            lo_a[gs + i] = lo_s[i];
+            ab_a[gs + i] = ab_s[i];
+        }
+    }
+}
+
+}  // namespace
+
+bool partition2_shape(u64 n, u64 B, u32 S, P2Shape& sh) {
+    if (n == 0 || B == 0 || S == 0 || S > kGroupCap || n >= (1ull << 32)) return false;
+    u32 gl = 0;
+    while (gl < 8 && (2ull << gl) * S <= kGroupCap) ++gl;
+    const u64 G = (B + (1ull << gl) - 1) >> gl;
+    if (G > kGroupMax) return false;
+    sh.gl = gl;
+    sh.G = (u32)G;
+    sh.cap = (u32)std::min<u64>(kGroupCap, (u64)S << gl);
+    // keys per level-1 block: about 4 blocks per SM, at least 8 keys per group per block
+    sh.chunk = std::max<u64>(std::max<u64>(4096, 8ull * G), (n + 148 * 4 - 1) / (148 * 4));
+    sh.chunk = (sh.chunk + 1023) & ~1023ull;
+    return true;
+}
+
+void launch_p2_count(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, unsigned long long* gcount,
+                     cudaStream_t st) {
+    if (!n) return;
+    const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>((n + 4095) / 4096, 148ull * 2));
+    cudaFuncSetAttribute(k_p2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_p2_count<<<grid, 1024, (size_t)sh.G * 4, st>>>(keys, n, g, B, sh.gl, sh.G, gcount);
+    g_launches++;
+}
+
+void launch_p2_scatter(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, unsigned long long* gcursor, u64* lo1,
+                       u16* meta1, cudaStream_t st) {
+    const unsigned nb1 = (unsigned)((n + sh.chunk - 1) / sh.chunk);
+    cudaFuncSetAttribute(k_p2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_p2_scatter<<<nb1, 1024, (size_t)sh.G * 4, st>>>(keys, n, g, B, sh.gl, sh.G, sh.chunk, gcursor, lo1, meta1);
+    g_launches++;
+}
+
+void launch_p2_group(u64 B, const P2Shape& sh, const unsigned long long* gstart, const u64* lo1, const u16* meta1,
+                     u64* C, u64* lo_a, u8* ab_a, u32* small, cudaStream_t st) {
+    const size_t smem = ((8u * (1u << sh.gl) + 15u) & ~15u) + (size_t)sh.cap * 9;
+    cudaFuncSetAttribute(k_p2_group, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2_group, 512, smem);
+    const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>(sh.G, 148ull * std::max(occ, 1)));
+    k_p2_group<<<grid, 512, smem, st>>>(lo1, meta1, gstart, B, sh.gl, sh.G, sh.cap, C, lo_a, ab_a, small);
+    g_launches++;
+}
+
+}  // namespace rs

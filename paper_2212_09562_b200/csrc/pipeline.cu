@@ -133,6 +133,7 @@ struct DevTables {
     uint32_t* tstart = nullptr;
     rsd::TNodeD* tnodes = nullptr;
     uint32_t* phase_cnt = nullptr;
+    uint64_t gen = 0;  // bumped whenever the device arrays are rebuilt (captured graphs hold them)
     uint32_t* N = nullptr;
     uint64_t* F = nullptr;
     int dev = -1;
@@ -150,10 +151,30 @@ struct DevTables {
     }
 };
 
+uint64_t& device_tables_gen_counter() {
+    static uint64_t g = 0;
+    return g;
+}
+std::mutex& device_tables_mu() {
+    static std::mutex mu;
+    return mu;
+}
+std::map<int, std::unique_ptr<DevTables>>& device_tables_cache() {
+    static std::map<int, std::unique_ptr<DevTables>> cache;
+    return cache;
+}
+
+// generation of the cached device tables of dev (0: none)
+uint64_t device_tables_generation(int dev) {
+    std::lock_guard<std::mutex> g(device_tables_mu());
+    auto it = device_tables_cache().find(dev);
+    return it == device_tables_cache().end() || !it->second ? 0 : it->second->gen;
+}
+
 const DevTables& device_tables(int dev, uint32_t leaf, bool rf, uint32_t smax, const std::vector<uint8_t>& present,
                                cudaStream_t st) {
-    static std::mutex mu;
-    static std::map<int, std::unique_ptr<DevTables>> cache;
+    std::mutex& mu = device_tables_mu();
+    auto& cache = device_tables_cache();
     std::lock_guard<std::mutex> g(mu);
     auto& slot = cache[dev];
     if (slot && slot->leaf == leaf && slot->rf == rf && slot->smax == smax && slot->present == present) return *slot;
@@ -161,6 +182,7 @@ const DevTables& device_tables(int dev, uint32_t leaf, bool rf, uint32_t smax, c
     DevTables& D = *slot;
     CK(cudaStreamSynchronize(st));
     D.release();
+    D.gen = ++device_tables_gen_counter();
     D.leaf = leaf;
     D.rf = rf;
     D.smax = smax;
@@ -933,6 +955,16 @@ void stitch(const std::vector<std::pair<const uint8_t*, size_t>>& parts, std::ve
 // are computed by kernels and the serialized MPHF is assembled in one device buffer.  One D2H
 // and one synchronization at the end.  A bucket above S (flagged by the kernels) makes the
 // call return false and the caller rebuilds on the synchronized path.
+//
+// CUDA graphs: since every launch parameter of this path depends only on the configuration
+// (n, l, b, rotation fitting, g) -- never on the keys -- the whole enqueue (memsets, ~30
+// kernels, the chunked H2D of host keys, the report and result D2H) is captured once per
+// configuration into a graph over a persistent workspace and replayed: the host then issues
+// one cudaGraphLaunch instead of ~40 API calls, so the GPU does not wait for the host's
+// enqueue between short kernels (small configurations).  Per replay only the key source
+// (kernel parameter of k_hash, or the source of the H2D chunk copies) and the destination of
+// the result copy change (cudaGraphExec*SetParams).  The first build of a configuration runs
+// uncaptured and measures its workspace; the second captures; later builds replay.
 namespace {
 
 struct PinnedReport {
@@ -945,41 +977,118 @@ struct PinnedReport {
 };
 PinnedReport g_report;
 
+using ConfigKey = std::tuple<int, uint64_t, uint32_t, uint32_t, bool, uint64_t, bool, bool>;  // dev n l b rf g host stats
 std::mutex g_est_mu;
-std::map<std::tuple<uint64_t, uint32_t, uint32_t, bool, uint64_t>, uint64_t> g_est_words;  // last blob size
+std::map<ConfigKey, uint64_t> g_est_words;  // last blob size (words) per configuration
+std::map<ConfigKey, size_t> g_ws_bytes;     // workspace of the last uncaptured build
 
-}  // namespace
+// Device allocations of one build: the library pool (stream-ordered, released at scope exit)
+// or, while a graph is captured, a bump allocator over the plan's persistent workspace.
+struct Alloc {
+    Arena* arena = nullptr;
+    uint8_t* base = nullptr;
+    size_t cap = 0, used = 0, total = 0;
+    template <typename T>
+    T* alloc(size_t count) {
+        const size_t bytes = (std::max<size_t>(count * sizeof(T), 16) + 255) & ~(size_t)255;
+        total += bytes;
+        if (arena) return arena->alloc<T>(count);
+        if (used + bytes > cap) throw Error(RECSPLIT_E_NOMEM, "graph workspace too small");
+        T* p = (T*)(base + used);
+        used += bytes;
+        return p;
+    }
+    void release(void* p) {
+        if (arena) arena->release(p);
+    }
+};
 
-bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out) {
-    auto t_start = std::chrono::steady_clock::now();
+// CUDA-event marks on a plan-owned event list (graph) or the thread's event pool (Timer)
+struct Marks {
+    Timer* tm = nullptr;
+    std::vector<cudaEvent_t>* ev = nullptr;
+    bool on = true;  // false: no events (the caller did not ask for timings)
+    int mark(cudaStream_t s) {
+        if (!on) return -1;
+        if (tm) {
+            if (s == tm->st) return tm->mark();
+            cudaStream_t keep = tm->st;  // (the copy stream's span of the streamed host keys)
+            tm->st = s;
+            const int i = tm->mark();
+            tm->st = keep;
+            return i;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        ev->push_back(e);
+        // (External: an event-record node of the graph, timed on every replay; a plain record in
+        // a capturing stream is only a dependency marker)
+        CK(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+        return (int)ev->size() - 1;
+    }
+    double secs(int a, int b) const {
+        if (a < 0 || b < 0) return 0.0;
+        if (tm) return tm->secs(a, b);
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, (*ev)[a], (*ev)[b]));
+        return ms * 1e-3;
+    }
+};
+
+struct PhaseEv {
+    uint32_t cls;
+    int a, b, c;
+};
+
+// What the host needs after the synchronization (marks, report layout, result buffer).
+struct SingleRun {
+    int e0 = -1, e1 = -1, e2 = -1, e3 = -1, e4 = -1, e5 = -1, et0 = -1, et1 = -1, h0 = -1, h1 = -1;
+    std::vector<PhaseEv> pev;
+    std::vector<uint32_t> phase_cls;  // class of each phase (stats)
+    uint32_t NP = 0;
+    uint64_t S = 0;
+    uint64_t est_words = 0;
+    unsigned long long* outw = nullptr;  // device result buffer
+    uint8_t* rep = nullptr;              // pinned report
+    uint8_t* buf = nullptr;              // pinned result (caller's buffer)
+    bool exec_counted = false;
+    // graph capture: the nodes a replay updates
+    std::vector<cudaGraphNode_t> hash_nodes;  // device keys: the kernels reading them (key pointer = parameter 0)
+    std::vector<int> hash_argc;               // ... their parameter counts
+    std::vector<uint64_t> hash_off;           // ... and key offsets
+    std::vector<cudaGraphNode_t> h2d_nodes;   // host keys: chunk copies
+    std::vector<std::pair<uint64_t, uint64_t>> chunks;  // (offset, length) in keys
+    cudaGraphNode_t blob_node = nullptr;
+    uint64_t* d_keys_ws = nullptr;  // host keys: the plan's device key buffer
+};
+
+// the node just added to a capturing stream (its only dependency afterwards)
+cudaGraphNode_t last_node(cudaStream_t s) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cs, nullptr, nullptr, &deps, &nd));
+    if (cs != cudaStreamCaptureStatusActive || nd != 1) throw Error(RECSPLIT_E_CUDA, "graph capture: no single last node");
+    return deps[0];
+}
+
+// Enqueue the whole one-enqueue build on st (uncaptured, or into a capture when `capture`).
+// Returns false if the configuration is not eligible (buckets above kSmallBucketKeys).
+bool enqueue_single(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, Alloc& A, Marks& tm,
+                    SingleRun& R, bool capture, cudaStream_t copy_stream) {
     const uint64_t n = p.n;
     const uint32_t leaf = p.leaf;
     const uint64_t B = (n + p.bucket - 1) / p.bucket;  // R12
     const double avg = (double)n / (double)B;
     const uint32_t S = (uint32_t)std::min<uint64_t>(n, (uint64_t)(avg + 8.0 * std::sqrt(avg) + 32.0));
     if (S > kSmallBucketKeys || B >= (1ull << 31)) return false;
-    g_launches = 0;
+    R.S = S;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     init_device(dev);
     const int sms = sm_count(dev);
     const Shape sh = make_shape(leaf);
-    recsplit_stats& Sst = out.stats;
-    memset(&Sst, 0, sizeof Sst);
-    Arena A(st);
-    Timer tm(st);
-    const int e0 = tm.mark();
-    cudaEvent_t h2d_ev[2];  // streamed host keys: the copy stream's span (stats.t_h2d)
-    bool h2d_timed = false;
-    CK(cudaEventCreate(&h2d_ev[0]));
-    CK(cudaEventCreate(&h2d_ev[1]));
-    struct EvGuard {
-        cudaEvent_t* e;
-        ~EvGuard() {
-            cudaEventDestroy(e[0]);
-            cudaEventDestroy(e[1]);
-        }
-    } evg{h2d_ev};
+    R.e0 = tm.mark(st);
 
     // small configurations: whole buckets per warp (k_bucket_tree), no node table; decided
     // before the partition because the tree kernel also does the duplicate check
@@ -1001,57 +1110,121 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         tree = tree && !help;
     }
     // ---- A1/A2 ----------------------------------------------------------------
-    u64* lo_t = A.alloc<u64>(n);
-    u8* ab_t = A.alloc<u8>(n);
-    u32* bkt = A.alloc<u32>(n);
-    u32* hist = A.alloc<u32>(B + 1);
     u64* C = A.alloc<u64>(B + 2);
-    u64* cursor = A.alloc<u64>(B + 1);
     u32* small = A.alloc<u32>(8);  // [0] max, [1] min bucket size, [2] dup, [3] lo == 0, [4] seed cap, [5] size > S
-    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(B + 1) + 64);
-    CK(cudaMemsetAsync(hist, 0, (B + 1) * 4, st));
-    const uint32_t small_init[8] = {0, 0xffffffffu, 0, 0, 0, 0, 0, 0};
-    CK(cudaMemcpyAsync(small, small_init, sizeof small_init, cudaMemcpyHostToDevice, st));
-    if (p.h_keys && !p.strings) {  // A1 overlapped with the chunked host->device copy
-        const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
-        std::vector<cudaEvent_t> evs;
-        CK(cudaEventRecord(h2d_ev[0], p.copy_stream));
-        for (uint64_t off = 0; off < n; off += chunk) {
-            const uint64_t len = std::min(chunk, n - off);
-            cudaEvent_t ev;
-            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-            evs.push_back(ev);
-            CK(cudaMemcpyAsync(const_cast<uint64_t*>(d_keys) + off, p.h_keys + off, len * 8, cudaMemcpyHostToDevice,
-                               p.copy_stream));
-            CK(cudaEventRecord(ev, p.copy_stream));
-            CK(cudaStreamWaitEvent(st, ev, 0));
-            launch_hash(d_keys + off, nullptr, len, p.g, B, 0, B, lo_t + off, ab_t + off, bkt + off, hist, st);
+    CK(cudaMemsetAsync(small, 0, 32, st));
+    CK(cudaMemsetAsync(small + 1, 0xff, 4, st));  // min bucket size starts at UINT32_MAX
+    // two-level counting sort (partition.cu) unless the groups would not fit its bounds
+    static const int p2_env = getenv("RS_P2") ? atoi(getenv("RS_P2")) : 1;
+    P2Shape p2;
+    const bool two = p2_env && !p.strings && partition2_shape(n, B, S, p2);
+    u64* lo_a = nullptr;
+    u8* ab_a = nullptr;
+    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(B, two ? p2.G : 0) + 1) + 64);
+    // the key source: device keys, or pinned host keys copied in chunks on the copy stream with
+    // `per_chunk(off, len)` enqueued on st behind each chunk (A1 overlapped with the H2D)
+    auto over_keys = [&](auto per_chunk) {
+        if (p.h_keys && !p.strings) {
+            const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
+            std::vector<cudaEvent_t> evs;
+            cudaEvent_t fork;
+            CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+            evs.push_back(fork);
+            CK(cudaEventRecord(fork, st));  // (the key buffer and the workspace are ordered on st)
+            CK(cudaStreamWaitEvent(copy_stream, fork, 0));
+            R.h0 = tm.mark(copy_stream);
+            for (uint64_t off = 0; off < n; off += chunk) {
+                const uint64_t len = std::min(chunk, n - off);
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                evs.push_back(ev);
+                CK(cudaMemcpyAsync(const_cast<uint64_t*>(d_keys) + off, p.h_keys + off, len * 8,
+                                   cudaMemcpyHostToDevice, copy_stream));
+                if (capture) {
+                    R.h2d_nodes.push_back(last_node(copy_stream));
+                    R.chunks.push_back({off, len});
+                }
+                CK(cudaEventRecord(ev, copy_stream));
+                CK(cudaStreamWaitEvent(st, ev, 0));
+                per_chunk(off, len);
+            }
+            R.h1 = tm.mark(copy_stream);
+            cudaEvent_t join;  // the copy stream's last event (the span mark) joins st
+            CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+            evs.push_back(join);
+            CK(cudaEventRecord(join, copy_stream));
+            CK(cudaStreamWaitEvent(st, join, 0));
+            for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // (released once complete)
+        } else {
+            per_chunk((uint64_t)0, n);
+            if (capture && !p.strings) {
+                R.hash_nodes.push_back(last_node(st));
+                R.hash_argc.push_back(two ? kP2CountParams : kHashParams);
+                R.hash_off.push_back(0);
+            }
+        }
+    };
+    if (two) {
+        unsigned long long* gcount = A.alloc<unsigned long long>(p2.G + 1);
+        u64* gstart = A.alloc<u64>(p2.G + 2);
+        unsigned long long* gcur = A.alloc<unsigned long long>(p2.G + 1);
+        u64* lo1 = A.alloc<u64>(n);
+        u16* meta1 = A.alloc<u16>(n);
+        CK(cudaMemsetAsync(gcount, 0, (p2.G + 1) * 8, st));
+        over_keys([&](uint64_t off, uint64_t len) {
+            launch_p2_count(d_keys + off, len, p.g, B, p2, gcount, st);
+            CKL();
+        });
+        exscan_u64((const u64*)gcount, gstart, p2.G, scan_tmp, st);
+        CKL();
+        CK(cudaMemcpyAsync(gcur, gstart, (p2.G + 1) * 8, cudaMemcpyDeviceToDevice, st));
+        lo_a = A.alloc<u64>(n);
+        ab_a = A.alloc<u8>(n);
+        launch_p2_scatter(d_keys, n, p.g, B, p2, gcur, lo1, meta1, st);
+        CKL();
+        if (capture && !p.h_keys) {
+            R.hash_nodes.push_back(last_node(st));
+            R.hash_argc.push_back(kP2ScatterParams);
+            R.hash_off.push_back(0);
+        }
+        launch_p2_group(B, p2, (const unsigned long long*)gstart, lo1, meta1, C, lo_a, ab_a, small, st);
+        CKL();
+        if (!tree) {  // (tree: each warp checks its own bucket)
+            launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
             CKL();
         }
-        CK(cudaEventRecord(h2d_ev[1], p.copy_stream));
-        h2d_timed = true;
-        for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+        A.release(lo1);
+        A.release(meta1);
     } else {
-        launch_hash(p.strings ? nullptr : d_keys, p.strings ? d_keys : nullptr, n, p.g, B, 0, B, lo_t, ab_t, bkt, hist, st);
+        u64* lo_t = A.alloc<u64>(n);
+        u8* ab_t = A.alloc<u8>(n);
+        u32* bkt = A.alloc<u32>(n);
+        u32* hist = A.alloc<u32>(B + 1);
+        u64* cursor = A.alloc<u64>(B + 1);
+        CK(cudaMemsetAsync(hist, 0, (B + 1) * 4, st));
+        over_keys([&](uint64_t off, uint64_t len) {
+            launch_hash(p.strings ? nullptr : d_keys + off, p.strings ? d_keys : nullptr, len, p.g, B, 0, B,
+                        lo_t + off, ab_t + off, bkt + off, hist, st);
+            CKL();
+        });
+        launch_bucket_stats(hist, B, small, nullptr, S, st);  // max / min only (no size histogram needed)
         CKL();
-    }
-    launch_bucket_stats(hist, B, small, nullptr, S, st);  // max / min only (no size histogram needed)
-    CKL();
-    exscan_u32_to_u64(hist, C, B, scan_tmp, st);
-    CKL();
-    CK(cudaMemcpyAsync(cursor, C, (B + 1) * 8, cudaMemcpyDeviceToDevice, st));
-    u64* lo_a = A.alloc<u64>(n);
-    u8* ab_a = A.alloc<u8>(n);
-    launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
-    CKL();
-    if (!tree) {  // (tree: each warp checks its own bucket)
-        launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
+        exscan_u32_to_u64(hist, C, B, scan_tmp, st);
         CKL();
+        CK(cudaMemcpyAsync(cursor, C, (B + 1) * 8, cudaMemcpyDeviceToDevice, st));
+        lo_a = A.alloc<u64>(n);
+        ab_a = A.alloc<u8>(n);
+        launch_scatter(lo_t, ab_t, bkt, n, cursor, lo_a, ab_a, st);
+        CKL();
+        if (!tree) {  // (tree: each warp checks its own bucket)
+            launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
+            CKL();
+        }
+        A.release(lo_t);
+        A.release(ab_t);
+        A.release(bkt);
     }
-    A.release(lo_t);
-    A.release(ab_t);
-    A.release(bkt);
-    const int e1 = tm.mark();
+    R.e1 = tm.mark(st);
 
     // ---- A3: node table for all sizes <= S --------------------------------------
     std::vector<uint8_t> present(S + 1, 1);
@@ -1059,6 +1232,10 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     const DevTables& DT = device_tables(dev, leaf, p.rf, S, present, st);
     const Tables& T = *DT.T;
     const uint32_t NP = T.NP;
+    R.NP = NP;
+    R.phase_cls.resize(NP);
+    for (uint32_t q = 0; q < NP; ++q)
+        R.phase_cls[q] = q < T.n_upper ? 0 : q == T.phase_L2() ? 1 : q == T.phase_L1() ? 2 : 3;
     const uint64_t rows = (uint64_t)(NP + 1) * (B + 1);
     u64* M = A.alloc<u64>(rows);
     u64* Ms = A.alloc<u64>(rows + 1);
@@ -1095,6 +1272,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
 #ifdef RS_COUNT_EVALS
     exec_d = A.alloc<unsigned long long>(4);
     CK(cudaMemsetAsync(exec_d, 0, 32, st));
+    R.exec_counted = true;
 #endif
     if (!tree) {  // (the bucket-tree kernel writes every value once and uses no dispensers)
         CK(cudaMemsetAsync(values_d, 0xff, nbound * 8, st));
@@ -1107,15 +1285,9 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         launch_expand(C, B, Ms, NP, DT.tstart, DT.tnodes, poff.data(), nodes, st, S);
         CKL();
     }
-    const int e2 = tm.mark();
+    R.e2 = tm.mark(st);
 
     // ---- A4-A9 -----------------------------------------------------------------
-    struct PhaseEv {
-        uint32_t cls;
-        int a, b, c;
-    };
-    std::vector<PhaseEv> pev;
-    int et0 = -1, et1 = -1;
     if (tree) {
         TreeLaunch L{};
         L.lo = lo_a;
@@ -1137,35 +1309,32 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         L.sm_count = sms;
         L.exec = exec_d;
         L.dedupe = true;
-        et0 = tm.mark();
+        R.et0 = tm.mark(st);
         launch_bucket_tree(L, st);
         CKL();
-        et1 = tm.mark();
+        R.et1 = tm.mark(st);
     }
     for (uint32_t q = 0; q < NP && !tree; ++q) {
         if (bound[q] == 0) continue;
         SearchKind kind;
-        uint32_t maxs, typical, cls;
-        if (q < T.n_upper) {
+        uint32_t maxs, typical;
+        const uint32_t cls = R.phase_cls[q];
+        if (cls == 0) {
             kind = SK_UPPER;
             maxs = S;
             typical = std::min<uint32_t>(S, 2 * sh.u2);
-            cls = 0;
-        } else if (q == T.phase_L2()) {
+        } else if (cls == 1) {
             kind = SK_LOWER;
             maxs = sh.u2;
             typical = sh.u2;
-            cls = 1;
-        } else if (q == T.phase_L1()) {
+        } else if (cls == 2) {
             kind = SK_LOWER;
             maxs = sh.u1;
             typical = sh.u1;
-            cls = 2;
         } else {
             kind = p.rf ? SK_LEAF_RF : SK_LEAF_BF;
             maxs = leaf;
             typical = leaf;
-            cls = 3;
         }
         PhaseLaunch P{};
         P.kind = kind;
@@ -1191,19 +1360,19 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
         P.ab_w = ab_a;
         P.exec = exec_d ? exec_d + cls : nullptr;
         CK(cudaMemsetAsync(active, 0xff, nslots * 4, st));
-        const int a = tm.mark();
+        const int a = tm.mark(st);
         const bool fused = launch_search(P, st);
         CKL();
-        const int b = tm.mark();
+        const int b = tm.mark(st);
         if ((kind == SK_UPPER || kind == SK_LOWER) && !fused) {
             launch_reorder(nodes + poff[q], P.n_nodes_host, values_d, lo_a, ab_a, leaf, sh.u1, sh.u2, maxs, sms, nullptr,
                            st, pcnt_d + q);
             CKL();
         }
-        const int c = tm.mark();
-        pev.push_back({cls, a, b, c});
+        const int c = tm.mark(st);
+        R.pev.push_back({cls, a, b, c});
     }
-    const int e3 = tm.mark();
+    R.e3 = tm.mark(st);
 
     // ---- A10-A12: lengths, globals, EF, data, header in one output buffer ----------
     u64* len = A.alloc<u64>(B + 1);
@@ -1220,6 +1389,7 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     const uint64_t k = B + 1;
     const uint64_t cap_words = 9 + 2 * (3 + k + (3 * k) / 64 + 2) + (8 * n + 4096) / 64 + 16;
     unsigned long long* outw = A.alloc<unsigned long long>(cap_words);
+    R.outw = outw;
     CK(cudaMemsetAsync(outw, 0, cap_words * 8, st));
     const uint64_t flags = (p.rf ? 1u : 0u) | (p.strings ? 2u : 0u);
     const uint64_t hdr0 = (uint64_t)'R' | ((uint64_t)'S' << 8) | ((uint64_t)'R' << 16) | ((uint64_t)'F' << 24) |
@@ -1231,90 +1401,288 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
     CKL();
     launch_single_ef(C, Pbits, B, sd, outw, st);
     CKL();
-    const int e4 = tm.mark();
+    R.e4 = tm.mark(st);
 
     // ---- one D2H of the report and (most likely all of) the serialized MPHF -----
-    const auto key = std::make_tuple(n, leaf, p.bucket, p.rf, p.g);
-    uint64_t est_words;
+    const ConfigKey key{dev, n, leaf, p.bucket, p.rf, p.g, false, false};
     {
         std::lock_guard<std::mutex> g(g_est_mu);
         auto it = g_est_words.find(key);
         // first build of a configuration: about 2.5 bits per key plus the index
-        est_words = it == g_est_words.end() ? std::min<uint64_t>(cap_words, 64 + (5 * n / 2 + 24 * k) / 64)
-                                            : std::min<uint64_t>(cap_words, it->second + it->second / 64 + 64);
+        R.est_words = it == g_est_words.end() ? std::min<uint64_t>(cap_words, 64 + (5 * n / 2 + 24 * k) / 64)
+                                              : std::min<uint64_t>(cap_words, it->second + it->second / 64 + 64);
     }
-    std::lock_guard<std::mutex> lk_rep(g_report.mu);
     uint8_t* rep = g_report.get();
+    R.rep = rep;
     CK(cudaMemcpyAsync(rep, small, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(rep + 32, sd, sizeof(SingleDev), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(rep + 32 + sizeof(SingleDev), evals, 32, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(rep + 64 + sizeof(SingleDev), pcnt_d, NP * 4, cudaMemcpyDeviceToHost, st));
     if (exec_d) CK(cudaMemcpyAsync(rep + 2048, exec_d, 32, cudaMemcpyDeviceToHost, st));
     // the serialized MPHF goes straight into the caller's (pinned) result buffer
-    uint8_t* buf = pinned_get(est_words * 8);
+    R.buf = pinned_get(R.est_words * 8);
+    CK(cudaMemcpyAsync(R.buf, outw, R.est_words * 8, cudaMemcpyDeviceToHost, st));
+    if (capture) R.blob_node = last_node(st);
+    R.e5 = tm.mark(st);
+    return true;
+}
+
+// After the synchronization: flags, the rest of the result if the estimate was short, stats.
+// Returns false when the build must be redone on the synchronized path (a bucket above S).
+bool finish_single(const BuildParams& p, cudaStream_t st, SingleRun& R, Marks& tm, BuildOutput& out,
+                   std::chrono::steady_clock::time_point t_start) {
     struct BufGuard {
         uint8_t*& b;
         ~BufGuard() {
             if (b) pinned_release(b);
         }
-    } bg{buf};
-    CK(cudaMemcpyAsync(buf, outw, est_words * 8, cudaMemcpyDeviceToHost, st));
+    } bg{R.buf};
     CK(cudaStreamSynchronize(st));
+    const uint8_t* rep = R.rep;
     uint32_t fl[8];
     memcpy(fl, rep, 32);
     SingleDev sdh;
     memcpy(&sdh, rep + 32, sizeof sdh);
     unsigned long long ev_h[4];
     memcpy(ev_h, rep + 32 + sizeof(SingleDev), 32);
-    std::vector<uint32_t> pc(NP);
-    memcpy(pc.data(), rep + 64 + sizeof(SingleDev), NP * 4);
+    std::vector<uint32_t> pc(R.NP);
+    memcpy(pc.data(), rep + 64 + sizeof(SingleDev), R.NP * 4);
     if (fl[2] || fl[3] > 1) throw Error(RECSPLIT_E_DUPLICATE, "duplicate keys in the input");
     if (fl[4]) throw Error(RECSPLIT_E_SEED_CAP, "a node exceeded the 2^40 trial cap");
-    if (fl[5] || fl[0] > S || sdh.overflow) return false;  // rebuild on the synchronized path
-    if (sdh.total_words > est_words) {  // the estimate was short: a larger buffer, copy the rest
+    if (fl[5] || fl[0] > R.S || sdh.overflow) return false;  // rebuild on the synchronized path
+    if (sdh.total_words > R.est_words) {  // the estimate was short: a larger buffer, copy the rest
         uint8_t* big = pinned_get(sdh.total_words * 8);
-        memcpy(big, buf, est_words * 8);
-        pinned_release(buf);
-        buf = big;
-        CK(cudaMemcpyAsync(buf + est_words * 8, outw + est_words, (sdh.total_words - est_words) * 8,
+        memcpy(big, R.buf, R.est_words * 8);
+        pinned_release(R.buf);
+        R.buf = big;
+        CK(cudaMemcpyAsync(R.buf + R.est_words * 8, R.outw + R.est_words, (sdh.total_words - R.est_words) * 8,
                            cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
     {
         std::lock_guard<std::mutex> g(g_est_mu);
-        g_est_words[key] = sdh.total_words;
+        g_est_words[ConfigKey{dev, p.n, p.leaf, p.bucket, p.rf, p.g, false, false}] = sdh.total_words;
     }
-    out.raw = buf;
+    out.raw = R.buf;
     out.raw_size = sdh.total_words * 8;
-    buf = nullptr;  // owned by out now
+    R.buf = nullptr;  // owned by out now
     // statistics
-    Sst.t_partition = tm.secs(e0, e1);
-    Sst.t_tree = tm.secs(e1, e2);
-    for (const PhaseEv& x : pev) {
+    recsplit_stats& Sst = out.stats;
+    memset(&Sst, 0, sizeof Sst);
+    Sst.t_partition = tm.secs(R.e0, R.e1);
+    Sst.t_tree = tm.secs(R.e1, R.e2);
+    for (const PhaseEv& x : R.pev) {
         Sst.t_search[x.cls] += tm.secs(x.a, x.b);
         Sst.t_reorder += tm.secs(x.b, x.c);
     }
-    (void)e3;
-    Sst.t_encode = tm.secs(e3, e4);
-    if (tree) Sst.t_search_tree = tm.secs(et0, et1);
-    if (h2d_timed) {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, h2d_ev[0], h2d_ev[1]));
-        Sst.t_h2d = ms * 1e-3;  // the chunked copy (overlapped with hashing, inside t_partition)
-    }
-    for (uint32_t q = 0; q < NP; ++q) {
-        const int cls = q < T.n_upper ? 0 : q == T.phase_L2() ? 1 : q == T.phase_L1() ? 2 : 3;
-        Sst.nodes[cls] += pc[q];
-    }
+    Sst.t_encode = tm.secs(R.e3, R.e4);
+    Sst.t_device = tm.secs(R.e0, R.e5);
+    if (R.et0 >= 0) Sst.t_search_tree = tm.secs(R.et0, R.et1);
+    if (R.h0 >= 0) Sst.t_h2d = tm.secs(R.h0, R.h1);  // the chunked copy (overlapped with hashing, inside t_partition)
+    for (uint32_t q = 0; q < R.NP; ++q) Sst.nodes[R.phase_cls[q]] += pc[q];
     for (int c = 0; c < 4; ++c) Sst.algo_evals[c] = ev_h[c];
-    if (exec_d) memcpy(Sst.exec_evals, rep + 2048, 32);
+    if (R.exec_counted) memcpy(Sst.exec_evals, rep + 2048, 32);
     Sst.data_bits = sdh.D;
     Sst.index_bits = sdh.lowC + sdh.upC + sdh.lowP + sdh.upP;
     Sst.max_bucket = fl[0];
     Sst.kernel_launches = g_launches;
-    Sst.t_d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count() - tm.secs(e0, e4);
+    Sst.t_d2h = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count() - tm.secs(R.e0, R.e4);
     if (Sst.t_d2h < 0) Sst.t_d2h = 0;
     Sst.t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    return true;
+}
+
+// A captured build of one configuration over its own workspace.
+struct SinglePlan {
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaStream_t cap_st = nullptr, copy_st = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<cudaEvent_t> events;
+    SingleRun R;
+    uint32_t launches = 0;
+    uint64_t dt_gen = 0;
+    ~SinglePlan() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
+        if (cap_st) cudaStreamDestroy(cap_st);
+        if (copy_st) cudaStreamDestroy(copy_st);
+        if (ws) cudaFree(ws);
+        if (R.buf) pinned_release(R.buf);
+    }
+};
+
+std::mutex g_plan_mu;
+std::map<ConfigKey, std::unique_ptr<SinglePlan>> g_plans;
+constexpr uint64_t kGraphMaxKeys = 1ull << 27;  // larger builds are not launch-bound (workspace ~3 GB)
+constexpr size_t kMaxPlans = 4;
+
+bool graphs_enabled() {
+    static const int v = getenv("RS_GRAPH") ? atoi(getenv("RS_GRAPH")) : 1;
+    return v != 0;
+}
+
+// capture the configuration's build into a new plan (nullptr if the capture fails)
+std::unique_ptr<SinglePlan> capture_plan(const uint64_t* d_keys, const BuildParams& p, size_t ws_bytes) {
+    std::unique_ptr<SinglePlan> P(new SinglePlan);
+    const bool host = p.h_keys != nullptr;
+    P->ws_bytes = ws_bytes + (host ? ((p.n * 8 + 255) & ~(size_t)255) : 0) + (1u << 20);
+    CK(cudaMalloc(&P->ws, P->ws_bytes));
+    CK(cudaStreamCreateWithFlags(&P->cap_st, cudaStreamNonBlocking));
+    if (host) CK(cudaStreamCreateWithFlags(&P->copy_st, cudaStreamNonBlocking));
+    Alloc A;
+    A.base = (uint8_t*)P->ws;
+    A.cap = P->ws_bytes;
+    const uint64_t* keys = d_keys;
+    if (host) {
+        P->R.d_keys_ws = A.alloc<uint64_t>(p.n);
+        keys = P->R.d_keys_ws;
+    }
+    {  // the per-size tables must be current before the capture (an upload synchronizes)
+        const uint64_t B = (p.n + p.bucket - 1) / p.bucket;
+        const double avg = (double)p.n / (double)B;
+        const uint32_t S = (uint32_t)std::min<uint64_t>(p.n, (uint64_t)(avg + 8.0 * std::sqrt(avg) + 32.0));
+        std::vector<uint8_t> present(S + 1, 1);
+        present[0] = 0;
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        device_tables(dev, p.leaf, p.rf, S, present, P->cap_st);
+        CK(cudaStreamSynchronize(P->cap_st));
+    }
+    Marks tm;
+    tm.ev = &P->events;
+    tm.on = p.want_stats;
+    g_launches = 0;
+    CK(cudaStreamBeginCapture(P->cap_st, cudaStreamCaptureModeRelaxed));
+    bool ok = false;
+    try {
+        ok = enqueue_single(keys, p, P->cap_st, A, tm, P->R, true, P->copy_st);
+    } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(P->cap_st, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return nullptr;
+    }
+    P->launches = g_launches;
+    CK(cudaStreamEndCapture(P->cap_st, &P->graph));
+    if (!ok) return nullptr;
+    CK(cudaGraphInstantiate(&P->exec, P->graph, 0));
+    // the result buffer of the capture is not used by replays (each replay gets its own)
+    pinned_release(P->R.buf);
+    P->R.buf = nullptr;
+    return P;
+}
+
+// launch a plan for this build's keys; false if the replay must be redone uncaptured
+bool replay_plan(SinglePlan& P, const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out,
+                 std::chrono::steady_clock::time_point t_start) {
+    if (p.h_keys) {
+        for (size_t c = 0; c < P.R.h2d_nodes.size(); ++c)
+            CK(cudaGraphExecMemcpyNodeSetParams1D(P.exec, P.R.h2d_nodes[c], P.R.d_keys_ws + P.R.chunks[c].first,
+                                                  p.h_keys + P.R.chunks[c].first, P.R.chunks[c].second * 8,
+                                                  cudaMemcpyHostToDevice));
+    } else {
+        for (size_t c = 0; c < P.R.hash_nodes.size(); ++c) {
+            cudaKernelNodeParams kp{};
+            CK(cudaGraphKernelNodeGetParams(P.R.hash_nodes[c], &kp));
+            const uint64_t* src = d_keys + P.R.hash_off[c];
+            std::vector<void*> args(kp.kernelParams, kp.kernelParams + P.R.hash_argc[c]);
+            args[0] = (void*)&src;
+            kp.kernelParams = args.data();
+            CK(cudaGraphExecKernelNodeSetParams(P.exec, P.R.hash_nodes[c], &kp));
+        }
+    }
+    SingleRun R = P.R;  // (marks and layout; this replay's own result buffer)
+    R.buf = pinned_get(R.est_words * 8);
+    CK(cudaGraphExecMemcpyNodeSetParams1D(P.exec, R.blob_node, R.buf, R.outw, R.est_words * 8, cudaMemcpyDeviceToHost));
+    g_launches = P.launches;
+    CK(cudaGraphLaunch(P.exec, st));
+    Marks tm;
+    tm.ev = &P.events;
+    tm.on = p.want_stats;
+    if (!finish_single(p, st, R, tm, out, t_start)) return false;
+    out.stats.graph_replay = 1;
+    return true;
+}
+
+}  // namespace
+
+bool replay_host_keys(const uint64_t* h_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out) {
+    if (!graphs_enabled() || p.strings || p.shards > 1 || !p.cuts.empty() || p.n > kGraphMaxKeys) return false;
+    auto t_start = std::chrono::steady_clock::now();
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk_rep(g_report.mu);
+    std::lock_guard<std::mutex> g(g_plan_mu);
+    auto it = g_plans.find(ConfigKey{dev, p.n, p.leaf, p.bucket, p.rf, p.g, true, p.want_stats});
+    if (it == g_plans.end() || it->second->dt_gen != device_tables_generation(dev)) return false;
+    BuildParams q = p;
+    q.h_keys = h_keys;
+    if (replay_plan(*it->second, nullptr, q, st, out, t_start)) return true;
+    g_plans.erase(it);  // (a bucket above the table bound: the caller takes the general path)
+    return false;
+}
+
+bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out) {
+    auto t_start = std::chrono::steady_clock::now();
+    {  // eligibility (enqueue_single repeats it)
+        const uint64_t B = (p.n + p.bucket - 1) / p.bucket;
+        const double avg = (double)p.n / (double)B;
+        const uint64_t S = std::min<uint64_t>(p.n, (uint64_t)(avg + 8.0 * std::sqrt(avg) + 32.0));
+        if (S > kSmallBucketKeys || B >= (1ull << 31)) return false;
+    }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk_rep(g_report.mu);  // (one pinned report buffer)
+    const bool host = p.h_keys && !p.strings;
+    const ConfigKey key{dev, p.n, p.leaf, p.bucket, p.rf, p.g, host, p.want_stats};
+    const bool graph = graphs_enabled() && !p.strings && p.n <= kGraphMaxKeys;
+    if (graph) {
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it != g_plans.end() && it->second->dt_gen != device_tables_generation(dev)) g_plans.erase(it), it = g_plans.end();
+        if (it == g_plans.end()) {
+            size_t ws = 0;
+            {
+                std::lock_guard<std::mutex> g2(g_est_mu);
+                auto w = g_ws_bytes.find(key);
+                if (w != g_ws_bytes.end()) ws = w->second;
+            }
+            if (ws) {  // built before: capture now
+                std::unique_ptr<SinglePlan> P = capture_plan(d_keys, p, ws);
+                if (P) {
+                    P->dt_gen = device_tables_generation(dev);
+                    if (g_plans.size() >= kMaxPlans) g_plans.erase(g_plans.begin());
+                    it = g_plans.emplace(key, std::move(P)).first;
+                }
+            }
+        }
+        if (it != g_plans.end()) {
+            if (replay_plan(*it->second, d_keys, p, st, out, t_start)) return true;
+            g_plans.erase(it);
+            return false;  // (a bucket above S: the synchronized path)
+        }
+    }
+    g_launches = 0;
+    Arena arena(st);
+    Alloc A;
+    A.arena = &arena;
+    Timer timer(st);
+    Marks tm;
+    tm.tm = &timer;
+    tm.on = p.want_stats;
+    SingleRun R;
+    if (!enqueue_single(d_keys, p, st, A, tm, R, false, p.copy_stream)) return false;
+    if (!finish_single(p, st, R, tm, out, t_start)) return false;
+    if (graph) {
+        std::lock_guard<std::mutex> g(g_est_mu);
+        g_ws_bytes[key] = A.total;
+    }
     return true;
 }
 

@@ -37,6 +37,9 @@ struct BuildParams {
     // buffer; chunk c is copied on copy_stream while the hash kernel runs on chunk c - 1
     const uint64_t* h_keys = nullptr;
     cudaStream_t copy_stream = nullptr;
+    // per-phase CUDA-event timings in the stats (the caller asked for stats); without them the
+    // one-enqueue build records no timing events and queries none after the synchronization
+    bool want_stats = true;
 };
 
 // the library's stream-ordered memory pool on device dev (kept reserved between builds)
@@ -124,6 +127,10 @@ void launch_mhc_strings(const uint8_t* data, const uint64_t* off, uint64_t n, ui
 // work ordered on st.
 void build_on_device(const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, bool want_values,
                      BuildOutput& out);
+// Host (pinned) keys through a captured CUDA graph of the configuration that holds its own
+// device key buffer (no allocation, no copy stream of the caller's); false if no graph of
+// this configuration exists yet (the caller then takes the general path, which captures one).
+bool replay_host_keys(const uint64_t* h_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out);
 
 // Batched query on the device; d_keys / d_out device arrays of n.
 struct Parsed;

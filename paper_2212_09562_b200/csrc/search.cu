@@ -22,6 +22,9 @@
 //    and searches each alone, windows in increasing order, first hit wins.
 #include <cstdlib>
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "kernels.h"
 
@@ -68,6 +71,8 @@ struct Args {
     u32 qwords;    // early-rejection queue words per warp (0 for the plain variants)
     unsigned long long* exec;  // RS_COUNT_EVALS builds: executed evaluations of this phase's class
     u32 lane_fit;  // leaves up to this size check rotations lane by lane (fit_rotation_lane)
+    const u8* fit_lut;  // rotation-fit table for leaves of <= kFitLutMax keys (fit_lut_device), null = off
+    u32 lean;           // batch mode: lean windows (lean_windows) while on the no-carry path
 };
 
 // Bucket-tree kernel (k_bucket_tree): buckets, their per-size preorder templates, slots.
@@ -387,7 +392,24 @@ __device__ __forceinline__ bool fit_rotation_lane(u32 a, u32 b, u32 m, u32 full,
     return r >= 0;
 }
 
-__device__ __forceinline__ bool fit_rotation(u32 a, u32 b, u32 m, u32 full, u32 lane, int& r, u32 lane_fit_max) {
+// The same test as one table load for leaves of m <= kFitLutMax keys: fit_lut[off(m) + (b << m | a)]
+// holds the smallest r in [0, m) with rot_m^r(b) = ~a & (2^m - 1) -- the r fit_rotation_lane finds --
+// or 0xff (no fit; this covers masks with a collision, whose complement cannot be a rotation
+// of b).  off(m) = (4^m - 4) / 3, 87,380 bytes for m = 1..8, read through the L1 cache.  At
+// l = 8 the serial rotation loop was 16 % of the leaf kernel's instructions and 30 % of its
+// stall samples (ncu, profiles/ncu_summary_r02.md).
+constexpr u32 kFitLutMax = 8;
+__host__ __device__ constexpr u32 fit_lut_off(u32 m) { return ((1u << (2 * m)) - 4u) / 3u; }
+
+__device__ __forceinline__ bool fit_rotation_lut(u32 a, u32 b, u32 m, const u8* __restrict__ lut, int& r) {
+    const u32 v = __ldg(lut + ((b << m) | a));
+    r = (int)v;
+    return v != 0xffu;
+}
+
+__device__ __forceinline__ bool fit_rotation(u32 a, u32 b, u32 m, u32 full, u32 lane, int& r, u32 lane_fit_max,
+                                             const u8* lut = nullptr) {
+    if (lut) return fit_rotation_lut(a, b, m, lut, r);
     return m <= lane_fit_max ? fit_rotation_lane(a, b, m, full, r) : fit_rotation_warp(a, b, m, full, lane, r);
 }
 
@@ -401,6 +423,9 @@ struct NodeCtx {
     u32 cp2; // second checkpoint (key groups), 0 = single stage
     u64 kW;  // key rebase: the buffered keys are lo + kW (values are tried relative to kW)
     u32 lane_fit;  // leaves: lane-by-lane rotation check up to this m (fit_rotation)
+    const u8* lut; // leaves of m <= kFitLutMax (rotation fitting): the table slice of m, else null
+    u32 nc_end;    // lean windows (batch mode, kW = 0): windows ending at or below this base value
+                   // (seed index units) stay on the no-carry path without a rebase
 };
 
 
@@ -412,7 +437,7 @@ __device__ __forceinline__ bool trial_fast(const KeysView& K, const NodeCtx& c, 
         u32 a, b;
         leaf_masks<MODE>(K, (c.s + 3) >> 2, c.s, base, a, b);
         if (KIND == SK_LEAF_BF) return a == c.full;
-        return fit_rotation(a, b, c.s, c.full, lane, r, c.lane_fit);
+        return fit_rotation(a, b, c.s, c.full, lane, r, c.lane_fit, c.lut);
     } else if (KIND == SK_UPPER) {
         return count_left<MODE>(K, c.s, sig, c.mask) == c.target;
     } else {
@@ -443,7 +468,7 @@ __device__ __forceinline__ bool trial_slow(const KeysView& K, const NodeCtx& c, 
             b |= bit & key_word<GW>(K, j, 4);
         }
         if (KIND == SK_LEAF_BF) return a == c.full;
-        return fit_rotation(a, b, s, c.full, lane, r, c.lane_fit);
+        return fit_rotation(a, b, s, c.full, lane, r, c.lane_fit, c.lut);
     } else if (KIND == SK_UPPER) {
         u32 cnt = 0;
         for (u32 j = 0; j < s; ++j) cnt += hash_slow<GW>(K, j, idx) < c.mask;
@@ -517,6 +542,7 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
         c.cp2 = c.cp && A.cp_leaf2 && s >= 14 ? c.cp + 1 : 0u;
         c.kW = 0;
         c.lane_fit = A.lane_fit;
+        c.lut = KIND == SK_LEAF_RF && A.fit_lut && s <= kFitLutMax ? A.fit_lut + fit_lut_off(s) : nullptr;
     } else {
         for (u32 j = lane; j < s; j += 32) {
             const u64 k = src_lo[rec.key_off + j];
@@ -577,6 +603,9 @@ __device__ __forceinline__ void load_node(const Args& A, u32 n, u32 lane, u32* G
     for (int d = 16; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
     c.margin = mg;
     c.kW = 0;
+    // a window [w, w + ws) of base values is on the no-carry path iff (w + ws) * sc - 1 <= margin
+    // (sc = m value units per rotation-fitting base seed)
+    c.nc_end = KIND == SK_LEAF_RF ? mg / s : mg;  // (floor(margin / sc) <= the exact bound)
     __syncwarp();
 }
 
@@ -776,7 +805,7 @@ __device__ __forceinline__ bool run_window_leaf_cp(const Args& A, const KeysView
         leaf_masks<0>(K, ng, c.s, base_of(sig), a, b, gf, a, b);
         if (!have) a = b = 0;  // no entry: cannot fit (m >= 10 keys)
         int r = 0;
-        const bool ok = KIND == SK_LEAF_BF ? a == c.full : fit_rotation(a, b, c.s, c.full, lane, r, c.lane_fit);
+        const bool ok = KIND == SK_LEAF_BF ? a == c.full : fit_rotation(a, b, c.s, c.full, lane, r, c.lane_fit, c.lut);
         const u32 bal = __ballot_sync(FULL, ok);
         if (bal) {
             const int win = __ffs(bal) - 1;
@@ -989,6 +1018,39 @@ __device__ __forceinline__ bool run_window(const Args& A, const KeysView& K, Nod
     return false;
 }
 
+// Lean windows (batch mode, a node's first windows): while the window's base values stay
+// within the node's carry margin (c.nc_end, key rebase 0) every trial takes the no-carry path,
+// so the per-window checks of run_window (64-bit margin and rebase arithmetic, kernel-variant
+// dispatch) reduce to one 32-bit compare.  Same trials in the same order as run_window's plain
+// loop: the first window with a hit gives the lowest lane (seed) with a hit, the minimal value.
+// Returns false with wstart = the first window not searched (the caller continues there).
+template <int KIND, int VAR>
+__device__ __forceinline__ bool lean_windows(const Args& A, const KeysView& K, const NodeCtx& c, u32 lane, u32 ws,
+                                             u64* val, u64& wstart) {
+    u32 w = 0;
+    if (c.nc_end >= ws) {
+        const u32 wlast = c.nc_end - ws;  // largest window start on the no-carry path (w + ws never wraps)
+#pragma unroll 1
+        for (; w <= wlast; w += ws) {
+#pragma unroll 1
+            for (u32 it = 0; it < A.iters; ++it) {
+                int r = 0;
+                const bool ok = trial_fast<KIND, 0, VAR == V_WIDE>(K, c, w + it * 32 + lane, lane, r);
+                const u32 bal = __ballot_sync(FULL, ok);
+                if (bal) {
+                    const int win = __ffs(bal) - 1;
+                    u64 v = (u64)w + it * 32 + win;
+                    if (KIND == SK_LEAF_RF) v = v * c.s + (u32)__shfl_sync(FULL, r, win);
+                    *val = v;
+                    return true;
+                }
+            }
+        }
+    }
+    wstart = w;
+    return false;
+}
+
 // A7 fused into the batch-mode split search: the warp that found the node's seed still holds
 // its keys (shared memory, natural order, possibly rebased by kW) and writes them in child
 // order -- the stable partition of reorder_node, without a separate pass over the keys.  The
@@ -1058,7 +1120,38 @@ __device__ __forceinline__ void fused_reorder(const Args& A, const u32* G, u32 k
 __device__ __forceinline__ u64 upper_keys_parallel(const Args& A, const u32* G, const NodeCtx& c, u32 lane) {
     constexpr u32 GW = Layout<SK_UPPER>::GW;
     const u32 s = c.s;
-    for (u64 sigma = 0; sigma < kSeedCap; ++sigma) {
+    // No-carry fast path (remix_hi_nc) while sigma <= the node's carry margin
+    // (k_lo + sigma < 2^32 for every key; the buffered keys are not rebased here): the lane's
+    // keys (<= kUpperKpMax / 32) in registers, all their hashes of one seed issued before the
+    // ballots (independent chains).
+    constexpr u32 kCh = kUpperKpMax / 32;
+    u32 kl[kCh], kh[kCh], kc[kCh];
+#pragma unroll
+    for (u32 q = 0; q < kCh; ++q) {
+        const u32 j = q * 32 + lane;
+        const u32* g = G + GW * (j >> 2) + (j & 3);
+        const bool v = j < s;
+        kl[q] = v ? g[0] : 0;
+        kh[q] = v ? g[4] : 0;
+        kc[q] = v ? g[8] : 0;
+    }
+    const u32 nch = (s + 31) >> 5;
+    for (u32 sigma = 0; sigma <= c.margin; ++sigma) {
+        u32 left = 0;
+#pragma unroll
+        for (u32 q = 0; q < kCh; ++q)
+            if (q < nch) {
+                RS_COUNT(1);
+                left |= (u32)(q * 32 + lane < s && remix_hi_nc(kl[q], kh[q], kc[q], sigma) < c.mask) << q;
+            }
+        u32 cnt = 0;
+#pragma unroll
+        for (u32 q = 0; q < kCh; ++q)
+            if (q < nch) cnt += __popc(__ballot_sync(FULL, (left >> q) & 1u));
+        if (cnt == c.target) return sigma;
+        if (sigma == 0xffffffffu) break;
+    }
+    for (u64 sigma = (u64)c.margin + 1; sigma < kSeedCap; ++sigma) {
         u32 cnt = 0;
         for (u32 j0 = 0; j0 < s; j0 += 32) {
             RS_COUNT(1);
@@ -1213,14 +1306,19 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32,
                 u64 val = 0;
                 if (KIND == SK_UPPER && A.upper_kp && c.s <= kUpperKpMax) {
                     val = upper_keys_parallel(A, G, c, lane);
-                } else
-                for (u64 wstart = 0;; wstart += ws) {
-                    if (wstart >= kSeedCap) {
-                        if (lane == 0) atomicOr(A.err, 1u);
-                        val = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
-                        break;
-                    }
-                    if (run_window<KIND, VAR>(A, K, c, wstart, lane, &val, QS, QC)) break;
+                } else {
+                    u64 wstart = 0;
+                    // (nodes that run_window sends to an early-rejection variant keep it)
+                    const bool lean = A.lean && (VAR == V_PLAIN || !c.cp);
+                    if (!(lean && lean_windows<KIND, VAR>(A, K, c, lane, (u32)ws, &val, wstart)))
+                        for (;; wstart += ws) {
+                            if (wstart >= kSeedCap) {
+                                if (lane == 0) atomicOr(A.err, 1u);
+                                val = KIND == SK_LEAF_RF ? wstart * c.s : wstart;
+                                break;
+                            }
+                            if (run_window<KIND, VAR>(A, K, c, wstart, lane, &val, QS, QC)) break;
+                        }
                 }
                 if (lane == 0) A.values[c.slot] = val;
                 if ((KIND == SK_UPPER || KIND == SK_LOWER) && A.lo_w)
@@ -1419,7 +1517,9 @@ __global__ void __launch_bounds__(128) k_leaf_sub(const Args A) {
             }
         }
         int r = -1;
-        const bool ok = busy && (KIND == SK_LEAF_BF ? (a == full && (r = 0) == 0) : fit_rotation_lane(a, b, m, full, r));
+        const bool ok = busy && (KIND == SK_LEAF_BF ? (a == full && (r = 0) == 0)
+                                 : A.fit_lut ? fit_rotation_lut(a, b, m, A.fit_lut + fit_lut_off(m), r)
+                                             : fit_rotation_lane(a, b, m, full, r));
         const u32 bal = __ballot_sync(FULL, ok);
         const u32 mine = (bal >> (sub * 8)) & 0xffu;
         const int rw = __shfl_sync(FULL, r, (int)(sub * 8) + (mine ? __ffs(mine) - 1 : 0));
@@ -1454,9 +1554,50 @@ void launch_kind(const PhaseLaunch& P, const Args& A, u32 wpb, size_t smem, u32 
 
 u32 search_active_slots(int sm_count) { return (u32)sm_count * 16u * kWarpsPerBlockMax; }
 
+// The rotation-fit table of fit_rotation_lut (kFitLutMax = 8: 87,380 bytes), built on the host
+// from the definition rot_m^r(b) = (bb >> (m - r)) & full, bb = b | b << m (the same test as
+// fit_rotation_lane), uploaded once per device.
+const u8* fit_lut_device() {
+    static std::mutex mu;
+    static std::map<int, u8*> tabs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = tabs.find(dev);
+    if (it != tabs.end()) return it->second;
+    std::vector<u8> t(fit_lut_off(kFitLutMax + 1), 0xff);
+    for (u32 m = 1; m <= kFitLutMax; ++m) {
+        const u32 full = (1u << m) - 1u;
+        for (u32 b = 0; b <= full; ++b) {
+            const u64 bb = (u64)b | ((u64)b << m);
+            for (u32 a = 0; a <= full; ++a) {
+                const u32 na = ~a & full;
+                u8 r = 0xff;
+                for (u32 q = 0; q < m; ++q)
+                    if (((u32)(bb >> (m - q)) & full) == na) {
+                        r = (u8)q;
+                        break;
+                    }
+                t[fit_lut_off(m) + ((b << m) | a)] = r;
+            }
+        }
+    }
+    u8* d = nullptr;
+    if (cudaMalloc(&d, t.size()) != cudaSuccess || cudaMemcpy(d, t.data(), t.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;  // (the serial rotation check then runs)
+    }
+    tabs[dev] = d;
+    return d;
+}
+
 bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     if (P.n_nodes_host == 0) return false;
-    Args A;
+    Args A{};
+    static const int lut_env = getenv("RS_FIT_LUT") ? atoi(getenv("RS_FIT_LUT")) : 1;
+    A.fit_lut = lut_env && P.kind == SK_LEAF_RF ? fit_lut_device() : nullptr;
+    static const int lean_env = getenv("RS_LEAN") ? atoi(getenv("RS_LEAN")) : 1;
+    A.lean = lean_env ? 1u : 0u;
     A.nodes = P.nodes;
     A.n_nodes = P.n_nodes;
     A.lo = P.lo;

@@ -735,3 +735,63 @@ def test_early_rejection_checkpoints_do_not_change_output(cp):
     want = [hashlib.sha256(oracle.build(synth.keys(n, 1000 * leaf + b), leaf, b, threads=os.cpu_count()))
             .hexdigest() for leaf, b, n in cases]
     assert out == want
+
+
+_GRAPH_SNIPPET = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2212_09562_b200 as rs, oracle, synth
+def want(k, leaf, b):
+    return oracle.build(k, leaf, b, threads=8)
+def dev(k):
+    return torch.from_numpy(k.view(np.int64).copy()).cuda()
+def pinned(k):
+    t = torch.from_numpy(k.view(np.int64).copy()).pin_memory()
+    return t, t.numpy().view(np.uint64)
+n, leaf, b = 30000, 8, 100
+k1, k2 = synth.keys(n, 501), synth.keys(n, 502)
+w1, w2 = want(k1, leaf, b), want(k2, leaf, b)
+d1, d2 = dev(k1), dev(k2)
+for i in range(4):  # uncaptured, capture + replay, replays
+    blob, st = rs.build_device(d1, leaf, b, stats=True)
+    assert blob == w1, ("device replay", i)
+    assert st["t_search"][2] > 0 and st["kernel_launches"] > 10, st
+assert rs.build_device(d2, leaf, b) == w2, "replay with other device keys"
+assert rs.build_device(d1, leaf, b) == w1
+# host (pinned) keys: the chunked H2D is part of the graph; sources updated per replay
+t1, p1 = pinned(k1)
+t2, p2 = pinned(k2)
+for i in range(3):
+    assert rs.build(p1, leaf, b) == w1, ("host replay", i)
+assert rs.build(p2, leaf, b) == w2, "host replay with other keys"
+# another configuration in between (different per-size tables): the plan is recaptured
+k3 = synth.keys(20000, 503)
+for i in range(3):
+    assert rs.build_device(dev(k3), 12, 300) == want(k3, 12, 300), ("other config", i)
+assert rs.build_device(d1, leaf, b) == w1, "after table change"
+assert rs.build_device(d2, leaf, b) == w2
+# a duplicate inside a replay, then a clean replay
+kd = k2.copy(); kd[7] = kd[20000]
+try:
+    rs.build_device(dev(kd), leaf, b)
+    raise SystemExit("duplicate not detected")
+except rs.RecSplitError as e:
+    assert e.code == rs.E_DUPLICATE
+assert rs.build_device(d1, leaf, b) == w1, "after duplicate"
+print("ok")
+"""
+
+
+def test_graph_replay_bytes():
+    """CUDA-graph replay of the one-enqueue build (pipeline.cu, RS_GRAPH default on): the
+    first build of a configuration runs uncaptured, the second captures, later ones replay
+    with the key source patched into the graph.  Every replay gives the oracle's bytes for
+    ITS keys (device keys and pinned host keys, other key sets of the same configuration,
+    after another configuration replaced the per-size tables, after a duplicate-key
+    rejection)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _GRAPH_SNIPPET.format(root=root)], env=dict(os.environ, RS_GRAPH="1"),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
