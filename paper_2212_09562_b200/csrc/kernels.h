@@ -38,25 +38,25 @@ void launch_dedupe(const u64* lo, const u64* C, u64 nb, u32 smax, u32* dup, u64*
 void launch_bucket_stats(const u32* hist, u64 B, u32* maxmin /*[2]*/, u32* size_hist, u32 cap,
                          cudaStream_t st);
 // Two-level counting sort (one-enqueue builds): groups of 2^gl consecutive buckets of at most
-// kGroupCap keys; level 0 counts per group (gcount zeroed), a scan gives the group starts
-// (gstart, G + 1 entries) and a copy of them the level-1 cursors; level 1 scatters (lo, meta) by
-// group, level 2 sorts each group by bucket in shared memory, writes lo_a / ab_a in bucket order,
-// C[0..B] and small[0] / small[1] (max / min bucket size); small[5] |= 1 if a group overflows.
+// kGroupCap keys, level-1 blocks of `chunk` keys.  Level 0 counts per (group, block) into M
+// (G x nb1, group-major); an exclusive scan of M gives Ms (G * nb1 + 1 entries: group g starts at
+// Ms[g * nb1]); level 1 scatters the keys to the blocks' ranges; level 2 sorts each group by
+// bucket in shared memory (master hash codes recomputed), writes lo_a / ab_a in bucket order, C[0..B] and small[0] / small[1]
+// (max / min bucket size); small[5] |= 1 if a group overflows.
 constexpr u32 kGroupCap = 12288;
-constexpr u32 kGroupMax = 16384;
+constexpr u32 kGroupMax = 4096;
 struct P2Shape {
-    u32 gl = 0, G = 0, cap = 0;
+    u32 gl = 0, G = 0, cap = 0, nb1 = 0;
     u64 chunk = 0;  // keys per level-1 block
 };
 bool partition2_shape(u64 n, u64 B, u32 S, P2Shape& sh);
-void launch_p2_count(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, unsigned long long* gcount,
-                     cudaStream_t st);
-void launch_p2_scatter(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, unsigned long long* gcursor, u64* lo1,
-                       u16* meta1, cudaStream_t st);
-void launch_p2_group(u64 B, const P2Shape& sh, const unsigned long long* gstart, const u64* lo1, const u16* meta1,
-                     u64* C, u64* lo_a, u8* ab_a, u32* small, cudaStream_t st);
+void launch_p2_count(const u64* keys, u64 n, u64 first_key, u64 g, u64 B, const P2Shape& sh, u32* M, cudaStream_t st);
+void launch_p2_scatter(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, const u64* Ms, u64* key1,
+                       cudaStream_t st);
+void launch_p2_group(const u64* key1, u64 g, u64 B, const P2Shape& sh, const u64* Ms, u64* C, u64* lo_a, u8* ab_a,
+                     u32* small, cudaStream_t st);
 // parameter counts of the kernels that read the keys (graph replays patch parameter 0, the keys)
-constexpr int kHashParams = 12, kP2CountParams = 7, kP2ScatterParams = 10;
+constexpr int kHashParams = 12, kP2CountParams = 10, kP2ScatterParams = 10;
 // scatter (lo, ab) to bucket order (cursor = copy of exclusive offsets)
 void launch_scatter(const u64* lo, const u8* ab, const u32* bkt, u64 n, u64* cursor, u64* lo2,
                     u8* ab2, cudaStream_t st);

@@ -436,40 +436,46 @@ __device__ __forceinline__ u64 bucket_of(u64 key, u64 g, u64 B) {
     return ((remix64(key ^ g ^ MHC_SALT_HI) >> 32) * B) >> 32;
 }
 
+// level 0: block blk counts the keys of its chunk [blk0 + blk) * chunk ... per group into
+// M[g * nb1 + blk] (group-major, so that one exclusive scan of M gives every (group, block)
+// its output offset: no atomics on global memory)
 __global__ void __launch_bounds__(1024) k_p2_count(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 gl, u32 G,
-                                                   unsigned long long* __restrict__ gcount) {
+                                                   u64 chunk, u32 nb1, u32 blk0, u32* __restrict__ M) {
     extern __shared__ u32 hc[];
+    const u32 blk = blk0 + blockIdx.x;
+    const u64 k0 = (u64)blockIdx.x * chunk, k1 = min(n, k0 + chunk);  // (keys: this launch's first key)
     for (u32 i = threadIdx.x; i < G; i += blockDim.x) hc[i] = 0;
     __syncthreads();
-    for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
-        atomicAdd(hc + (u32)(bucket_of(keys[i], g, B) >> gl), 1u);
-    __syncthreads();
-    for (u32 i = threadIdx.x; i < G; i += blockDim.x)
-        if (hc[i]) atomicAdd(gcount + i, (unsigned long long)hc[i]);
-}
-
-// gcursor: the groups' start offsets (advanced); chunk = keys per block
-__global__ void __launch_bounds__(1024) k_p2_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 gl,
-                                                     u32 G, u64 chunk, unsigned long long* __restrict__ gcursor,
-                                                     u64* __restrict__ lo1, u16* __restrict__ meta1) {
-    extern __shared__ u32 sc[];  // per group: count, then write cursor
-    const u64 k0 = (u64)blockIdx.x * chunk, k1 = min(n, k0 + chunk);
-    for (u32 i = threadIdx.x; i < G; i += blockDim.x) sc[i] = 0;
-    __syncthreads();
-    for (u64 i = k0 + threadIdx.x; i < k1; i += blockDim.x) atomicAdd(sc + (u32)(bucket_of(keys[i], g, B) >> gl), 1u);
-    __syncthreads();
-    for (u32 i = threadIdx.x; i < G; i += blockDim.x) {
-        const u32 c = sc[i];
-        sc[i] = c ? (u32)atomicAdd(gcursor + i, (unsigned long long)c) : 0u;  // (n < 2^32)
+    // (four keys in flight per thread: the loads are issued before the hashes and atomics)
+    for (u64 i = k0 + threadIdx.x; i < k1; i += 4 * blockDim.x) {
+        u64 kk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kk[q] = i + q * blockDim.x < k1 ? keys[i + q * blockDim.x] : 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (i + q * blockDim.x < k1) atomicAdd(hc + (u32)(bucket_of(kk[q], g, B) >> gl), 1u);
     }
     __syncthreads();
-    for (u64 i = k0 + threadIdx.x; i < k1; i += blockDim.x) {
-        const u64 k = keys[i] ^ g;
-        const u64 h = remix64(k ^ MHC_SALT_HI);
-        const u64 b = ((h >> 32) * B) >> 32;
-        const u32 pos = atomicAdd(sc + (u32)(b >> gl), 1u);
-        lo1[pos] = remix64(k ^ MHC_SALT_LO);
-        meta1[pos] = (u16)((b & ((1u << gl) - 1u)) | ((h & 1) << 8));
+    for (u32 i = threadIdx.x; i < G; i += blockDim.x) M[(u64)i * nb1 + blk] = hc[i];
+}
+
+// level 1: block blk writes its chunk's keys at the scanned offsets Ms[g * nb1 + blk] of their
+// groups (the raw key: one 8-byte write per key; level 2 recomputes its master hash code)
+__global__ void __launch_bounds__(1024) k_p2_scatter(const u64* __restrict__ keys, u64 n, u64 g, u64 B, u32 gl,
+                                                     u32 G, u64 chunk, u32 nb1, const u64* __restrict__ Ms,
+                                                     u64* __restrict__ key1) {
+    extern __shared__ u32 sc[];  // per group: this block's write cursor
+    const u32 blk = blockIdx.x;
+    const u64 k0 = (u64)blk * chunk, k1 = min(n, k0 + chunk);
+    for (u32 i = threadIdx.x; i < G; i += blockDim.x) sc[i] = (u32)Ms[(u64)i * nb1 + blk];  // (n < 2^32)
+    __syncthreads();
+    for (u64 i = k0 + threadIdx.x; i < k1; i += 4 * blockDim.x) {
+        u64 kk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) kk[q] = i + q * blockDim.x < k1 ? keys[i + q * blockDim.x] : 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)  // (one 8-byte write per key)
+            if (i + q * blockDim.x < k1) key1[atomicAdd(sc + (u32)(bucket_of(kk[q], g, B) >> gl), 1u)] = kk[q];
     }
 }
 
@@ -477,10 +483,9 @@ __global__ void __launch_bounds__(1024) k_p2_scatter(const u64* __restrict__ key
 // max / min bucket size (small[0], small[1]); a group above cap keys (a bucket above the
 // build's bound S) sets small[5] and leaves its buckets empty (the build is redone on the
 // synchronized path)
-__global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ lo1, const u16* __restrict__ meta1,
-                                                  const unsigned long long* __restrict__ gstart, u64 B, u32 gl, u32 G,
-                                                  u32 cap, u64* __restrict__ C, u64* __restrict__ lo_a,
-                                                  u8* __restrict__ ab_a, u32* small) {
+__global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ key1, u64 g, const u64* __restrict__ Ms,
+                                                  u32 nb1, u64 B, u32 gl, u32 G, u32 cap, u64* __restrict__ C,
+                                                  u64* __restrict__ lo_a, u8* __restrict__ ab_a, u32* small) {
     extern __shared__ __align__(16) unsigned char p2s[];
     const u32 gb = 1u << gl;
     u32* cnt = reinterpret_cast<u32*>(p2s);  // gb counts -> exclusive offsets
@@ -488,7 +493,7 @@ __global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ lo1, c
     u64* lo_s = reinterpret_cast<u64*>(p2s + ((8u * gb + 15u) & ~15u));
     u8* ab_s = reinterpret_cast<u8*>(lo_s + cap);
     for (u32 grp = blockIdx.x; grp < G; grp += gridDim.x) {
-        const u64 gs = gstart[grp], ge = gstart[grp + 1];
+        const u64 gs = Ms[(u64)grp * nb1], ge = Ms[(u64)(grp + 1) * nb1];  // (Ms[G * nb1] = n)
         const u64 b0 = (u64)grp << gl;
         const u32 nb = (u32)min((u64)gb, B - b0);
         const u32 cg = (u32)(ge - gs);
@@ -501,7 +506,12 @@ __global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ lo1, c
         }
         for (u32 j = threadIdx.x; j < gb; j += blockDim.x) cnt[j] = 0;
         __syncthreads();
-        for (u32 i = threadIdx.x; i < cg; i += blockDim.x) atomicAdd(cnt + (meta1[gs + i] & 0xffu), 1u);
+        const u32 lmask = gb - 1u;
+        for (u32 i = threadIdx.x; i < cg; i += 2 * blockDim.x) {
+            const u64 ka = key1[gs + i], kb = i + blockDim.x < cg ? key1[gs + i + blockDim.x] : 0;
+            atomicAdd(cnt + ((u32)bucket_of(ka, g, B) & lmask), 1u);
+            if (i + blockDim.x < cg) atomicAdd(cnt + ((u32)bucket_of(kb, g, B) & lmask), 1u);
+        }
         __syncthreads();
         if (threadIdx.x < 32) {  // exclusive scan of gb <= 256 counts by one warp; sizes' max / min
             const u32 lane = threadIdx.x;
@@ -535,11 +545,12 @@ __global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ lo1, c
         }
         __syncthreads();
         for (u32 j = threadIdx.x; j < nb; j += blockDim.x) C[b0 + j] = gs + cnt[j];
-        for (u32 i = threadIdx.x; i < cg; i += blockDim.x) {
-            const u32 m = meta1[gs + i];
-            const u32 pos = atomicAdd(cur + (m & 0xffu), 1u);
-            lo_s[pos] = lo1[gs + i];
-            ab_s[pos] = (u8)(m >> 8);
+        for (u32 i = threadIdx.x; i < cg; i += blockDim.x) {  // A1: lo, A/B bit (R2, R7)
+            const u64 k = key1[gs + i] ^ g;
+            const u64 h = remix64(k ^ MHC_SALT_HI);
+            const u32 pos = atomicAdd(cur + ((u32)(((h >> 32) * B) >> 32) & lmask), 1u);
+            lo_s[pos] = remix64(k ^ MHC_SALT_LO);
+            ab_s[pos] = (u8)(h & 1);
         }
         __syncthreads();
         for (u32 i = threadIdx.x; i < cg; i += blockDim.x) {
@@ -556,41 +567,44 @@ bool partition2_shape(u64 n, u64 B, u32 S, P2Shape& sh) {
     u32 gl = 0;
     while (gl < 8 && (2ull << gl) * S <= kGroupCap) ++gl;
     const u64 G = (B + (1ull << gl) - 1) >> gl;
+    // (many groups: the (group, block) count matrix and the level-1 blocks' short runs per
+    // group cost more than the one-level scatter -- C5, G = 12,500: 6.0 vs 4.9 ms, pass W)
     if (G > kGroupMax) return false;
     sh.gl = gl;
     sh.G = (u32)G;
     sh.cap = (u32)std::min<u64>(kGroupCap, (u64)S << gl);
-    // keys per level-1 block: about 4 blocks per SM, at least 8 keys per group per block
-    sh.chunk = std::max<u64>(std::max<u64>(4096, 8ull * G), (n + 148 * 4 - 1) / (148 * 4));
-    sh.chunk = (sh.chunk + 1023) & ~1023ull;
+    // keys per level-1 block: about 4 blocks per SM (592), at least 8192
+    sh.chunk = std::max<u64>(8192, ((n + 591) / 592 + 1023) & ~1023ull);
+    sh.nb1 = (u32)((n + sh.chunk - 1) / sh.chunk);
+    if ((u64)sh.G * sh.nb1 > (1ull << 28)) return false;
     return true;
 }
 
-void launch_p2_count(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, unsigned long long* gcount,
-                     cudaStream_t st) {
+void launch_p2_count(const u64* keys, u64 n, u64 first_key, u64 g, u64 B, const P2Shape& sh, u32* M, cudaStream_t st) {
     if (!n) return;
-    const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>((n + 4095) / 4096, 148ull * 2));
+    // (first_key: a multiple of the chunk -- the chunked host->device copy hands over whole chunks)
+    const u32 blk0 = (u32)(first_key / sh.chunk);
+    const unsigned grid = (unsigned)((n + sh.chunk - 1) / sh.chunk);
     cudaFuncSetAttribute(k_p2_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    k_p2_count<<<grid, 1024, (size_t)sh.G * 4, st>>>(keys, n, g, B, sh.gl, sh.G, gcount);
+    k_p2_count<<<grid, 1024, (size_t)sh.G * 4, st>>>(keys, n, g, B, sh.gl, sh.G, sh.chunk, sh.nb1, blk0, M);
     g_launches++;
 }
 
-void launch_p2_scatter(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, unsigned long long* gcursor, u64* lo1,
-                       u16* meta1, cudaStream_t st) {
-    const unsigned nb1 = (unsigned)((n + sh.chunk - 1) / sh.chunk);
+void launch_p2_scatter(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, const u64* Ms, u64* key1,
+                       cudaStream_t st) {
     cudaFuncSetAttribute(k_p2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    k_p2_scatter<<<nb1, 1024, (size_t)sh.G * 4, st>>>(keys, n, g, B, sh.gl, sh.G, sh.chunk, gcursor, lo1, meta1);
+    k_p2_scatter<<<sh.nb1, 1024, (size_t)sh.G * 4, st>>>(keys, n, g, B, sh.gl, sh.G, sh.chunk, sh.nb1, Ms, key1);
     g_launches++;
 }
 
-void launch_p2_group(u64 B, const P2Shape& sh, const unsigned long long* gstart, const u64* lo1, const u16* meta1,
-                     u64* C, u64* lo_a, u8* ab_a, u32* small, cudaStream_t st) {
+void launch_p2_group(const u64* key1, u64 g, u64 B, const P2Shape& sh, const u64* Ms, u64* C, u64* lo_a, u8* ab_a,
+                     u32* small, cudaStream_t st) {
     const size_t smem = ((8u * (1u << sh.gl) + 15u) & ~15u) + (size_t)sh.cap * 9;
     cudaFuncSetAttribute(k_p2_group, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2_group, 512, smem);
     const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>(sh.G, 148ull * std::max(occ, 1)));
-    k_p2_group<<<grid, 512, smem, st>>>(lo1, meta1, gstart, B, sh.gl, sh.G, sh.cap, C, lo_a, ab_a, small);
+    k_p2_group<<<grid, 512, smem, st>>>(key1, g, Ms, sh.nb1, B, sh.gl, sh.G, sh.cap, C, lo_a, ab_a, small);
     g_launches++;
 }
 

@@ -1120,12 +1120,13 @@ bool enqueue_single(const uint64_t* d_keys, const BuildParams& p, cudaStream_t s
     const bool two = p2_env && !p.strings && partition2_shape(n, B, S, p2);
     u64* lo_a = nullptr;
     u8* ab_a = nullptr;
-    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(B, two ? p2.G : 0) + 1) + 64);
+    void* scan_tmp = A.alloc<u8>(scan_temp_bytes(std::max<uint64_t>(B, two ? (uint64_t)p2.G * p2.nb1 : 0) + 1) + 64);
     // the key source: device keys, or pinned host keys copied in chunks on the copy stream with
     // `per_chunk(off, len)` enqueued on st behind each chunk (A1 overlapped with the H2D)
     auto over_keys = [&](auto per_chunk) {
         if (p.h_keys && !p.strings) {
-            const uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
+            uint64_t chunk = std::max<uint64_t>(1u << 20, (n + 7) / 8);
+            if (two) chunk = (chunk + p2.chunk - 1) / p2.chunk * p2.chunk;  // whole level-1 blocks per copy
             std::vector<cudaEvent_t> evs;
             cudaEvent_t fork;
             CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
@@ -1165,36 +1166,34 @@ bool enqueue_single(const uint64_t* d_keys, const BuildParams& p, cudaStream_t s
         }
     };
     if (two) {
-        unsigned long long* gcount = A.alloc<unsigned long long>(p2.G + 1);
-        u64* gstart = A.alloc<u64>(p2.G + 2);
-        unsigned long long* gcur = A.alloc<unsigned long long>(p2.G + 1);
-        u64* lo1 = A.alloc<u64>(n);
-        u16* meta1 = A.alloc<u16>(n);
-        CK(cudaMemsetAsync(gcount, 0, (p2.G + 1) * 8, st));
+        const uint64_t cells = (uint64_t)p2.G * p2.nb1;
+        u32* M = A.alloc<u32>(cells);
+        u64* Ms = A.alloc<u64>(cells + 1);
+        u64* key1 = A.alloc<u64>(n);
         over_keys([&](uint64_t off, uint64_t len) {
-            launch_p2_count(d_keys + off, len, p.g, B, p2, gcount, st);
+            launch_p2_count(d_keys + off, len, off, p.g, B, p2, M, st);
             CKL();
         });
-        exscan_u64((const u64*)gcount, gstart, p2.G, scan_tmp, st);
+        exscan_u32_to_u64(M, Ms, cells, scan_tmp, st);
         CKL();
-        CK(cudaMemcpyAsync(gcur, gstart, (p2.G + 1) * 8, cudaMemcpyDeviceToDevice, st));
         lo_a = A.alloc<u64>(n);
         ab_a = A.alloc<u8>(n);
-        launch_p2_scatter(d_keys, n, p.g, B, p2, gcur, lo1, meta1, st);
+        launch_p2_scatter(d_keys, n, p.g, B, p2, Ms, key1, st);
         CKL();
         if (capture && !p.h_keys) {
             R.hash_nodes.push_back(last_node(st));
             R.hash_argc.push_back(kP2ScatterParams);
             R.hash_off.push_back(0);
         }
-        launch_p2_group(B, p2, (const unsigned long long*)gstart, lo1, meta1, C, lo_a, ab_a, small, st);
+        launch_p2_group(key1, p.g, B, p2, Ms, C, lo_a, ab_a, small, st);
         CKL();
         if (!tree) {  // (tree: each warp checks its own bucket)
             launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
             CKL();
         }
-        A.release(lo1);
-        A.release(meta1);
+        A.release(key1);
+        A.release(M);
+        A.release(Ms);
     } else {
         u64* lo_t = A.alloc<u64>(n);
         u8* ab_t = A.alloc<u8>(n);

@@ -1120,38 +1120,7 @@ __device__ __forceinline__ void fused_reorder(const Args& A, const u32* G, u32 k
 __device__ __forceinline__ u64 upper_keys_parallel(const Args& A, const u32* G, const NodeCtx& c, u32 lane) {
     constexpr u32 GW = Layout<SK_UPPER>::GW;
     const u32 s = c.s;
-    // No-carry fast path (remix_hi_nc) while sigma <= the node's carry margin
-    // (k_lo + sigma < 2^32 for every key; the buffered keys are not rebased here): the lane's
-    // keys (<= kUpperKpMax / 32) in registers, all their hashes of one seed issued before the
-    // ballots (independent chains).
-    constexpr u32 kCh = kUpperKpMax / 32;
-    u32 kl[kCh], kh[kCh], kc[kCh];
-#pragma unroll
-    for (u32 q = 0; q < kCh; ++q) {
-        const u32 j = q * 32 + lane;
-        const u32* g = G + GW * (j >> 2) + (j & 3);
-        const bool v = j < s;
-        kl[q] = v ? g[0] : 0;
-        kh[q] = v ? g[4] : 0;
-        kc[q] = v ? g[8] : 0;
-    }
-    const u32 nch = (s + 31) >> 5;
-    for (u32 sigma = 0; sigma <= c.margin; ++sigma) {
-        u32 left = 0;
-#pragma unroll
-        for (u32 q = 0; q < kCh; ++q)
-            if (q < nch) {
-                RS_COUNT(1);
-                left |= (u32)(q * 32 + lane < s && remix_hi_nc(kl[q], kh[q], kc[q], sigma) < c.mask) << q;
-            }
-        u32 cnt = 0;
-#pragma unroll
-        for (u32 q = 0; q < kCh; ++q)
-            if (q < nch) cnt += __popc(__ballot_sync(FULL, (left >> q) & 1u));
-        if (cnt == c.target) return sigma;
-        if (sigma == 0xffffffffu) break;
-    }
-    for (u64 sigma = (u64)c.margin + 1; sigma < kSeedCap; ++sigma) {
+    for (u64 sigma = 0; sigma < kSeedCap; ++sigma) {
         u32 cnt = 0;
         for (u32 j0 = 0; j0 < s; j0 += 32) {
             RS_COUNT(1);
@@ -1428,71 +1397,114 @@ __global__ void __launch_bounds__(1024) k_search_upper_big(const NodeRec* __rest
 
 // --------------------------------------------------------- sub-warp leaves --
 //
-// Leaves of at most 8 keys (l <= 8, e.g. C2: ~56 base seeds per leaf): a 32-seed window per leaf
-// overshoots its minimal base seed by ~16 of ~56 seeds and the per-leaf load / ballot work is
-// paid per 1.8 windows.  Here a warp is four 8-lane sub-warps, each owning one leaf: its lanes
-// try 8 consecutive base seeds k .. k+7 per step (lane i: k + i), the keys of the leaf in the
+// Leaves of at most 8 keys (l <= 8, e.g. C2: ~52 base seeds per leaf): a 32-seed window per leaf
+// overshoots its minimal base seed by ~16 of ~52 seeds (executed / algorithmic evaluations 1.32
+// at C2).  Here a warp is four 8-lane sub-warps, each owning one leaf: its lanes try 8
+// consecutive base seeds k .. k+7 per step (lane i: k + i), the keys of the leaf in the
 // sub-warp's shared-memory groups; the lowest lane of the sub-warp with a fit, with its
 // smallest r, gives the minimal value of that step, and every smaller base seed failed in
-// earlier steps, so it is the minimal stored value.  A finished sub-warp takes the
-// next leaf (one cursor atomic per warp for all sub-warps that need one).
+// earlier steps, so it is the minimal stored value.
+// Feeding four independent leaves without stalls: the warp claims kSubBatch leaf records per
+// cursor atomic (one per lane, kept in registers), and every sub-warp holds the keys of its NEXT leaf
+// in registers (loaded when the current one is installed), so a finished sub-warp installs
+// the next leaf from registers; the only global-memory waits are one record batch per
+// kSubBatch leaves.
 constexpr u32 kSubLeafMax = 8;
+// records per cursor atomic: a batch is ~2 steps of work per leaf it holds; 32 left up to one
+// batch (~100 us at C2) of tail when the cursor ran out (ncu: 42 % warps active, pass X)
+constexpr u32 kSubBatch = 8;
 
 template <int KIND>
-__global__ void __launch_bounds__(128) k_leaf_sub(const Args A) {
+__global__ void __launch_bounds__(128, 8) k_leaf_sub(const Args A) {
     __shared__ __align__(16) u32 sG[4][4][2 * 20];  // [warp][sub-warp][2 groups x 20 words]
     const u32 lane = threadIdx.x & 31, wib = threadIdx.x >> 5, sub = lane >> 3, sl = lane & 7;
     RS_COUNT_INIT();
     if (A.dup[0] || A.dup[1] > 1) return;
     const u32 nn = *A.n_nodes;
     u32* G = sG[wib][sub];
-    u32 m = 0, full = 0, slot = 0, margin = 0;
-    u64 k = 0;
-    bool busy = false, dry = false;
+    // record batch: lane i holds record (batch base + i); bnext = the next one to hand out
+    NodeRec brec{};
+    u32 bnext = 0, bcount = 0;
+    bool dry = false;  // the cursor passed the last leaf (warp-uniform)
+    // current leaf of the sub-warp, and its prefetched next leaf (this lane's key / A-B byte)
+    u32 m = 0, full = 0, slot = 0, margin = 0, k = 0;
+    bool busy = false;
+    bool have_pf = false;
+    u32 pf_m = 0, pf_slot = 0;
+    u64 pf_key = 0;
+    u8 pf_ab = 0;
+    const u8* lut = nullptr;
     for (;;) {
-        // sub-warps without a leaf take the next ones
-        const u32 want = __ballot_sync(FULL, !busy && !dry && sl == 0);
-        if (want) {
-            const int leader = __ffs(want) - 1;
-            u32 first = 0;
-            if ((int)lane == leader) first = atomicAdd(A.cursor, (u32)__popc(want));
-            first = __shfl_sync(FULL, first, leader);
-            if (!busy && !dry) {
-                const u32 idx = first + __popc(want & ((1u << (sub * 8)) - 1u));  // rank among the wanting
-                if (idx < nn) {
-                    const NodeRec rec = A.nodes[idx];
-                    m = rec.size;
-                    slot = rec.slot;
-                    full = (1u << m) - 1u;
-                    k = 0;
-                    busy = true;
-                    const bool valid = sl < m;
-                    const u64 key = valid ? A.lo[rec.key_off + sl] : 0;
-                    const bool isb = KIND == SK_LEAF_RF && valid && A.ab[rec.key_off + sl];
-                    const u32 g = 20 * (sl >> 2), q = sl & 3, kh = (u32)(key >> 32);
-                    G[g + q] = (u32)key;
-                    G[g + 4 + q] = kh;
-                    G[g + 8 + q] = key_const(kh);
-                    G[g + 12 + q] = valid && !isb ? FULL : 0u;
-                    G[g + 16 + q] = isb ? FULL : 0u;
-                    margin = valid ? ~(u32)key : FULL;  // reduced over the sub-warp below
-                } else {
-                    dry = true;
-                }
+        // 1. sub-warps whose leaf is done (or none yet) install their prefetched leaf
+        const bool inst = !busy && have_pf;
+        if (__any_sync(FULL, inst)) {
+            if (inst) {
+                m = pf_m;
+                slot = pf_slot;
+                full = (1u << m) - 1u;
+                k = 0;
+                busy = true;
+                have_pf = false;
+                const bool valid = sl < m;
+                const u64 key = valid ? pf_key : 0;
+                const bool isb = KIND == SK_LEAF_RF && valid && pf_ab;
+                const u32 g = 20 * (sl >> 2), q = sl & 3, kh = (u32)(key >> 32);
+                G[g + q] = (u32)key;
+                G[g + 4 + q] = kh;
+                G[g + 8 + q] = key_const(kh);
+                G[g + 12 + q] = valid && !isb ? FULL : 0u;
+                G[g + 16 + q] = isb ? FULL : 0u;
+                margin = valid ? ~(u32)key : FULL;
             }
+            // carry margin of each sub-warp's leaf: min over its keys of 2^32 - 1 - k_lo (the
+            // installing sub-warps' values; the others keep theirs)
+            u32 mg = margin;
+            for (int d = 4; d; d >>= 1) mg = min(mg, __shfl_xor_sync(FULL, mg, d));
+            if (inst) margin = mg;
+            if (inst) lut = KIND == SK_LEAF_RF && A.fit_lut ? A.fit_lut + fit_lut_off(m) : nullptr;
+            __syncwarp();
         }
-        // carry margin of each sub-warp's leaf: min over its keys of 2^32 - 1 - k_lo
-        for (int d = 4; d; d >>= 1) margin = min(margin, __shfl_xor_sync(FULL, margin, d));
-        __syncwarp();
-        if (!__any_sync(FULL, busy)) break;
-        // one step: lane sl tries base seed k + sl.  No-carry path (remix_hi_nc, the engine's
+        // 2. sub-warps without a prefetched leaf take the next records of the warp's batch (in
+        // sub-warp order; a new batch of 32 records per cursor atomic when it runs out); each
+        // record is broadcast from the lane holding it and the taker loads its lane's key and
+        // A/B byte, consumed at its next install (no wait here)
+        u32 want = __ballot_sync(FULL, !have_pf && sl == 0);
+        while (want) {
+            if (bnext >= bcount) {
+                if (dry) break;
+                u32 b0 = 0;
+                if (lane == 0) b0 = atomicAdd(A.cursor, kSubBatch);
+                b0 = __shfl_sync(FULL, b0, 0);
+                bcount = b0 >= nn ? 0u : min(kSubBatch, nn - b0);
+                bnext = 0;
+                if (lane < bcount) brec = A.nodes[b0 + lane];
+                if (bcount < kSubBatch) dry = true;  // (the cursor passed the last leaf)
+                if (bcount == 0) break;
+            }
+            const u32 who = (u32)(__ffs(want) - 1) >> 3;  // the requesting sub-warp
+            const u32 idx = bnext++;
+            const u32 koff = __shfl_sync(FULL, brec.key_off, (int)idx);
+            const u32 ksz = __shfl_sync(FULL, brec.size, (int)idx);
+            const u32 kslot = __shfl_sync(FULL, brec.slot, (int)idx);
+            if (sub == who) {
+                have_pf = true;
+                pf_m = ksz;
+                pf_slot = kslot;
+                pf_key = sl < ksz ? A.lo[koff + sl] : 0;
+                pf_ab = KIND == SK_LEAF_RF && sl < ksz ? A.ab[koff + sl] : 0;
+            }
+            want &= want - 1;
+        }
+        if (!__any_sync(FULL, busy || have_pf)) break;
+        if (!__any_sync(FULL, busy)) continue;  // (only prefetched leaves: install them)
+        // 3. one step: lane sl tries base seed k + sl.  No-carry path (remix_hi_nc, the engine's
         // 4-key groups) while every key's low word + the step's largest value stays below 2^32
         // (the leaf's carry margin), else the generic 64-bit path.
-        const u64 base = KIND == SK_LEAF_RF ? (k + sl) * m : k + sl;
+        const u64 base = KIND == SK_LEAF_RF ? ((u64)k + sl) * m : (u64)k + sl;
         u32 a = 0, b = 0;
+        RS_COUNT_RAW(__reduce_add_sync(FULL, busy ? m : 0u));
         if (busy) {
-            RS_COUNT_RAW(__reduce_add_sync(FULL, m));
-            const u64 top = KIND == SK_LEAF_RF ? (k + kSubLeafMax) * m : k + kSubLeafMax;
+            const u64 top = KIND == SK_LEAF_RF ? ((u64)k + kSubLeafMax) * m : (u64)k + kSubLeafMax;
             if (top <= margin) {
 #pragma unroll
                 for (u32 gi = 0; gi < kSubLeafMax / 4; ++gi) {
@@ -1518,22 +1530,22 @@ __global__ void __launch_bounds__(128) k_leaf_sub(const Args A) {
         }
         int r = -1;
         const bool ok = busy && (KIND == SK_LEAF_BF ? (a == full && (r = 0) == 0)
-                                 : A.fit_lut ? fit_rotation_lut(a, b, m, A.fit_lut + fit_lut_off(m), r)
-                                             : fit_rotation_lane(a, b, m, full, r));
+                                 : lut ? fit_rotation_lut(a, b, m, lut, r)
+                                       : fit_rotation_lane(a, b, m, full, r));
         const u32 bal = __ballot_sync(FULL, ok);
         const u32 mine = (bal >> (sub * 8)) & 0xffu;
         const int rw = __shfl_sync(FULL, r, (int)(sub * 8) + (mine ? __ffs(mine) - 1 : 0));
         if (busy) {
             if (mine) {
                 const u32 win = __ffs(mine) - 1;
-                if (sl == 0) A.values[slot] = KIND == SK_LEAF_RF ? (k + win) * m + (u32)rw : k + win;
+                if (sl == 0) A.values[slot] = KIND == SK_LEAF_RF ? ((u64)k + win) * m + (u32)rw : (u64)k + win;
                 busy = false;
             } else {
                 k += kSubLeafMax;
-                if (k >= kSeedCap) {
+                if ((u64)k + kSubLeafMax >= (1ull << 32)) {  // (far beyond any leaf of <= 8 keys)
                     if (sl == 0) {
                         atomicOr(A.err, 1u);
-                        A.values[slot] = KIND == SK_LEAF_RF ? k * m : k;
+                        A.values[slot] = KIND == SK_LEAF_RF ? (u64)k * m : k;
                     }
                     busy = false;
                 }
@@ -1648,7 +1660,7 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     static const int subleaf = getenv("RS_SUB_LEAF") ? atoi(getenv("RS_SUB_LEAF")) : 0;
     if (subleaf && (P.kind == SK_LEAF_RF || P.kind == SK_LEAF_BF) && P.max_size <= kSubLeafMax) {
         // leaves of at most 8 keys: four per warp (k_leaf_sub); the phase's batch cursor is zeroed
-        const u32 blocks = std::max<u32>(1, std::min<u32>((P.n_nodes_host + 15) / 16, (u32)P.sm_count * 16));
+        const u32 blocks = std::max<u32>(1, std::min<u32>((P.n_nodes_host + 15) / 16, (u32)P.sm_count * 8));
         if (P.kind == SK_LEAF_RF)
             k_leaf_sub<SK_LEAF_RF><<<blocks, 128, 0, st>>>(A);
         else

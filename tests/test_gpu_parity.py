@@ -795,3 +795,58 @@ def test_graph_replay_bytes():
     r = subprocess.run([sys.executable, "-c", _GRAPH_SNIPPET.format(root=root)], env=dict(os.environ, RS_GRAPH="1"),
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+_KNOB_SNIPPET = """
+import hashlib, sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2212_09562_b200 as rs, synth
+for leaf, b, n, rf in {cases!r}:
+    keys = synth.keys(n, 7000 + 10 * leaf + b)
+    print(hashlib.sha256(rs.build(keys, leaf, b, rotation_fitting=rf)).hexdigest())
+rng = np.random.default_rng(5)
+for rf in (True, False):
+    sizes = rng.integers(1, 9, size=3000).astype(np.uint32)
+    off = np.zeros(len(sizes) + 1, dtype=np.uint32); off[1:] = np.cumsum(sizes)
+    lo = rng.integers(0, 2**64 - 1, size=int(off[-1]), dtype=np.uint64, endpoint=True)
+    isb = rng.integers(0, 2, size=int(off[-1]), dtype=np.uint8)
+    v = np.asarray(rs.search_leaves(lo, isb, off, rotation_fitting=rf), dtype=np.uint64)
+    print(hashlib.sha256(v.tobytes() + lo.tobytes() + isb.tobytes() + off.tobytes()).hexdigest())
+"""
+
+
+@pytest.mark.parametrize("env", ["RS_SUB_LEAF=1", "RS_FIT_LUT=0", "RS_LEAN=0", "RS_P2=0", "RS_GRAPH=0",
+                                 "RS_SUB_LEAF=1,RS_FIT_LUT=0"])
+def test_engine_knobs_do_not_change_output(env):
+    """Every engine variant of round 2's small-configuration work gives the oracle's bytes:
+    the sub-warp leaf kernel (k_leaf_sub: four leaves of <= 8 keys per warp, prefetched),
+    the rotation-fit table off (serial rotation check), lean windows off, the one-level
+    partition instead of the two-level counting sort, no CUDA graphs -- on configurations
+    with leaves of 1..8 keys (rotation fitting and brute force), upper splits and ragged
+    buckets; plus kernel-level leaf searches against the oracle's leaf values."""
+    import hashlib
+    import subprocess
+    import sys
+    cases = [(8, 100, 20000, True), (5, 5, 20000, True), (7, 200, 30000, True), (4, 50, 8000, True),
+             (8, 100, 20000, False), (3, 9, 5000, True), (12, 1000, 30000, True)]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    for kv in env.split(","):
+        k, v = kv.split("=")
+        e[k] = v
+    out = subprocess.run([sys.executable, "-c", _KNOB_SNIPPET.format(root=root, cases=cases)], env=e,
+                         capture_output=True, text=True, timeout=900, check=True).stdout.split()
+    want = [hashlib.sha256(oracle.build(synth.keys(n, 7000 + 10 * leaf + b), leaf, b, rf=rf,
+                                        threads=os.cpu_count())).hexdigest() for leaf, b, n, rf in cases]
+    assert out[:len(cases)] == want
+    rng = np.random.default_rng(5)
+    for i, rf in enumerate((True, False)):
+        sizes = rng.integers(1, 9, size=3000).astype(np.uint32)
+        off = np.zeros(len(sizes) + 1, dtype=np.uint32)
+        off[1:] = np.cumsum(sizes)
+        lo = rng.integers(0, 2**64 - 1, size=int(off[-1]), dtype=np.uint64, endpoint=True)
+        isb = rng.integers(0, 2, size=int(off[-1]), dtype=np.uint8)
+        vals = np.array([oracle.leaf_rf(lo[off[j]:off[j + 1]], isb[off[j]:off[j + 1]]) if rf else
+                         oracle.leaf_bf(lo[off[j]:off[j + 1]]) for j in range(len(sizes))], dtype=np.uint64)
+        assert out[len(cases) + i] == hashlib.sha256(vals.tobytes() + lo.tobytes() + isb.tobytes() +
+                                                     off.tobytes()).hexdigest(), rf
