@@ -95,10 +95,26 @@ def executed_evals(cfg: dict, world: int):
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
+NVML_SAMPLER = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+while True:
+    try:
+        r = (nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+             nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+    except Exception:
+        break
+    print(*r, flush=True)
+    time.sleep(0.002)
+"""
+
+
 class NvmlClocks:
-    """NVML sampler thread (every 2 ms) running during the timed region: SM clock, max SM
-    clock and the active clock-event reasons -- enough samples even for a 30 ms timed region
-    (C2), where an nvidia-smi process does not get to its first sample."""
+    """NVML sampler (every ~2 ms) in a separate process running during the timed region: SM
+    clock, max SM clock and the active clock-event reasons -- enough samples even for a 30 ms
+    timed region (C2), and no GIL shared with the timed thread (a sampler thread in this process
+    once delayed a timed step by a whole GIL switch interval)."""
 
     NAMES = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
              ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -106,36 +122,28 @@ class NvmlClocks:
              ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap")]
 
     def __init__(self, index: int):
-        import threading
-
-        import pynvml
+        import pynvml  # noqa: F401 -- fail here (fallback to nvidia-smi) if NVML is absent
         self.nv = pynvml
-        pynvml.nvmlInit()
-        self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-        self.rows = []
-        self.stop_ev = threading.Event()
-        self.t = threading.Thread(target=self._run, daemon=True)
-        self.t.start()
-        while not self.rows and self.t.is_alive():  # first sample before the timed region starts
-            time.sleep(0.001)
-
-    def _run(self):
-        nv = self.nv
-        while True:
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs_ = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-            except Exception:  # noqa: BLE001 -- a failed query ends sampling
-                return
-            self.rows.append((sm, mx, rs_))
-            if self.stop_ev.wait(0.002):
-                return
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".txt", delete=False)
+        self.p = subprocess.Popen([sys.executable, "-c", NVML_SAMPLER, str(index)], stdout=self.f,
+                                  stderr=subprocess.DEVNULL)
+        t0 = time.time()
+        while time.time() - t0 < 20:  # first sample before the timed region starts
+            if os.path.getsize(self.f.name) > 0 or self.p.poll() is not None:
+                break
+            time.sleep(0.01)
 
     def stop(self) -> dict:
-        self.stop_ev.set()
-        self.t.join()
-        rows = self.rows[1:] or self.rows  # (the first sample was taken before the timed region)
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = []
+        for line in self.f.read().split("\n"):
+            p = line.split()
+            if len(p) == 3:
+                rows.append((float(p[0]), float(p[1]), int(p[2])))
+        os.unlink(self.f.name)
+        rows = rows[1:] or rows  # (the first sample was taken before the timed region)
         reasons = sorted({nm for _, _, r in rows for nm, c in self.NAMES if r & getattr(self.nv, c)})
         busy = [s for s, _, _ in rows if s > 300] or [s for s, _, _ in rows]
         return {"sm_mhz": float(np.median(busy)) if busy else None,
@@ -331,6 +339,8 @@ def main():
         blob = b if b is not None else blob
     torch.cuda.synchronize()
     clocks = clk.stop()
+    print(f"[bench] step ms: {[round(1e3 * t, 4) for t in times]} graph replays: "
+          f"{[int(x.get('graph_replay', 0)) for x in stats if x is not None]}", file=sys.stderr, flush=True)
     if world > 1:
         torch.distributed.barrier()
     mean_t = float(np.mean(times))
