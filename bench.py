@@ -333,6 +333,8 @@ def main():
     times, stats = [], []
     blob = None
     for _ in range(args.steps):
+        if world == 1:
+            blob = None  # (the previous result's pinned buffer back to the library's pool first)
         t, b, st = one_step()
         times.append(t)
         stats.append(st)
@@ -363,7 +365,9 @@ def main():
     for _ in range(max(3, args.warmup)):  # warm (the first builds of a configuration capture its CUDA graph)
         e2e_once()
     e2e_times = []
+    eb = None
     for _ in range(args.steps):
+        eb = None  # (as above: one result buffer in flight)
         flush.zero_()
         torch.cuda.synchronize()
         if world > 1:

@@ -25,27 +25,30 @@ SOURCES = ["scan.cu", "partition.cu", "search.cu", "encode.cu", "pipeline.cu", "
 HEADERS = ["device.cuh", "kernels.h", "pipeline.h", "tables.h", "format.h", "murmur3.h"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "recsplit.h"))
     deps.append(__file__)
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    obj_dir = os.path.join(OUT_DIR, "obj")
+def build(force: bool = False, verbose: bool = False, out_dir: str = OUT_DIR, extra=None) -> str:
+    """Compile the library into out_dir (extra: additional nvcc flags; default RS_NVCC_FLAGS)."""
+    extra = EXTRA if extra is None else extra
+    lib = os.path.join(out_dir, "librecsplit_b200.so")
+    if not force and not _stale(lib):
+        return lib
+    obj_dir = os.path.join(out_dir, "obj")
     os.makedirs(obj_dir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
 
     def compile_one(src):
         path = os.path.join(CSRC, src)
         obj = os.path.join(obj_dir, src + ".o")
-        cmd = [NVCC, *ARCH, *common, *EXTRA, "-c", path, "-o", obj]
+        cmd = [NVCC, *ARCH, *common, *extra, "-c", path, "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-lineinfo", "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -59,15 +62,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     # the translation units are independent: compile them concurrently
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
            "-Xlinker", "--exclude-libs,ALL", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
+
+
+def build_count_variant(force: bool = False) -> str:
+    """Diagnostic build with -DRS_COUNT_EVALS (every search kernel counts the key evaluations it
+    executes): bench.py's executed-evaluation fraction loads it in a subprocess.
+    Never the product path (paper_2212_09562_b200 loads lib/ only)."""
+    return build(force=force, out_dir=os.path.join(HERE, "..", "build_var", "count"), extra=["-DRS_COUNT_EVALS"])
 
 
 if __name__ == "__main__":

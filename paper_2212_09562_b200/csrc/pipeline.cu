@@ -1653,10 +1653,18 @@ bool build_single_fast(const uint64_t* d_keys, const BuildParams& p, cudaStream_
                 if (w != g_ws_bytes.end()) ws = w->second;
             }
             if (ws) {  // built before: capture now
-                std::unique_ptr<SinglePlan> P = capture_plan(d_keys, p, ws);
+                if (g_plans.size() >= kMaxPlans) g_plans.erase(g_plans.begin());  // (frees its workspace first)
+                std::unique_ptr<SinglePlan> P;
+                try {
+                    P = capture_plan(d_keys, p, ws);
+                } catch (const Error&) {  // e.g. no memory for a workspace: build uncaptured
+                    P.reset();
+                    cudaGetLastError();
+                    std::lock_guard<std::mutex> g2(g_est_mu);
+                    g_ws_bytes.erase(key);  // (no new attempt until the next uncaptured build)
+                }
                 if (P) {
                     P->dt_gen = device_tables_generation(dev);
-                    if (g_plans.size() >= kMaxPlans) g_plans.erase(g_plans.begin());
                     it = g_plans.emplace(key, std::move(P)).first;
                 }
             }
