@@ -105,7 +105,7 @@ while True:
              nv.nvmlDeviceGetCurrentClocksEventReasons(h))
     except Exception:
         break
-    print(*r, flush=True)
+    print(*r, time.time(), flush=True)
     time.sleep(0.002)
 """
 
@@ -133,22 +133,28 @@ class NvmlClocks:
                 break
             time.sleep(0.01)
 
-    def stop(self) -> dict:
+    def stop(self, t_start: float = 0.0) -> dict:
+        """Summary of the samples taken after t_start (time.time() at the timed region's start)."""
         self.p.terminate()
         self.p.wait()
         self.f.seek(0)
         rows = []
         for line in self.f.read().split("\n"):
             p = line.split()
-            if len(p) == 3:
+            if len(p) == 4 and float(p[3]) >= t_start:
                 rows.append((float(p[0]), float(p[1]), int(p[2])))
         os.unlink(self.f.name)
-        rows = rows[1:] or rows  # (the first sample was taken before the timed region)
         reasons = sorted({nm for _, _, r in rows for nm, c in self.NAMES if r & getattr(self.nv, c)})
         busy = [s for s, _, _ in rows if s > 300] or [s for s, _, _ in rows]
         return {"sm_mhz": float(np.median(busy)) if busy else None,
                 "sm_max_mhz": float(max(m for _, m, _ in rows)) if rows else None,
                 "reasons": reasons, "samples": len(rows), "source": "nvml"}
+
+
+def nvml_index(dev: int) -> int:
+    """NVML (physical) index of CUDA device dev under CUDA_VISIBLE_DEVICES (integer lists)."""
+    vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    return int(vis[dev]) if dev < len(vis) and vis[dev].isdigit() else dev
 
 
 def clock_sampler(index: int):
@@ -173,7 +179,7 @@ class Clocks:
         except OSError:
             self.p = None
 
-    def stop(self) -> dict:
+    def stop(self, t_start: float = 0.0) -> dict:
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
@@ -293,6 +299,19 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
+    # run on the CPUs local to this GPU (pinned host buffers then live on its NUMA node; an H2D
+    # from the far socket measured ~20 % slower end to end at C2)
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(nvml_index(dev))
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+    except Exception:  # noqa: BLE001 -- no NVML / affinity: leave the scheduler's choice
+        pass
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     # weak scaling: N ranks build ONE MPHF of N x n keys, each rank owning 1/N of the
     # buckets (bucket-range sharding).  Each rank starts from its own n-key slice of
@@ -324,29 +343,32 @@ def main():
         z.synchronize()
         return a.elapsed_time(z) * 1e-3, blob, st
 
-    for _ in range(max(3, args.warmup)):
-        one_step()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
+    # the clock sampler starts before the warm-up steps, so that the GPU is not left idle (and
+    # its clocks ramping back up) between warm-up and timed steps; only the samples taken
+    # during the timed region are reported
+    clk = clock_sampler(nvml_index(dev)) if not os.environ.get("RS_BENCH_NO_CLOCKS") else None
     # the collector off in the timed loops (as timeit does): a full collection of this process's
     # objects (torch imported) took one timed C2 step from 2.6 to 18-22 ms
     import gc
     gc.collect()
     gc.disable()
-    clk = clock_sampler(dev) if not os.environ.get("RS_BENCH_NO_CLOCKS") else None
-    time.sleep(0.2)  # (the sampler's first NVML queries before the timed region)
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t_timed = time.time()
     times, stats = [], []
     blob = None
     for _ in range(args.steps):
-        if world == 1:
-            blob = None  # (the previous result's pinned buffer back to the library's pool first)
+        if world == 1:  # (the previous result's pinned buffer back to the library's pool first: a
+            blob = b = None  # second live result costs a cudaMallocHost inside the timed step)
         t, b, st = one_step()
         times.append(t)
         stats.append(st)
         blob = b if b is not None else blob
     torch.cuda.synchronize()
-    clocks = clk.stop() if clk else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled"], "samples": 0}
+    clocks = clk.stop(t_timed) if clk else {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["not sampled"], "samples": 0}
     print(f"[bench] step ms: {[round(1e3 * t, 4) for t in times]} graph replays: "
           f"{[int(x.get('graph_replay', 0)) for x in stats if x is not None]}", file=sys.stderr, flush=True)
     if world > 1:

@@ -237,7 +237,12 @@ void phase_policy(const Tables& T, SearchKind kind, uint32_t typical, uint32_t& 
     }
     const double it = trials / 32.0;
     iters = (uint32_t)std::min(16.0, std::max(1.0, std::floor(it / 16.0)));
-    help = it >= 32.0;
+    // help mode (per-node window dispensers, warps joining unfinished nodes) from this many
+    // expected 32-seed iterations per node; below, batch mode (each node searched by one warp,
+    // no dispenser atomics).  RS_HELP_IT / RS_LEAF_HELP_IT override (development A/B).
+    static const double help_it = getenv("RS_HELP_IT") ? atof(getenv("RS_HELP_IT")) : 32.0;
+    static const double leaf_help_it = getenv("RS_LEAF_HELP_IT") ? atof(getenv("RS_LEAF_HELP_IT")) : 32.0;
+    help = it >= (kind == SK_LEAF_RF || kind == SK_LEAF_BF ? leaf_help_it : help_it);
 }
 
 }  // namespace
