@@ -482,7 +482,11 @@ def main():
         "phases_s": {"partition": st0["t_partition"], "tree": st0["t_tree"],
                      "search_bucket_tree": st0.get("t_search_tree", 0.0), "upper": st0["t_search"][0],
                      "lower2": st0["t_search"][1], "lower1": st0["t_search"][2], "leaves": st0["t_search"][3],
-                     "reorder": st0["t_reorder"], "encode": st0["t_encode"], "d2h": st0["t_d2h"]},
+                     "reorder": st0["t_reorder"], "encode": st0["t_encode"], "d2h": st0["t_d2h"],
+                     # the library's own device span (first enqueued operation to the end of the
+                     # result D2H) and host wall time inside the C ABI call, means over the timed steps
+                     "device_span": float(np.mean([x.get("t_device", 0.0) for x in stats])),
+                     "abi_call": float(np.mean([x.get("t_total", 0.0) for x in stats]))},
         "algo_evals_per_step": [int(x) for x in st0["algo_evals"]],
         # INT32 fraction per search phase: that phase's algorithmic evaluations /
         # its CUDA-event time / the same peak; "step" = all evaluations / the whole step

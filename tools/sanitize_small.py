@@ -21,6 +21,9 @@ for n, leaf, b, seed, shards in cases:
     if shards:
         B = (n + b - 1) // b
         cuts = [0] + [B * (r + 1) // (shards + 1) for r in range(shards - 1)] + [B]  # uneven ranges
-    got = rs.build(keys, leaf, b, virtual_shards=shards, cuts=cuts)
-    assert got == oracle.build(keys, leaf, b, threads=os.cpu_count() or 1), (n, leaf, b)
+    want = oracle.build(keys, leaf, b, threads=os.cpu_count() or 1)
+    # unsharded builds three times: uncaptured, captured + replayed, replayed (CUDA-graph path)
+    for rep in range(1 if shards else 3):
+        got = rs.build(keys, leaf, b, virtual_shards=shards, cuts=cuts)
+        assert got == want, (n, leaf, b, rep)
     print("ok", n, leaf, b, shards, len(got))
