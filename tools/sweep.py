@@ -28,7 +28,8 @@ import synth  # noqa: E402
 
 def point(kt, n, leaf, b, rf, reps):
     stream = torch.cuda.current_stream()
-    rs.build_device(kt, leaf, b, rotation_fitting=rf, stream=stream)  # warm-up
+    for _ in range(2):  # warm-up: the first build of a configuration measures, the second captures its graph
+        rs.build_device(kt, leaf, b, rotation_fitting=rf, stream=stream, stats=True)
     ts = []
     st = None
     blob = None
