@@ -1252,18 +1252,28 @@ bool enqueue_single(const uint64_t* d_keys, const BuildParams& p, cudaStream_t s
     // for a typical bucket (launch sizing only)
     std::vector<uint64_t> bound(NP, 0), poff(NP, 0), est(NP, 0);
     uint64_t nbound = 0;
-    const uint32_t typ = (uint32_t)std::max<double>(1.0, std::min<double>(S, std::round(avg)));
+    // expected node count of each phase under Poisson(n / B) bucket sizes (launch sizing: grid
+    // and batch size; the counts themselves stay on the device).  (A phase that a bucket of
+    // the mean size does not have -- a second or third upper level -- still gets its expected
+    // share: sizing it from the mean bucket alone gave such phases one block, 10-100x slower
+    // upper splits at l = 4..9, C4 sweep pass AK.)
+    std::vector<double> expect(NP, 0.0);
+    const double lavg = std::log(std::max(avg, 1e-300));
     for (uint32_t x = 1; x <= S; ++x) {
         const Tables::Tmpl& tp = T.tmpl(x);
-        for (uint32_t q = 0; q < NP; ++q)
+        const double px = std::exp(x * lavg - avg - std::lgamma((double)x + 1.0));
+        for (uint32_t q = 0; q < NP; ++q) {
             bound[q] = std::max<uint64_t>(bound[q], ((uint64_t)tp.phase_cnt[q] * n + x - 1) / x);
+            expect[q] += px * tp.phase_cnt[q];
+        }
         nbound = std::max<uint64_t>(nbound, ((uint64_t)T.N[x] * n + x - 1) / x);
     }
     uint64_t acc = 0;
     for (uint32_t q = 0; q < NP; ++q) {
         poff[q] = acc;
         acc += bound[q];
-        est[q] = std::max<uint64_t>(bound[q] ? 1 : 0, B * (uint64_t)T.tmpl(typ).phase_cnt[q]);
+        const double e = std::ceil((double)B * expect[q] * 1.1 + 64.0);
+        est[q] = bound[q] ? std::min<uint64_t>(bound[q], std::max<uint64_t>(1, (uint64_t)e)) : 0;
     }
     rsd::NodeRec* nodes = tree ? nullptr : A.alloc<rsd::NodeRec>(acc);
     u64* values_d = A.alloc<u64>(nbound);
@@ -1521,7 +1531,9 @@ struct SinglePlan {
 };
 
 std::mutex g_plan_mu;
-std::map<ConfigKey, std::unique_ptr<SinglePlan>> g_plans;
+// (never destroyed: a plan's graph, streams and device memory must not be released by static
+// destructors after the CUDA runtime has shut down; the process exit reclaims them)
+std::map<ConfigKey, std::unique_ptr<SinglePlan>>& g_plans = *new std::map<ConfigKey, std::unique_ptr<SinglePlan>>;
 constexpr uint64_t kGraphMaxKeys = 1ull << 27;  // larger builds are not launch-bound (workspace ~3 GB)
 constexpr size_t kMaxPlans = 4;
 
