@@ -67,7 +67,8 @@ struct Args {
     u32 cp_wide2;  // wide-counter splits: second checkpoint too (0 = single stage)
     u64* lo_w;     // fused redistribution (batch-mode split phases, nodes <= kFuseMax keys): the
     u8* ab_w;      // key arrays written in child order right after the node's search; null = off
-    u32 upper_kp;  // upper splits in batch mode: keys-parallel sequential seeds (upper_keys_parallel)
+    u32 upper_kp;  // upper splits in batch mode: keys-parallel sequential seeds (upper_keys_parallel) for nodes up to this size (0 = off)
+    u32 upper_kp_var;  // ... whose left-count variance c0 (s - c0) / s is at most this
     u32 qwords;    // early-rejection queue words per warp (0 for the plain variants)
     unsigned long long* exec;  // RS_COUNT_EVALS builds: executed evaluations of this phase's class
     u32 lane_fit;  // leaves up to this size check rotations lane by lane (fit_rotation_lane)
@@ -1275,7 +1276,10 @@ __global__ void __launch_bounds__(kWarpsPerBlockMax * 32,
                     if (n + 2 < n1) rec2 = A.nodes[n + 2];
                 }
                 u64 val = 0;
-                if (KIND == SK_UPPER && A.upper_kp && c.s <= kUpperKpMax) {
+                // (keys-parallel only where few trials are expected: c0 (s - c0) / s = the
+                // binomial variance of the left count, trials ~ sqrt(2 pi var); balanced splits
+                // need more and run faster as 32-seed windows, pass AO)
+                if (KIND == SK_UPPER && c.s <= A.upper_kp && (u64)c.target * (c.s - c.target) <= (u64)A.upper_kp_var * c.s) {
                     val = upper_keys_parallel(A, G, c, lane);
                 } else {
                     u64 wstart = 0;
@@ -1746,7 +1750,10 @@ bool launch_search(const PhaseLaunch& P, cudaStream_t st) {
     const bool fused = fuse && P.fuse_reorder && (P.kind == SK_UPPER || P.kind == SK_LOWER) && !P.help &&
                        A.tail == 0 && P.max_size <= kFuseMax;
     static const int ukp = getenv("RS_UPPER_KP") ? atoi(getenv("RS_UPPER_KP")) : 1;
-    A.upper_kp = ukp && P.kind == SK_UPPER && !P.help && A.tail == 0 ? 1u : 0u;
+    static const int ukp_max = getenv("RS_UPPER_KP_MAX") ? atoi(getenv("RS_UPPER_KP_MAX")) : (int)kUpperKpMax;
+    A.upper_kp = ukp && P.kind == SK_UPPER && !P.help && A.tail == 0 ? (u32)std::min<int>(ukp_max, (int)kUpperKpMax) : 0u;
+    static const int ukp_var = getenv("RS_UPPER_KP_VAR") ? atoi(getenv("RS_UPPER_KP_VAR")) : 5;  // (pass AP)
+    A.upper_kp_var = (u32)std::max(0, ukp_var);
     A.lo_w = fused ? P.lo_w : nullptr;
     A.ab_w = fused ? P.ab_w : nullptr;
     switch (P.kind) {
@@ -1909,7 +1916,7 @@ __device__ __forceinline__ u64 tree_search_node(const Args& A, const NodeRec& re
                                                 const u64* blo, const u8* bab, u32* QS, u32* QC) {
     NodeCtx c{};
     load_node<KIND, false>(A, 0, lane, G, T8, c, nullptr, &rec, blo, bab);
-    if (KIND == SK_UPPER && A.upper_kp && c.s <= kUpperKpMax) return upper_keys_parallel(A, G, c, lane);
+    if (KIND == SK_UPPER && c.s <= A.upper_kp) return upper_keys_parallel(A, G, c, lane);
     const KeysView K{G, (u32)__cvta_generic_to_shared(T8), 0u, (u32)__cvta_generic_to_shared(&s_full_tab[0][0])};
     const u64 ws = 32ull * A.iters;
     for (u64 wstart = 0;; wstart += ws) {
@@ -2041,7 +2048,8 @@ void launch_bucket_tree(const TreeLaunch& L, cudaStream_t st) {
     static const int lane_fit = getenv("RS_LANE_FIT") ? atoi(getenv("RS_LANE_FIT")) : 10;
     A.lane_fit = (u32)std::max(0, lane_fit);
     static const int ukp = getenv("RS_UPPER_KP") ? atoi(getenv("RS_UPPER_KP")) : 1;
-    A.upper_kp = ukp ? 1u : 0u;
+    A.upper_kp = ukp ? kUpperKpMax : 0u;
+    A.upper_kp_var = 1u << 30;  // (the bucket-tree kernel: every upper node up to kUpperKpMax)
     A.qwords = 0;
     const u32 cap = (L.S + 15) & ~15u;
     A.warp_cap = cap;
