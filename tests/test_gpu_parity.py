@@ -816,12 +816,13 @@ for rf in (True, False):
 
 
 @pytest.mark.parametrize("env", ["RS_SUB_LEAF=1", "RS_FIT_LUT=0", "RS_LEAN=0", "RS_P2=0", "RS_GRAPH=0",
-                                 "RS_SUB_LEAF=1,RS_FIT_LUT=0"])
+                                 "RS_SUB_LEAF=1,RS_FIT_LUT=0", "RS_UPPER_KP=0", "RS_UPPER_KP_VAR=100000"])
 def test_engine_knobs_do_not_change_output(env):
     """Every engine variant of round 2's small-configuration work gives the oracle's bytes:
     the sub-warp leaf kernel (k_leaf_sub: four leaves of <= 8 keys per warp, prefetched),
     the rotation-fit table off (serial rotation check), lean windows off, the one-level
-    partition instead of the two-level counting sort, no CUDA graphs -- on configurations
+    partition instead of the two-level counting sort, no CUDA graphs, upper splits all as
+    windows / all keys-parallel up to 256 keys -- on configurations
     with leaves of 1..8 keys (rotation fitting and brute force), upper splits and ragged
     buckets; plus kernel-level leaf searches against the oracle's leaf values."""
     import hashlib
