@@ -1373,17 +1373,19 @@ bool enqueue_single(const uint64_t* d_keys, const BuildParams& p, cudaStream_t s
         P.lo_w = lo_a;
         P.ab_w = ab_a;
         P.exec = exec_d ? exec_d + cls : nullptr;
-        CK(cudaMemsetAsync(active, 0xff, nslots * 4, st));
+        static const bool tail_help = getenv("RS_TAIL") && atoi(getenv("RS_TAIL")) > 0;
+        if (P.help || tail_help) CK(cudaMemsetAsync(active, 0xff, nslots * 4, st));  // (help mode's list of open nodes)
         const int a = tm.mark(st);
         const bool fused = launch_search(P, st);
         CKL();
         const int b = tm.mark(st);
+        int c = b;  // (no redistribution kernel: the search fused it, or a leaf phase)
         if ((kind == SK_UPPER || kind == SK_LOWER) && !fused) {
             launch_reorder(nodes + poff[q], P.n_nodes_host, values_d, lo_a, ab_a, leaf, sh.u1, sh.u2, maxs, sms, nullptr,
                            st, pcnt_d + q);
             CKL();
+            c = tm.mark(st);
         }
-        const int c = tm.mark(st);
         R.pev.push_back({cls, a, b, c});
     }
     R.e3 = tm.mark(st);
@@ -1519,6 +1521,8 @@ struct SinglePlan {
     SingleRun R;
     uint32_t launches = 0;
     uint64_t dt_gen = 0;
+    const void* last_src = nullptr;  // key source / result buffer the executable graph holds now
+    const void* last_dst = nullptr;
     ~SinglePlan() {
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
@@ -1589,15 +1593,21 @@ std::unique_ptr<SinglePlan> capture_plan(const uint64_t* d_keys, const BuildPara
     if (!ok) return nullptr;
     CK(cudaGraphInstantiate(&P->exec, P->graph, 0));
     // the result buffer of the capture is not used by replays (each replay gets its own)
+    P->last_dst = P->R.buf;
     pinned_release(P->R.buf);
     P->R.buf = nullptr;
+    P->last_src = host ? (const void*)p.h_keys : (const void*)d_keys;
     return P;
 }
 
 // launch a plan for this build's keys; false if the replay must be redone uncaptured
 bool replay_plan(SinglePlan& P, const uint64_t* d_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out,
                  std::chrono::steady_clock::time_point t_start) {
-    if (p.h_keys) {
+    // (the executable graph keeps the last parameters set: a replay with the same key source or
+    // result buffer as the previous one skips the update)
+    const void* src_now = p.h_keys ? (const void*)p.h_keys : (const void*)d_keys;
+    if (src_now == P.last_src) {
+    } else if (p.h_keys) {
         for (size_t c = 0; c < P.R.h2d_nodes.size(); ++c)
             CK(cudaGraphExecMemcpyNodeSetParams1D(P.exec, P.R.h2d_nodes[c], P.R.d_keys_ws + P.R.chunks[c].first,
                                                   p.h_keys + P.R.chunks[c].first, P.R.chunks[c].second * 8,
@@ -1613,9 +1623,15 @@ bool replay_plan(SinglePlan& P, const uint64_t* d_keys, const BuildParams& p, cu
             CK(cudaGraphExecKernelNodeSetParams(P.exec, P.R.hash_nodes[c], &kp));
         }
     }
+    P.last_src = src_now;
     SingleRun R = P.R;  // (marks and layout; this replay's own result buffer)
     R.buf = pinned_get(R.est_words * 8);
-    CK(cudaGraphExecMemcpyNodeSetParams1D(P.exec, R.blob_node, R.buf, R.outw, R.est_words * 8, cudaMemcpyDeviceToHost));
+    if (R.buf != P.last_dst) {
+        P.last_dst = nullptr;  // (unknown until the update succeeds)
+        CK(cudaGraphExecMemcpyNodeSetParams1D(P.exec, R.blob_node, R.buf, R.outw, R.est_words * 8,
+                                              cudaMemcpyDeviceToHost));
+        P.last_dst = R.buf;
+    }
     g_launches = P.launches;
     CK(cudaGraphLaunch(P.exec, st));
     Marks tm;
