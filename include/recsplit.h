@@ -127,6 +127,15 @@ RECSPLIT_API int recsplit_version(void);
 RECSPLIT_API uint32_t recsplit_max_bucket_keys(void);
 
 /*
+ * Release what the library keeps between builds: the captured build graphs and their
+ * device workspaces, the unused part of its device memory pool and its idle pinned host
+ * buffers.  Results already returned stay valid (free them with recsplit_free).  Returns
+ * RECSPLIT_OK, or RECSPLIT_E_CUDA if a CUDA call failed.  Not to be called concurrently
+ * with a build.
+ */
+RECSPLIT_API int recsplit_trim(void);
+
+/*
  * Build the MPHF of the n distinct 64-bit keys at `keys` (HOST memory, pageable or
  * pinned) with leaf size l = leaf_size (P:110, 2..24) and expected bucket size
  * b = bucket_size.  Rotation fitting on, global seed 0.  On success *out
@@ -143,6 +152,13 @@ RECSPLIT_API int recsplit_build_ex(const uint64_t *keys, size_t n, uint32_t leaf
  * As recsplit_build_ex, but `d_keys` is a DEVICE pointer (n x u64, on opt->device)
  * and all work is ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
  * The call returns after the serialized bytes are in host memory.
+ *
+ * Caching (single-GPU builds of up to 2^27 keys, both entries): the second build of a
+ * configuration (n, leaf_size, bucket_size, options, host or device keys, stats or not)
+ * captures the whole device pipeline as a CUDA graph over a workspace it keeps (about 22 B
+ * per key plus the node tables); later builds of that configuration replay it.  At most 4
+ * such configurations are kept per process (least recently captured dropped first);
+ * recsplit_trim() releases them.
  */
 RECSPLIT_API int recsplit_build_device(const uint64_t *d_keys, size_t n, uint32_t leaf_size,
                           uint32_t bucket_size, const recsplit_options *opt, void *stream,

@@ -27,7 +27,7 @@ SYMBOLS = [
     "recsplit_shard_globals", "recsplit_query_device", "recsplit_build_strings", "recsplit_query_strings",
     "recsplit_open", "recsplit_handle_query_many", "recsplit_handle_query_device", "recsplit_close",
     "recsplit_check_bijective_device", "recsplit_route_keys", "recsplit_bucket_histogram",
-    "recsplit_balanced_cuts",
+    "recsplit_balanced_cuts", "recsplit_trim",
 ]
 
 
@@ -133,6 +133,8 @@ def lib():
         L.recsplit_balanced_cuts.restype = i32
         L.recsplit_close.argtypes = [C.c_void_p]
         L.recsplit_close.restype = None
+        L.recsplit_trim.argtypes = []
+        L.recsplit_trim.restype = i32
         for name in ("recsplit_shard_begin", "recsplit_shard_min_step", "recsplit_shard_finish", "recsplit_stitch",
                      "recsplit_shard_globals"):
             getattr(L, name).restype = i32
@@ -632,3 +634,9 @@ def build_sharded(keys_tensor, leaf_size: int, bucket_size: int, rotation_fittin
         sh.close()
     parts = gather_parts(part, 0, group)
     return stitch(parts) if parts is not None else None
+
+
+def trim() -> None:
+    """Release the library's cached build graphs and workspaces, unused pool memory and idle
+    pinned buffers (recsplit_trim)."""
+    _check(lib().recsplit_trim())

@@ -352,6 +352,14 @@ int recsplit_version(void) { return 1; }
 
 uint32_t recsplit_max_bucket_keys(void) { return rs::kMaxBucketKeys; }
 
+int recsplit_trim(void) {
+    return guarded([&]() -> int {
+        std::lock_guard<std::mutex> g(g_build_mu);
+        rs::trim_caches();
+        return RECSPLIT_OK;
+    });
+}
+
 int recsplit_build(const uint64_t* keys, size_t n, uint32_t leaf_size, uint32_t bucket_size, recsplit_bytes* out) {
     return build_host_keys(keys, n, leaf_size, bucket_size, nullptr, out, nullptr, nullptr, false);
 }

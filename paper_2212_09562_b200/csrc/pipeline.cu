@@ -36,9 +36,18 @@ namespace {
 // that, the driver returns the excess to the OS at the next synchronization.
 constexpr uint64_t kPoolKeepBytes = 8ull << 30;
 
-cudaMemPool_t device_pool_impl(int dev) {
+std::mutex& pools_mu() {
     static std::mutex mu;
-    static std::map<int, cudaMemPool_t> pools;
+    return mu;
+}
+std::map<int, cudaMemPool_t>& pools_map() {
+    static std::map<int, cudaMemPool_t>& pools = *new std::map<int, cudaMemPool_t>;
+    return pools;
+}
+
+cudaMemPool_t device_pool_impl(int dev) {
+    std::mutex& mu = pools_mu();
+    std::map<int, cudaMemPool_t>& pools = pools_map();
     std::lock_guard<std::mutex> g(mu);
     auto it = pools.find(dev);
     if (it != pools.end()) return it->second;
@@ -1643,6 +1652,34 @@ bool replay_plan(SinglePlan& P, const uint64_t* d_keys, const BuildParams& p, cu
 }
 
 }  // namespace
+
+void trim_caches() {
+    {
+        std::lock_guard<std::mutex> lk(g_report.mu);
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        g_plans.clear();  // (destroys graphs, events, streams; frees the workspaces)
+    }
+    {
+        std::lock_guard<std::mutex> g(g_est_mu);
+        g_ws_bytes.clear();  // (the next build of a configuration runs uncaptured again)
+    }
+    {  // the pools the library created (devices it never used are not touched)
+        std::lock_guard<std::mutex> g(pools_mu());
+        int cur = -1;
+        if (!pools_map().empty()) CK(cudaGetDevice(&cur));
+        for (auto& kv : pools_map()) {
+            CK(cudaSetDevice(kv.first));
+            CK(cudaDeviceSynchronize());  // (frees of finished builds are stream-ordered)
+            CK(cudaMemPoolTrimTo(kv.second, 0));
+        }
+        if (cur >= 0) CK(cudaSetDevice(cur));
+    }
+    PinnedPool& P = pinned_pool();
+    std::lock_guard<std::mutex> g(P.mu);
+    for (auto& kv : P.idle) cudaFreeHost(kv.second);
+    P.idle.clear();
+    P.idle_bytes = 0;
+}
 
 bool replay_host_keys(const uint64_t* h_keys, const BuildParams& p, cudaStream_t st, BuildOutput& out) {
     if (!graphs_enabled() || p.strings || p.shards > 1 || !p.cuts.empty() || p.n > kGraphMaxKeys) return false;

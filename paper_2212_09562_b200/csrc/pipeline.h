@@ -44,6 +44,8 @@ struct BuildParams {
 
 // the library's stream-ordered memory pool on device dev (kept reserved between builds)
 cudaMemPool_t device_pool(int dev);
+// drop the captured build graphs (and workspaces), trim the pools, free idle pinned buffers
+void trim_caches();
 
 // Pinned host result buffers (single-GPU builds D2H straight into the caller's result):
 // pinned_get returns a buffer of >= bytes (reused when possible), pinned_release takes back

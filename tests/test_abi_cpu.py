@@ -147,3 +147,9 @@ def test_corrupt_blob_rejected_or_in_range():
     # truncated / bit-flipped index words are rejected too
     with pytest.raises(rs.RecSplitError):
         rs.query_many(blob[:-8], keys[:10])
+
+
+def test_trim_without_gpu():
+    """recsplit_trim only releases what exists: without a GPU (or before any build) it succeeds."""
+    rs.trim()
+    rs.trim()

@@ -778,6 +778,18 @@ try:
 except rs.RecSplitError as e:
     assert e.code == rs.E_DUPLICATE
 assert rs.build_device(d1, leaf, b) == w1, "after duplicate"
+# recsplit_trim: the cached graphs, workspaces and pool memory go back; builds recapture
+big = synth.keys(2_000_000, 504)
+dbig = dev(big)
+for i in range(3):
+    rs.build_device(dbig, 12, 1000)
+torch.cuda.synchronize()
+free0 = torch.cuda.mem_get_info()[0]
+rs.trim()
+free1 = torch.cuda.mem_get_info()[0]
+assert free1 > free0 + (16 << 20), (free0, free1)
+for i in range(3):
+    assert rs.build_device(d1, leaf, b) == w1, ("after trim", i)
 print("ok")
 """
 
