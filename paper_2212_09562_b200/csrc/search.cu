@@ -1214,6 +1214,11 @@ __device__ __forceinline__ void init_lower_tables(const Args& A) {
 // registers: C2 upper phase -5 % (pass AF)
 #define RS_MIN_BLOCKS 8
 #endif
+#ifndef RS_LOWER_MIN_BLOCKS
+// lower-split kernels at 8 blocks x 4 warps per SM (64 registers): 9 or 10 blocks (56 / 48
+// registers) spill and grow the split loop 83 -> 86 instructions
+#define RS_LOWER_MIN_BLOCKS 8
+#endif
 #ifndef RS_LEAF_MIN_BLOCKS
 // leaf kernels at 8 blocks x 4 warps per SM (64 registers): measured -8.5 % on the C5 leaf phase,
 // -3 % at C3, neutral at C2 against the unconstrained 78-88 registers (gpurun pass L)
@@ -1221,7 +1226,7 @@ __device__ __forceinline__ void init_lower_tables(const Args& A) {
 #endif
 template <int KIND, int VAR = V_PLAIN>
 __global__ void __launch_bounds__(kWarpsPerBlockMax * 32,
-                                                     KIND == SK_LOWER                             ? 8
+                                                     KIND == SK_LOWER                             ? RS_LOWER_MIN_BLOCKS
                                                      : (KIND == SK_LEAF_RF || KIND == SK_LEAF_BF) ? RS_LEAF_MIN_BLOCKS
                                                                                                   : RS_MIN_BLOCKS) k_search(const Args A) {
     constexpr u32 GW = Layout<KIND>::GW;
