@@ -53,8 +53,10 @@ bool partition2_shape(u64 n, u64 B, u32 S, P2Shape& sh);
 void launch_p2_count(const u64* keys, u64 n, u64 first_key, u64 g, u64 B, const P2Shape& sh, u32* M, cudaStream_t st);
 void launch_p2_scatter(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, const u64* Ms, u64* key1,
                        cudaStream_t st);
+// dts > 0: the duplicate check fused into level 2 (small[2] |= 1 on a repeated key, small[3] +=
+// keys with lo == 0), per-warp index tables of dts entries (a power of two >= 2 x the size bound)
 void launch_p2_group(const u64* key1, u64 g, u64 B, const P2Shape& sh, const u64* Ms, u64* C, u64* lo_a, u8* ab_a,
-                     u32* small, cudaStream_t st);
+                     u32* small, cudaStream_t st, u32 dts = 0);
 // parameter counts of the kernels that read the keys (graph replays patch parameter 0, the keys)
 constexpr int kHashParams = 12, kP2CountParams = 10, kP2ScatterParams = 10;
 // scatter (lo, ab) to bucket order (cursor = copy of exclusive offsets)

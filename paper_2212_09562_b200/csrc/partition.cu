@@ -485,13 +485,19 @@ __global__ void __launch_bounds__(1024) k_p2_scatter(const u64* __restrict__ key
 // synchronized path)
 __global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ key1, u64 g, const u64* __restrict__ Ms,
                                                   u32 nb1, u64 B, u32 gl, u32 G, u32 cap, u64* __restrict__ C,
-                                                  u64* __restrict__ lo_a, u8* __restrict__ ab_a, u32* small) {
+                                                  u64* __restrict__ lo_a, u8* __restrict__ ab_a, u32* small, u32 dts) {
     extern __shared__ __align__(16) unsigned char p2s[];
     const u32 gb = 1u << gl;
     u32* cnt = reinterpret_cast<u32*>(p2s);  // gb counts -> exclusive offsets
     u32* cur = cnt + gb;                     // gb write cursors
     u64* lo_s = reinterpret_cast<u64*>(p2s + ((8u * gb + 15u) & ~15u));
     u8* ab_s = reinterpret_cast<u8*>(lo_s + cap);
+    // (dts > 0: the duplicate check is fused here -- per warp an open-addressing set of indices
+    // into lo_s, dts entries, after the staged keys)
+    u32* dtab = reinterpret_cast<u32*>(p2s + ((((8u * gb + 15u) & ~15u) + (size_t)cap * 9 + 15u) & ~(size_t)15u)) +
+                (threadIdx.x >> 5) * dts;
+    bool rep = false;
+    u32 zeros = 0;
     for (u32 grp = blockIdx.x; grp < G; grp += gridDim.x) {
         const u64 gs = Ms[(u64)grp * nb1], ge = Ms[(u64)(grp + 1) * nb1];  // (Ms[G * nb1] = n)
         const u64 b0 = (u64)grp << gl;
@@ -557,6 +563,37 @@ __global__ void __launch_bounds__(512) k_p2_group(const u64* __restrict__ key1, 
             lo_a[gs + i] = lo_s[i];
             ab_a[gs + i] = ab_s[i];
         }
+        if (dts) {  // A2 duplicate check: equal keys have equal lo (R2) and share a bucket
+            const u32 lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+            for (u32 j = threadIdx.x >> 5; j < nb; j += nw) {
+                const u32 b0 = cnt[j], b1 = j + 1 < gb ? cnt[j + 1] : cg;
+                if (b1 - b0 < 2) continue;
+                for (u32 t = lane; t < dts; t += 32) dtab[t] = 0xffffffffu;
+                __syncwarp();
+                for (u32 i = b0 + lane; i < b1; i += 32) {
+                    const u64 v = lo_s[i];
+                    if (v == 0) {  // (0 is not special here, but counted like k_dedupe does)
+                        ++zeros;
+                        continue;
+                    }
+                    u32 slot = (u32)(v ^ (v >> 32)) & (dts - 1);
+                    for (;;) {
+                        const u32 old = atomicCAS(dtab + slot, 0xffffffffu, i);
+                        if (old == 0xffffffffu) break;
+                        if (lo_s[old] == v) {
+                            rep = true;
+                            break;
+                        }
+                        slot = (slot + 1) & (dts - 1);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+    if (dts) {
+        if (rep) atomicOr(small + 2, 1u);
+        if (zeros) atomicAdd(small + 3, zeros);
     }
 }
 
@@ -598,13 +635,14 @@ void launch_p2_scatter(const u64* keys, u64 n, u64 g, u64 B, const P2Shape& sh, 
 }
 
 void launch_p2_group(const u64* key1, u64 g, u64 B, const P2Shape& sh, const u64* Ms, u64* C, u64* lo_a, u8* ab_a,
-                     u32* small, cudaStream_t st) {
-    const size_t smem = ((8u * (1u << sh.gl) + 15u) & ~15u) + (size_t)sh.cap * 9;
+                     u32* small, cudaStream_t st, u32 dts) {
+    const size_t smem = ((((8u * (1u << sh.gl) + 15u) & ~15u) + (size_t)sh.cap * 9 + 15u) & ~(size_t)15u) +
+                        (size_t)dts * 4 * (512 / 32);
     cudaFuncSetAttribute(k_p2_group, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2_group, 512, smem);
     const unsigned grid = (unsigned)std::max<u64>(1, std::min<u64>(sh.G, 148ull * std::max(occ, 1)));
-    k_p2_group<<<grid, 512, smem, st>>>(key1, g, Ms, sh.nb1, B, sh.gl, sh.G, sh.cap, C, lo_a, ab_a, small);
+    k_p2_group<<<grid, 512, smem, st>>>(key1, g, Ms, sh.nb1, B, sh.gl, sh.G, sh.cap, C, lo_a, ab_a, small, dts);
     g_launches++;
 }
 

@@ -1199,9 +1199,17 @@ bool enqueue_single(const uint64_t* d_keys, const BuildParams& p, cudaStream_t s
             R.hash_argc.push_back(kP2ScatterParams);
             R.hash_off.push_back(0);
         }
-        launch_p2_group(key1, p.g, B, p2, Ms, C, lo_a, ab_a, small, st);
+        // the duplicate check fused into level 2 when its per-warp tables are small (size bound
+        // S <= 512: 16 warps x 2 KB); else the separate pass
+        static const int fdd_env = getenv("RS_FUSED_DEDUPE") ? atoi(getenv("RS_FUSED_DEDUPE")) : 1;
+        uint32_t dts = 0;
+        if (fdd_env && !tree && S <= 512) {
+            dts = 64;
+            while (dts < 2 * S) dts <<= 1;
+        }
+        launch_p2_group(key1, p.g, B, p2, Ms, C, lo_a, ab_a, small, st, dts);
         CKL();
-        if (!tree) {  // (tree: each warp checks its own bucket)
+        if (!tree && !dts) {  // (tree: each warp checks its own bucket)
             launch_dedupe(lo_a, C, B, S, small + 2, nullptr, st);
             CKL();
         }

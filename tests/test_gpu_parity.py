@@ -213,6 +213,28 @@ def test_duplicate_keys_rejected():
     assert e.value.code == rs.E_DUPLICATE
 
 
+@pytest.mark.parametrize("leaf,b,n", [(8, 100, 30_000), (12, 1000, 40_000), (16, 2000, 20_000)])
+def test_duplicate_check_paths(leaf, b, n):
+    """The duplicate check in each partition path (fused into the two-level sort for size bounds
+    <= 512, the separate pass above): a repeated key anywhere is rejected, also in a replayed
+    build; the one key whose lo word is 0 (lo = remix(key ^ salt), remix(0) = 0: key = the salt)
+    is an ordinary key once -- bytes equal the oracle's -- and a duplicate twice."""
+    salt_lo = np.uint64(0xC2B2AE3D27D4EB4F)
+    keys = synth.keys(n, 70 + leaf)
+    keys = keys[keys != salt_lo]
+    keys[n // 3] = salt_lo
+    want = oracle.build(keys, leaf, b, threads=os.cpu_count())
+    for _ in range(3):  # (uncaptured, captured, replayed)
+        assert rs.build(keys, leaf, b) == want
+    for i, j in [(5, n // 2), (5, n // 3)]:  # (a plain repeat; the lo == 0 key twice)
+        bad = keys.copy()
+        bad[i] = bad[j]
+        for _ in range(2):
+            with pytest.raises(rs.RecSplitError) as e:
+                rs.build(bad, leaf, b)
+            assert e.value.code == rs.E_DUPLICATE
+
+
 @pytest.mark.parametrize("leaf,b,n", [(8, 20_000, 30_000), (16, 12_000, 30_000), (5, 9_000, 60_000),
                                       (12, 10_000, 25_000), (3, 8_500, 17_000)])
 def test_oversized_buckets_full_parity(leaf, b, n):
@@ -828,7 +850,8 @@ for rf in (True, False):
 
 
 @pytest.mark.parametrize("env", ["RS_SUB_LEAF=1", "RS_FIT_LUT=0", "RS_LEAN=0", "RS_P2=0", "RS_GRAPH=0",
-                                 "RS_SUB_LEAF=1,RS_FIT_LUT=0", "RS_UPPER_KP=0", "RS_UPPER_KP_VAR=100000"])
+                                 "RS_SUB_LEAF=1,RS_FIT_LUT=0", "RS_UPPER_KP=0", "RS_UPPER_KP_VAR=100000",
+                                 "RS_FUSED_DEDUPE=0"])
 def test_engine_knobs_do_not_change_output(env):
     """Every engine variant of round 2's small-configuration work gives the oracle's bytes:
     the sub-warp leaf kernel (k_leaf_sub: four leaves of <= 8 keys per warp, prefetched),
