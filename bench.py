@@ -15,7 +15,10 @@ e2e        the same metric through recsplit_build with HOST keys (pinned), H2D a
            the result D2H inside the timed region (host wall clock around the call).
 roofline   dominant kernel = the lower-level-1 split search (62% of the work at C3):
            algorithmic remix evaluations (sum over nodes of (minimal seed + 1) x keys)
-           / that kernel's CUDA-event duration, against the INT32-pipe peak.
+           / that kernel's CUDA-event duration, against the INT32-pipe peak (DESIGN.md 7);
+           at N > 1 from one extra single-GPU build of rank 0's key slice (the sharded build
+           returns no per-kernel events).  Single-GPU builds of a configuration replay a
+           captured CUDA graph after the first two (warm-up) builds.
 cpu_baseline / --impl reference: the plain C oracle, as it stands, on this host's cores,
            on a bounded sample of the same workload (whole buckets).
 """
