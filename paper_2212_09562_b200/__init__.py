@@ -612,28 +612,51 @@ def build_sharded(keys_tensor, leaf_size: int, bucket_size: int, rotation_fittin
     balance=True: contiguous bucket ranges of about equal expected work (bucket-size
     histogram -> recsplit_balanced_cuts; one extra allreduce of B int32 when distributed);
     False: equal bucket counts.  The output bytes are the same either way."""
+    import os
+    import time
+
     import torch.distributed as dist
+
+    trace = os.environ.get("RS_TRACE_SHARDED")  # (development: stage wall times to stderr)
+    marks = [("start", time.perf_counter())]
+
+    def mark(name):
+        if trace:
+            marks.append((name, time.perf_counter()))
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     total = allreduce_sum(keys_tensor.numel(), group) if distribute else keys_tensor.numel()
     cuts = None
     if balance and world > 1:
         hist = global_histogram(keys_tensor, total, bucket_size, global_seed, group, stream, distribute)
+        mark("histogram")
         cuts = balanced_cuts(hist, leaf_size, world, rotation_fitting)
+        mark("cuts")
     if distribute:
         routed, counts = route_keys(keys_tensor, total, bucket_size, world, global_seed, stream, cuts)
+        mark("route")
         keys_tensor = exchange_keys(routed, counts, group)
+        mark("exchange")
         del routed
     sh = Shard(keys_tensor, leaf_size, bucket_size, rank, world, rotation_fitting, global_seed, stream,
                total if distribute else 0, cuts)
+    mark("shard")
     try:
         allsum = exchange_summaries(sh.summary, group)
         step = allreduce_min(sh.min_step(allsum), group)
         part = sh.finish(step)
+        mark("finish")
     finally:
         sh.close()
     parts = gather_parts(part, 0, group)
-    return stitch(parts) if parts is not None else None
+    mark("gather")
+    out = stitch(parts) if parts is not None else None
+    mark("stitch")
+    if trace:
+        import sys
+        print(f"[rank {rank}] build_sharded ms: " + ", ".join(
+            f"{n} {1e3 * (t - marks[i][1]):.2f}" for i, (n, t) in enumerate(marks[1:])), file=sys.stderr, flush=True)
+    return out
 
 
 def trim() -> None:
